@@ -1,0 +1,140 @@
+/*
+ * hegwas_b200.h -- C-ABI of the B200 (sm_100a) evaluator for the power-of-two-modulus
+ * approximate HE scheme of arXiv 1902.04303 (reference package `hegwas`).
+ *
+ * Every entry point takes plain device pointers, sizes and a cudaStream_t passed as
+ * void*.  No torch types cross this boundary.  The Python host layer
+ * (paper_1902_04303_b200/) binds these with ctypes; a maintainer of the reference would
+ * bind the same symbols.
+ *
+ * Polynomial layout ("limb-major"): a ring element of Z_{2^bits}[x]/(x^N+1) is stored as
+ * W = ceil(bits/32) arrays of N uint32 words, word w of coefficient j at p[w*N + j]
+ * (little-endian radix 2^32).  Canonical representatives are in [0, 2^bits) with the
+ * top word masked, exactly like ring.RingElement (reference ring.py:68-85).
+ *
+ * An operand descriptor (hg_operand) additionally says how to read the value:
+ *   signed_rep = 0 : unsigned integer of `bits` bits (canonical residue),
+ *   signed_rep = 1 : two's complement integer of `bits` bits (centered representative).
+ * Products mod 2^k do not depend on the representative when k <= bits of the operand
+ * (SURVEY §8a R3), so the host picks the narrowest legal view.
+ *
+ * Status codes: 0 = HG_OK, otherwise an HG_E* value; hg_last_error() returns a
+ * thread-local message.  The library never silently falls back to the CPU.
+ */
+#ifndef HEGWAS_B200_H
+#define HEGWAS_B200_H
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HG_OK 0
+#define HG_EINVAL 1      /* bad argument (maps to ParameterError on the Python side) */
+#define HG_ENOMEM 2      /* device allocation failed */
+#define HG_ECUDA 3       /* CUDA runtime error */
+#define HG_ERANGE 4      /* product too wide for the NTT prime basis */
+
+typedef struct hg_ctx hg_ctx;
+typedef struct hg_key hg_key;
+
+typedef struct hg_operand {
+    const uint32_t* words;  /* device pointer, [W][N] */
+    int32_t bits;           /* value width (W = ceil(bits/32) words are read) */
+    int32_t signed_rep;     /* 0 unsigned, 1 two's complement */
+} hg_operand;
+
+/* ---- library / context ------------------------------------------------------------ */
+const char* hg_last_error(void);
+int hg_version(void);
+/* Context for ring degree N = 2^log_n (2 <= log_n <= 17): NTT prime basis
+ * (30-bit primes p = 1 mod 2^18), twiddles, base-conversion tables.  Replaces the
+ * implicit CPython/gmpy2 big-int engine behind ring.negacyclic_mul (ring.py:61-65). */
+int hg_ctx_create(int log_n, int device, hg_ctx** out);
+int hg_ctx_destroy(hg_ctx* ctx);
+/* Largest exact product width (bits) the prime basis supports. */
+int hg_ctx_max_product_bits(const hg_ctx* ctx);
+int hg_ctx_num_primes(const hg_ctx* ctx);
+/* Copy the prime list (host array of length hg_ctx_num_primes). */
+int hg_ctx_primes(const hg_ctx* ctx, uint32_t* out);
+int hg_sync(hg_ctx* ctx, void* stream);
+
+/* ---- elementwise ring ops (ring.py:114-196) ---------------------------------------- */
+/* out = a + b mod 2^bits                                     RingElement.add  ring.py:114 */
+int hg_poly_add(hg_ctx* ctx, uint32_t* out, const uint32_t* a, const uint32_t* b,
+                int bits, void* stream);
+/* out = a - b mod 2^bits                                     RingElement.sub  ring.py:123 */
+int hg_poly_sub(hg_ctx* ctx, uint32_t* out, const uint32_t* a, const uint32_t* b,
+                int bits, void* stream);
+/* out = -a mod 2^bits                                        RingElement.neg  ring.py:132 */
+int hg_poly_neg(hg_ctx* ctx, uint32_t* out, const uint32_t* a, int bits, void* stream);
+/* out = a * k mod 2^bits; k given as (k mod 2^bits) in kw host words (kw <= W)
+ *                                                     RingElement.scalar_mul  ring.py:136 */
+int hg_poly_scalar_mul(hg_ctx* ctx, uint32_t* out, const uint32_t* a, int bits,
+                       const uint32_t* k_words_host, int kw, void* stream);
+/* out (out_bits) = a mod 2^out_bits, a has in_bits >= out_bits  RingElement.reduce_to  ring.py:168 */
+int hg_poly_reduce_to(hg_ctx* ctx, uint32_t* out, int out_bits, const uint32_t* a,
+                      int in_bits, void* stream);
+/* out (out_bits) = centered(a) mod 2^out_bits (sign-extend)  lift_centered_to  ring.py:177 */
+int hg_poly_lift_centered(hg_ctx* ctx, uint32_t* out, int out_bits, const uint32_t* a,
+                          int in_bits, void* stream);
+/* out (out_bits) = ((a + 2^(shift-1)) >> shift) mod 2^out_bits   divide_round  ring.py:184 */
+int hg_poly_divide_round(hg_ctx* ctx, uint32_t* out, int out_bits, const uint32_t* a,
+                         int in_bits, int shift, void* stream);
+/* out = a(x^k) mod (x^N+1), k odd                       RingElement.automorphism  ring.py:152 */
+int hg_poly_automorphism(hg_ctx* ctx, uint32_t* out, const uint32_t* a, int bits,
+                         int64_t k, void* stream);
+
+/* ---- exact negacyclic product ------------------------------------------------------ */
+/* out (out_bits) = (a * b) mod 2^out_bits, exact negacyclic convolution of the two
+ * operand values.  Replaces RingElement.mul / mul_mod (ring.py:140-150), i.e.
+ * negacyclic_mul + mask (ring.py:46-65).                                               */
+int hg_poly_mul(hg_ctx* ctx, uint32_t* out, int out_bits, hg_operand a, hg_operand b,
+                void* stream);
+/* Same, for the ciphertext tensor of ckks.mult (ckks.py:176-178):
+ *   d0 = a0*b0, d1 = a0*b1 + a1*b0, d2 = a1*b1   (all mod 2^out_bits).               */
+int hg_poly_tensor(hg_ctx* ctx, uint32_t* d0, uint32_t* d1, uint32_t* d2, int out_bits,
+                   hg_operand a0, hg_operand a1, hg_operand b0, hg_operand b1, void* stream);
+
+/* ---- key switching (ckks._keyswitch, ckks.py:187-194) ------------------------------ */
+/* Prepare a switching key (b, a) (device, key_bits each) for inputs at `level`:
+ * reduce to level+big_l bits, convert to the NTT/RNS domain and keep it resident. */
+int hg_key_prepare(hg_ctx* ctx, const uint32_t* kb, const uint32_t* ka, int key_bits,
+                   int level, int big_l, void* stream, hg_key** out);
+int hg_key_destroy(hg_key* key);
+size_t hg_key_device_bytes(const hg_key* key);
+/* (out0, out1) = (round(x*kb / 2^L), round(x*ka / 2^L)) mod 2^level, x canonical
+ * (level bits).  If automorph_k != 1, x is first mapped by x -> x(X^k) (fused
+ * _apply_automorphism, ckks.py:247-253).                                                */
+int hg_keyswitch(hg_ctx* ctx, const hg_key* key, const uint32_t* x, int64_t automorph_k,
+                 uint32_t* out0, uint32_t* out1, void* stream);
+
+/* ---- fused scheme ops --------------------------------------------------------------- */
+/* HeEngine.mult (ckks.py:310-313): tensor, relinearise with evk prepared at `level`,
+ * add, rescale by rescale_bits.  Inputs canonical at `level`; outputs at
+ * level - rescale_bits.  (rescale_bits = 0 skips the rescale.)                         */
+int hg_ct_mult(hg_ctx* ctx, const hg_key* evk, const uint32_t* a0, const uint32_t* a1,
+               const uint32_t* b0, const uint32_t* b1, int level, int rescale_bits,
+               uint32_t* out0, uint32_t* out1, void* stream);
+/* _apply_automorphism (ckks.py:247-253): out = (phi_k(c0) + e0, e1), (e0, e1) =
+ * keyswitch(phi_k(c1)).  Used by rotate (ckks.py:256-273) and conjugate (:276-279). */
+int hg_ct_automorph(hg_ctx* ctx, const hg_key* key, const uint32_t* c0, const uint32_t* c1,
+                    int level, int64_t k, uint32_t* out0, uint32_t* out1, void* stream);
+
+/* ---- microbenchmarks / measurement ------------------------------------------------ */
+/* Batched forward+inverse negacyclic NTT over `count` length-N rows of residues
+ * (prime i % num_primes for row i); data is [count][N] uint32 on device.            */
+int hg_ntt_forward(hg_ctx* ctx, uint32_t* data, int count, int prime_offset, void* stream);
+int hg_ntt_inverse(hg_ctx* ctx, uint32_t* data, int count, int prime_offset, void* stream);
+/* Integer-pipe peak microbenchmark: runs the NTT butterfly modmul sequence register-
+ * resident on all SMs; returns butterflies executed (host) for `iters`.              */
+int hg_bench_modmul(hg_ctx* ctx, int iters, uint32_t* sink, double* ops_out, void* stream);
+/* Number of kernel launches issued by this library since context creation. */
+long long hg_launch_count(const hg_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HEGWAS_B200_H */

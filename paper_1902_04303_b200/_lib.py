@@ -1,0 +1,166 @@
+"""ctypes binding of libhegwas_b200.so (the C-ABI in include/hegwas_b200.h).
+
+There is no CPU fallback: if the shared library is missing or no CUDA device is
+present, every device operation raises.  Build the library with
+``python -c "import __graft_entry__ as g; g.build()"`` (or ``make -C
+paper_1902_04303_b200/csrc``).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from .errors import HegwasError, ParameterError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhegwas_b200.so")
+
+HG_OK = 0
+HG_EINVAL = 1
+HG_ENOMEM = 2
+HG_ECUDA = 3
+HG_ERANGE = 4
+
+
+class DeviceError(HegwasError):
+    """CUDA failure or missing native library (never silently falls back)."""
+
+
+class Operand(ctypes.Structure):
+    _fields_ = [("words", ctypes.c_void_p), ("bits", ctypes.c_int32), ("signed_rep", ctypes.c_int32)]
+
+
+_u32p = ctypes.POINTER(ctypes.c_uint32)
+_vp = ctypes.c_void_p
+_i = ctypes.c_int
+_i64 = ctypes.c_int64
+
+# name -> (restype, argtypes)
+SIGNATURES = {
+    "hg_last_error": (ctypes.c_char_p, []),
+    "hg_version": (_i, []),
+    "hg_ctx_create": (_i, [_i, _i, ctypes.POINTER(_vp)]),
+    "hg_ctx_destroy": (_i, [_vp]),
+    "hg_ctx_max_product_bits": (_i, [_vp]),
+    "hg_ctx_num_primes": (_i, [_vp]),
+    "hg_ctx_primes": (_i, [_vp, _u32p]),
+    "hg_sync": (_i, [_vp, _vp]),
+    "hg_poly_add": (_i, [_vp, _vp, _vp, _vp, _i, _vp]),
+    "hg_poly_sub": (_i, [_vp, _vp, _vp, _vp, _i, _vp]),
+    "hg_poly_neg": (_i, [_vp, _vp, _vp, _i, _vp]),
+    "hg_poly_scalar_mul": (_i, [_vp, _vp, _vp, _i, _u32p, _i, _vp]),
+    "hg_poly_reduce_to": (_i, [_vp, _vp, _i, _vp, _i, _vp]),
+    "hg_poly_lift_centered": (_i, [_vp, _vp, _i, _vp, _i, _vp]),
+    "hg_poly_divide_round": (_i, [_vp, _vp, _i, _vp, _i, _i, _vp]),
+    "hg_poly_automorphism": (_i, [_vp, _vp, _vp, _i, _i64, _vp]),
+    "hg_poly_mul": (_i, [_vp, _vp, _i, Operand, Operand, _vp]),
+    "hg_poly_tensor": (_i, [_vp, _vp, _vp, _vp, _i, Operand, Operand, Operand, Operand, _vp]),
+    "hg_key_prepare": (_i, [_vp, _vp, _vp, _i, _i, _i, _vp, ctypes.POINTER(_vp)]),
+    "hg_key_destroy": (_i, [_vp]),
+    "hg_key_device_bytes": (ctypes.c_size_t, [_vp]),
+    "hg_keyswitch": (_i, [_vp, _vp, _vp, _i64, _vp, _vp, _vp]),
+    "hg_ct_mult": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _vp, _vp, _vp]),
+    "hg_ct_automorph": (_i, [_vp, _vp, _vp, _vp, _i, _i64, _vp, _vp, _vp]),
+    "hg_ntt_forward": (_i, [_vp, _vp, _i, _i, _vp]),
+    "hg_ntt_inverse": (_i, [_vp, _vp, _i, _i, _vp]),
+    "hg_bench_modmul": (_i, [_vp, _i, _vp, ctypes.POINTER(ctypes.c_double), _vp]),
+    "hg_launch_count": (ctypes.c_longlong, [_vp]),
+}
+
+_lib = None
+_lock = threading.RLock()
+
+
+def load_library(path: str = LIB_PATH):
+    """Load and type the shared library (no CUDA calls are made)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise DeviceError(
+                f"native library {path} not built; run __graft_entry__.build() "
+                "(there is no CPU fallback)"
+            )
+        lib = ctypes.CDLL(path)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def check(rc: int):
+    if rc == HG_OK:
+        return
+    msg = load_library().hg_last_error().decode(errors="replace")
+    if rc in (HG_EINVAL, HG_ERANGE):
+        raise ParameterError(msg)
+    raise DeviceError(f"native error {rc}: {msg}")
+
+
+def operand(words, bits: int, signed: bool) -> Operand:
+    return Operand(ctypes.c_void_p(words.data_ptr()), int(bits), 1 if signed else 0)
+
+
+class Context:
+    """One native context per (log_n, device): prime basis, twiddles, CRT tables."""
+
+    def __init__(self, log_n: int, device: int):
+        import torch
+
+        if not torch.cuda.is_available():
+            raise DeviceError("no CUDA device: the B200 evaluator has no CPU fallback")
+        self.lib = load_library()
+        self.log_n = log_n
+        self.device = device
+        handle = ctypes.c_void_p()
+        with torch.cuda.device(device):
+            check(self.lib.hg_ctx_create(log_n, device, ctypes.byref(handle)))
+        self.handle = handle
+
+    def stream(self):
+        import torch
+
+        return ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def primes(self) -> list[int]:
+        n = self.lib.hg_ctx_num_primes(self.handle)
+        arr = (ctypes.c_uint32 * n)()
+        check(self.lib.hg_ctx_primes(self.handle, arr))
+        return list(arr)
+
+    def launches(self) -> int:
+        return int(self.lib.hg_launch_count(self.handle))
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown ordering
+        try:
+            if self.handle:
+                self.lib.hg_ctx_destroy(self.handle)
+        except Exception:
+            pass
+
+
+_contexts: dict[tuple[int, int], Context] = {}
+
+
+def get_context(log_n: int, device: int | None = None) -> Context:
+    import torch
+
+    if device is None:
+        device = torch.cuda.current_device() if torch.cuda.is_available() else 0
+    key = (log_n, device)
+    ctx = _contexts.get(key)
+    if ctx is None:
+        with _lock:
+            ctx = _contexts.get(key)
+            if ctx is None:
+                ctx = Context(log_n, device)
+                _contexts[key] = ctx
+    return ctx
+
+
+def total_launches() -> int:
+    return sum(c.launches() for c in _contexts.values())

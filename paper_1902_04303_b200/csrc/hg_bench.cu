@@ -1,0 +1,49 @@
+// hg_bench.cu -- integer-pipe roofline probe: the exact lazy Harvey butterfly (Shoup
+// modmul + add/sub) the NTT kernels execute, register resident, 8 independent chains per
+// thread, enough CTAs to fill all SMs.  The measured butterflies/s is the integer-pipe
+// "peak" that NTT kernel throughput is reported against (MEASURED_PEAKS.json has no
+// integer figure).
+#include "hg_internal.cuh"
+
+namespace {
+
+__global__ void __launch_bounds__(256) modmul_probe_kernel(int iters, uint32_t p, uint32_t w,
+                                                           uint32_t wsh, uint32_t* sink) {
+    uint32_t x[8], y[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        x[k] = (threadIdx.x * 2654435761u + k * 40503u) % p;
+        y[k] = (blockIdx.x * 97u + k * 7919u + threadIdx.x) % p;
+    }
+    const uint32_t p2 = p << 1;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            uint32_t a = x[k] >= p2 ? x[k] - p2 : x[k];
+            uint32_t t = mul_shoup_lazy(y[k], w, wsh, p);
+            x[k] = a + t;
+            y[k] = a - t + p2;
+        }
+    }
+    uint32_t acc = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc ^= x[k] ^ y[k];
+    if (acc == 0x12345678u) sink[0] = acc;  // keep the chains live
+}
+
+}  // namespace
+
+extern "C" int hg_bench_modmul(hg_ctx* ctx, int iters, uint32_t* sink, double* ops_out,
+                               void* stream) {
+    if (!ctx || !sink || iters < 1) return hg_fail(HG_EINVAL, "hg_bench_modmul: bad arguments");
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+    const int blocks = sms * 8, threads = 256;
+    uint32_t p = ctx->primes[0];
+    uint32_t w = 123456789u % p;
+    uint32_t wsh = (uint32_t)(((uint64_t)w << 32) / p);
+    modmul_probe_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(iters, p, w, wsh, sink);
+    HG_LAUNCH_CHECK(ctx);
+    if (ops_out) *ops_out = (double)blocks * threads * 8.0 * iters;
+    return HG_OK;
+}

@@ -1,0 +1,290 @@
+// hg_context.cu -- context creation: NTT prime basis, twiddles, base-conversion and CRT
+// tables.  Host-side set-up only; kernels live in hg_ntt.cu / hg_rns.cu / hg_elementwise.cu.
+#include "hg_internal.cuh"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+
+static thread_local std::string g_last_error;
+
+void hg_set_error(const std::string& msg) { g_last_error = msg; }
+int hg_fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+extern "C" const char* hg_last_error(void) { return g_last_error.c_str(); }
+extern "C" int hg_version(void) { return 1; }
+
+// ---- 32-bit number theory (host) -------------------------------------------------------
+static uint64_t mulmod64(uint64_t a, uint64_t b, uint64_t m) { return (a * b) % m; }
+static uint64_t powmod(uint64_t b, uint64_t e, uint64_t m) {
+    uint64_t r = 1 % m;
+    b %= m;
+    while (e) {
+        if (e & 1) r = mulmod64(r, b, m);
+        b = mulmod64(b, b, m);
+        e >>= 1;
+    }
+    return r;
+}
+static bool is_prime_u32(uint32_t n) {
+    if (n < 2) return false;
+    for (uint32_t sp : {2u, 3u, 5u, 7u, 11u, 13u}) {
+        if (n % sp == 0) return n == sp;
+    }
+    uint32_t d = n - 1;
+    int s = 0;
+    while ((d & 1) == 0) { d >>= 1; ++s; }
+    for (uint32_t a : {2u, 7u, 61u}) {
+        uint64_t x = powmod(a, d, n);
+        if (x == 1 || x == n - 1) continue;
+        bool comp = true;
+        for (int r = 1; r < s; ++r) {
+            x = mulmod64(x, x, n);
+            if (x == n - 1) { comp = false; break; }
+        }
+        if (comp) return false;
+    }
+    return true;
+}
+static uint32_t shoup_of(uint32_t w, uint32_t p) {
+    return (uint32_t)(((uint64_t)w << 32) / p);
+}
+static uint32_t bitrev(uint32_t x, int bits) {
+    uint32_t r = 0;
+    for (int i = 0; i < bits; ++i) { r = (r << 1) | (x & 1); x >>= 1; }
+    return r;
+}
+
+// ---- context ----------------------------------------------------------------------------
+extern "C" int hg_ctx_create(int log_n, int device, hg_ctx** out) {
+    if (!out) return hg_fail(HG_EINVAL, "null output pointer");
+    if (log_n < 2 || log_n > HG_PRIME_SHIFT - 1)
+        return hg_fail(HG_EINVAL, "log_n must be in [2, 17] for the 30-bit NTT prime basis");
+    HG_CUDA_TRY(cudaSetDevice(device));
+    hg_ctx* ctx = new hg_ctx();
+    ctx->log_n = log_n;
+    ctx->N = 1 << log_n;
+    ctx->device = device;
+    // primes p = k * 2^18 + 1 < 2^30, descending
+    for (uint64_t k = ((1ull << 30) - 2) >> HG_PRIME_SHIFT; k >= 1 && ctx->primes.size() < HG_MAX_PRIMES; --k) {
+        uint64_t p = (k << HG_PRIME_SHIFT) + 1;
+        if (p >= (1ull << 30)) continue;
+        if (p < (1ull << 26)) break;
+        if (is_prime_u32((uint32_t)p)) ctx->primes.push_back((uint32_t)p);
+    }
+    ctx->nprimes = (int)ctx->primes.size();
+    ctx->prefix_bits.assign(ctx->nprimes + 1, 0.0);
+    for (int j = 0; j < ctx->nprimes; ++j)
+        ctx->prefix_bits[j + 1] = ctx->prefix_bits[j] + std::log2((double)ctx->primes[j]);
+
+    std::vector<PrimeInfo> pinfo(ctx->nprimes);
+    std::vector<uint32_t> modup((size_t)ctx->nprimes * HG_MODUP_WMAX);
+    for (int j = 0; j < ctx->nprimes; ++j) {
+        uint32_t p = ctx->primes[j];
+        PrimeInfo& pi = pinfo[j];
+        pi.p = p;
+        // -p^{-1} mod 2^32 by Newton iteration
+        uint32_t inv = p;  // correct to 3 bits for odd p
+        for (int it = 0; it < 5; ++it) inv *= 2u - p * inv;
+        pi.pinv_neg = (uint32_t)(0u - inv);
+        pi.c32 = (uint32_t)((1ull << 32) % p);
+        pi.c30 = (uint32_t)((1ull << 30) % p);
+        pi.c30_sh = shoup_of(pi.c30, p);
+        pi.ninv = (uint32_t)powmod(ctx->N, p - 2, p);
+        pi.ninv_sh = shoup_of(pi.ninv, p);
+        pi.pad = 0;
+        uint64_t v = 1;
+        for (int w = 0; w < HG_MODUP_WMAX; ++w) {
+            modup[(size_t)j * HG_MODUP_WMAX + w] = (uint32_t)v;
+            v = mulmod64(v, pi.c32, p);
+        }
+    }
+    size_t tw_bytes = (size_t)ctx->nprimes * ctx->N * sizeof(uint32_t);
+    if (cudaMalloc(&ctx->d_pinfo, sizeof(PrimeInfo) * ctx->nprimes) != cudaSuccess ||
+        cudaMalloc(&ctx->d_modup, modup.size() * sizeof(uint32_t)) != cudaSuccess ||
+        cudaMalloc(&ctx->d_psi, tw_bytes) != cudaSuccess ||
+        cudaMalloc(&ctx->d_psi_sh, tw_bytes) != cudaSuccess ||
+        cudaMalloc(&ctx->d_ipsi, tw_bytes) != cudaSuccess ||
+        cudaMalloc(&ctx->d_ipsi_sh, tw_bytes) != cudaSuccess) {
+        hg_ctx_destroy(ctx);
+        return hg_fail(HG_ENOMEM, "context allocation failed");
+    }
+    cudaMemcpy(ctx->d_pinfo, pinfo.data(), sizeof(PrimeInfo) * ctx->nprimes, cudaMemcpyHostToDevice);
+    cudaMemcpy(ctx->d_modup, modup.data(), modup.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
+    // keep freed stream-ordered allocations cached in the pool (residue scratch is reused
+    // every op; returning it to the driver would serialise on cudaFree)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        hg_ctx_destroy(ctx);
+        return hg_fail(HG_ECUDA, std::string("context upload: ") + cudaGetErrorString(e));
+    }
+    *out = ctx;
+    return HG_OK;
+}
+
+extern "C" int hg_ctx_destroy(hg_ctx* ctx) {
+    if (!ctx) return HG_OK;
+    cudaFree(ctx->d_pinfo);
+    cudaFree(ctx->d_modup);
+    cudaFree(ctx->d_psi);
+    cudaFree(ctx->d_psi_sh);
+    cudaFree(ctx->d_ipsi);
+    cudaFree(ctx->d_ipsi_sh);
+    for (auto& kv : ctx->crt) {
+        cudaFree(kv.second.d_M);
+        cudaFree(kv.second.d_negQ);
+        cudaFree(kv.second.d_cinv);
+        cudaFree(kv.second.d_cinv_sh);
+        cudaFree(kv.second.d_invp);
+    }
+    delete ctx;
+    return HG_OK;
+}
+
+extern "C" int hg_ctx_max_product_bits(const hg_ctx* ctx) {
+    return ctx ? (int)std::floor(ctx->prefix_bits[ctx->nprimes]) : 0;
+}
+extern "C" int hg_ctx_num_primes(const hg_ctx* ctx) { return ctx ? ctx->nprimes : 0; }
+extern "C" int hg_ctx_primes(const hg_ctx* ctx, uint32_t* out) {
+    if (!ctx || !out) return hg_fail(HG_EINVAL, "null argument");
+    std::memcpy(out, ctx->primes.data(), ctx->primes.size() * sizeof(uint32_t));
+    return HG_OK;
+}
+extern "C" long long hg_launch_count(const hg_ctx* ctx) { return ctx ? ctx->launches.load() : 0; }
+
+extern "C" int hg_sync(hg_ctx* ctx, void* stream) {
+    (void)ctx;
+    HG_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+    return HG_OK;
+}
+
+int hg_primes_for_bits(const hg_ctx* ctx, double bits) {
+    for (int P = 1; P <= ctx->nprimes; ++P)
+        if (ctx->prefix_bits[P] >= bits) return P;
+    return -1;
+}
+
+// ---- twiddles ----------------------------------------------------------------------------
+// psi_rev[k] = psi^bitrev(k), ipsi_rev[k] = psi^-bitrev(k) for a primitive 2N-th root psi
+// (merged negacyclic Cooley-Tukey forward / Gentleman-Sande inverse).
+int hg_ensure_twiddles(hg_ctx* ctx, int P) {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (P <= ctx->tw_ready) return HG_OK;
+    const int N = ctx->N, logn = ctx->log_n;
+    int j0 = ctx->tw_ready;
+    size_t cnt = (size_t)(P - j0) * N;
+    std::vector<uint32_t> psi(cnt), psi_sh(cnt), ipsi(cnt), ipsi_sh(cnt), pw(N);
+    for (int j = j0; j < P; ++j) {
+        uint32_t p = ctx->primes[j];
+        uint64_t root = 0;
+        for (uint64_t g = 2; g < p; ++g) {
+            uint64_t cand = powmod(g, (p - 1) / (2ull * N), p);
+            if (powmod(cand, N, p) == p - 1) { root = cand; break; }
+        }
+        if (!root) return hg_fail(HG_EINVAL, "no primitive 2N-th root");
+        uint64_t v = 1;
+        for (int i = 0; i < N; ++i) { pw[i] = (uint32_t)v; v = mulmod64(v, root, p); }
+        size_t base = (size_t)(j - j0) * N;
+        for (int k = 0; k < N; ++k) {
+            uint32_t e = bitrev((uint32_t)k, logn);
+            uint32_t w = pw[e];
+            uint32_t iw = e == 0 ? 1u : (uint32_t)(p - pw[N - e]);  // psi^-e = -psi^(N-e)
+            psi[base + k] = w;
+            psi_sh[base + k] = shoup_of(w, p);
+            ipsi[base + k] = iw;
+            ipsi_sh[base + k] = shoup_of(iw, p);
+        }
+    }
+    size_t off = (size_t)j0 * N;
+    HG_CUDA_TRY(cudaMemcpy(ctx->d_psi + off, psi.data(), cnt * 4, cudaMemcpyHostToDevice));
+    HG_CUDA_TRY(cudaMemcpy(ctx->d_psi_sh + off, psi_sh.data(), cnt * 4, cudaMemcpyHostToDevice));
+    HG_CUDA_TRY(cudaMemcpy(ctx->d_ipsi + off, ipsi.data(), cnt * 4, cudaMemcpyHostToDevice));
+    HG_CUDA_TRY(cudaMemcpy(ctx->d_ipsi_sh + off, ipsi_sh.data(), cnt * 4, cudaMemcpyHostToDevice));
+    ctx->tw_ready = P;
+    return HG_OK;
+}
+
+// ---- CRT tables ---------------------------------------------------------------------------
+// multiply a little-endian word array (truncated to W words) by a 32-bit value in place
+static void mul_small_trunc(std::vector<uint32_t>& a, uint32_t m) {
+    uint64_t carry = 0;
+    for (size_t i = 0; i < a.size(); ++i) {
+        uint64_t t = (uint64_t)a[i] * m + carry;
+        a[i] = (uint32_t)t;
+        carry = t >> 32;
+    }
+}
+
+int hg_get_crt(hg_ctx* ctx, int P, const CrtTable** out) {
+    {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        auto it = ctx->crt.find(P);
+        if (it != ctx->crt.end()) { *out = &it->second; return HG_OK; }
+    }
+    CrtTable t;
+    t.P = P;
+    t.P4 = (P + 3) & ~3;
+    t.W = (int)std::ceil(ctx->prefix_bits[P] / 32.0) + 2;
+    if (t.W < HG_MODUP_WMAX) t.W = HG_MODUP_WMAX;  // any emitted window up to 6144 bits
+    const int W = t.W;
+    std::vector<uint32_t> M((size_t)W * t.P4, 0u), negQ(W, 0u), cinv(P), cinv_sh(P);
+    std::vector<double> invp(P);
+    // Q mod 2^(32W) and Q/p_j mod 2^(32W)
+    std::vector<uint32_t> Q(W, 0u);
+    Q[0] = 1;
+    for (int i = 0; i < P; ++i) mul_small_trunc(Q, ctx->primes[i]);
+    // negQ = 2^(32W) - Q
+    {
+        uint64_t borrow = 0;
+        for (int w = 0; w < W; ++w) {
+            uint64_t v = (uint64_t)0 - Q[w] - borrow;
+            negQ[w] = (uint32_t)v;
+            borrow = (Q[w] != 0 || borrow) ? 1 : 0;
+        }
+    }
+    for (int j = 0; j < P; ++j) {
+        std::vector<uint32_t> Qj(W, 0u);
+        Qj[0] = 1;
+        uint64_t qmodp = 1;
+        uint32_t pj = ctx->primes[j];
+        for (int i = 0; i < P; ++i) {
+            if (i == j) continue;
+            mul_small_trunc(Qj, ctx->primes[i]);
+            qmodp = mulmod64(qmodp, ctx->primes[i] % pj, pj);
+        }
+        for (int w = 0; w < W; ++w) M[(size_t)w * t.P4 + j] = Qj[w];
+        uint64_t inv = powmod(qmodp, pj - 2, pj);
+        uint64_t ninv = powmod(ctx->N % pj, pj - 2, pj);
+        uint64_t r32 = (1ull << 32) % pj;
+        uint64_t c = mulmod64(mulmod64(inv, ninv, pj), r32, pj);
+        cinv[j] = (uint32_t)c;
+        cinv_sh[j] = shoup_of((uint32_t)c, pj);
+        invp[j] = 1.0 / (double)pj;
+    }
+    HG_CUDA_TRY(cudaMalloc(&t.d_M, M.size() * 4));
+    HG_CUDA_TRY(cudaMalloc(&t.d_negQ, negQ.size() * 4));
+    HG_CUDA_TRY(cudaMalloc(&t.d_cinv, P * 4));
+    HG_CUDA_TRY(cudaMalloc(&t.d_cinv_sh, P * 4));
+    HG_CUDA_TRY(cudaMalloc(&t.d_invp, P * 8));
+    HG_CUDA_TRY(cudaMemcpy(t.d_M, M.data(), M.size() * 4, cudaMemcpyHostToDevice));
+    HG_CUDA_TRY(cudaMemcpy(t.d_negQ, negQ.data(), negQ.size() * 4, cudaMemcpyHostToDevice));
+    HG_CUDA_TRY(cudaMemcpy(t.d_cinv, cinv.data(), P * 4, cudaMemcpyHostToDevice));
+    HG_CUDA_TRY(cudaMemcpy(t.d_cinv_sh, cinv_sh.data(), P * 4, cudaMemcpyHostToDevice));
+    HG_CUDA_TRY(cudaMemcpy(t.d_invp, invp.data(), P * 8, cudaMemcpyHostToDevice));
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    auto ins = ctx->crt.emplace(P, t);
+    if (!ins.second) {  // another thread won the race
+        cudaFree(t.d_M); cudaFree(t.d_negQ); cudaFree(t.d_cinv); cudaFree(t.d_cinv_sh); cudaFree(t.d_invp);
+    }
+    *out = &ins.first->second;
+    return HG_OK;
+}

@@ -1,0 +1,303 @@
+// hg_elementwise.cu -- HBM-bound limb-major ring kernels (ring.py:114-196).
+//
+// One thread per coefficient walks the W words of that coefficient (word w of all
+// coefficients is contiguous, so every word access is coalesced across the warp) and
+// carries between words in registers.  Values are canonical residues mod 2^bits.
+#include "hg_internal.cuh"
+
+namespace {
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ uint32_t mask_for(int bits) {
+    return (bits & 31) ? ((1u << (bits & 31)) - 1u) : 0xffffffffu;
+}
+
+// out = a + b (or a - b) mod 2^bits           RingElement.add / sub  ring.py:114-130
+template <bool SUB>
+__global__ void __launch_bounds__(kThreads) add_kernel(uint32_t* __restrict__ out,
+                                                       const uint32_t* __restrict__ a,
+                                                       const uint32_t* __restrict__ b, int W,
+                                                       int bits, int N) {
+    const int i = blockIdx.x * kThreads + threadIdx.x;
+    if (i >= N) return;
+    uint32_t carry = SUB ? 1u : 0u;  // a - b = a + ~b + 1
+    for (int w = 0; w < W; ++w) {
+        uint32_t x = a[(size_t)w * N + i];
+        uint32_t y = b[(size_t)w * N + i];
+        if (SUB) y = ~y;
+        uint64_t s = (uint64_t)x + y + carry;
+        uint32_t r = (uint32_t)s;
+        carry = (uint32_t)(s >> 32);
+        if (w == W - 1) r &= mask_for(bits);
+        out[(size_t)w * N + i] = r;
+    }
+}
+
+// out = -a mod 2^bits                          RingElement.neg  ring.py:132-134
+__global__ void __launch_bounds__(kThreads) neg_kernel(uint32_t* __restrict__ out,
+                                                       const uint32_t* __restrict__ a, int W,
+                                                       int bits, int N) {
+    const int i = blockIdx.x * kThreads + threadIdx.x;
+    if (i >= N) return;
+    uint32_t carry = 1u;
+    for (int w = 0; w < W; ++w) {
+        uint64_t s = (uint64_t)(~a[(size_t)w * N + i]) + carry;
+        uint32_t r = (uint32_t)s;
+        carry = (uint32_t)(s >> 32);
+        if (w == W - 1) r &= mask_for(bits);
+        out[(size_t)w * N + i] = r;
+    }
+}
+
+struct ScalarWords {
+    uint32_t k[HG_MODUP_WMAX];
+};
+
+// out = a * k mod 2^bits, k given mod 2^bits as kw words (truncated schoolbook, column
+// order so every output word is written once)   RingElement.scalar_mul  ring.py:136-138
+__global__ void __launch_bounds__(kThreads) scalar_mul_kernel(uint32_t* __restrict__ out,
+                                                              const uint32_t* __restrict__ a,
+                                                              int W, int bits, int N,
+                                                              ScalarWords ks, int kw) {
+    const int i = blockIdx.x * kThreads + threadIdx.x;
+    if (i >= N) return;
+    uint64_t carry_lo = 0;  // running column carry (< 2^(32+log2 W+1))
+    uint32_t carry_hi = 0;
+    for (int w = 0; w < W; ++w) {
+        uint64_t acc = carry_lo;
+        uint32_t hi = carry_hi;
+        int jmax = w < kw - 1 ? w : kw - 1;
+        for (int j = 0; j <= jmax; ++j) {
+            uint64_t prod = (uint64_t)a[(size_t)(w - j) * N + i] * ks.k[j];
+            uint64_t s = acc + prod;
+            hi += (s < acc);
+            acc = s;
+        }
+        uint32_t r = (uint32_t)acc;
+        if (w == W - 1) r &= mask_for(bits);
+        out[(size_t)w * N + i] = r;
+        carry_lo = (acc >> 32) | ((uint64_t)hi << 32);
+        carry_hi = 0;
+    }
+}
+
+// out (out_bits) = a mod 2^out_bits              RingElement.reduce_to  ring.py:168-175
+// out (out_bits) = sign-extended a (in_bits)     RingElement.lift_centered_to  ring.py:177-182
+template <bool LIFT>
+__global__ void __launch_bounds__(kThreads) resize_kernel(uint32_t* __restrict__ out, int out_bits,
+                                                          const uint32_t* __restrict__ a,
+                                                          int in_bits, int N) {
+    const int i = blockIdx.x * kThreads + threadIdx.x;
+    if (i >= N) return;
+    const int Wo = (out_bits + 31) >> 5, Wi = (in_bits + 31) >> 5;
+    uint32_t fill = 0;
+    if (LIFT) {
+        // centered(): c > 2^(in_bits-1) is negative; c == 2^(in_bits-1) stays positive
+        // (ring.py:106-110).  Negative <=> top bit set and lower bits not all zero.
+        uint32_t topw = a[(size_t)(Wi - 1) * N + i] & mask_for(in_bits);
+        bool topbit = (topw >> ((in_bits - 1) & 31)) & 1u;
+        bool rest = (topw & ~(1u << ((in_bits - 1) & 31))) != 0;
+        for (int w = 0; w < Wi - 1 && !rest; ++w) rest = a[(size_t)w * N + i] != 0;
+        if (topbit && rest) fill = 0xffffffffu;
+    }
+    for (int w = 0; w < Wo; ++w) {
+        uint32_t r;
+        if (w < Wi) {
+            r = a[(size_t)w * N + i];
+            if (w == Wi - 1) {
+                uint32_t m = mask_for(in_bits);
+                r = (r & m) | (fill & ~m);
+            }
+        } else {
+            r = fill;
+        }
+        if (w == Wo - 1) r &= mask_for(out_bits);
+        out[(size_t)w * N + i] = r;
+    }
+}
+
+// out (out_bits) = ((a + 2^(shift-1)) >> shift) mod 2^out_bits   divide_round  ring.py:184-196
+__global__ void __launch_bounds__(kThreads) divide_round_kernel(uint32_t* __restrict__ out,
+                                                                int out_bits,
+                                                                const uint32_t* __restrict__ a,
+                                                                int in_bits, int shift, int N) {
+    const int i = blockIdx.x * kThreads + threadIdx.x;
+    if (i >= N) return;
+    const int Wi = (in_bits + 31) >> 5, Wo = (out_bits + 31) >> 5;
+    const int sw = shift >> 5, sb = shift & 31;
+    const int rc = shift > 0 ? (shift - 1) >> 5 : -1;
+    const uint32_t rbit = shift > 0 ? 1u << ((shift - 1) & 31) : 0u;
+    // value words v[t] = (a + round)[t] for t in [0, Wi]; word Wi holds the final carry
+    uint32_t carry = 0;
+    uint32_t prev = 0;
+    const int T = sw + Wo + 1;
+    for (int t = 0; t < T; ++t) {
+        uint32_t x = 0;
+        if (t < Wi) {
+            x = a[(size_t)t * N + i];
+            if (t == Wi - 1) x &= mask_for(in_bits);
+        }
+        uint64_t s = (uint64_t)x + carry + (t == rc ? rbit : 0u);
+        uint32_t word = (uint32_t)s;
+        carry = (uint32_t)(s >> 32);
+        if (sb == 0) {
+            if (t >= sw && t - sw < Wo) {
+                int u = t - sw;
+                uint32_t o = word;
+                if (u == Wo - 1) o &= mask_for(out_bits);
+                out[(size_t)u * N + i] = o;
+            }
+        } else if (t > sw && t - sw - 1 < Wo) {
+            int u = t - sw - 1;
+            uint32_t o = (prev >> sb) | (word << (32 - sb));
+            if (u == Wo - 1) o &= mask_for(out_bits);
+            out[(size_t)u * N + i] = o;
+        }
+        prev = word;
+    }
+}
+
+// out[i] = (+/-) a[i * kinv mod 2N]  for x -> x^k            automorphism  ring.py:152-166
+__global__ void __launch_bounds__(kThreads) automorphism_kernel(uint32_t* __restrict__ out,
+                                                                const uint32_t* __restrict__ a,
+                                                                int W, int bits, int N,
+                                                                int64_t kinv) {
+    const int i = blockIdx.x * kThreads + threadIdx.x;
+    if (i >= N) return;
+    int64_t j = ((int64_t)i * kinv) & (2ll * N - 1);
+    bool neg = j >= N;
+    int src = (int)(neg ? j - N : j);
+    uint32_t carry = 1u;
+    for (int w = 0; w < W; ++w) {
+        uint32_t x = a[(size_t)w * N + src];
+        uint32_t r;
+        if (neg) {
+            uint64_t s = (uint64_t)(~x) + carry;
+            r = (uint32_t)s;
+            carry = (uint32_t)(s >> 32);
+        } else {
+            r = x;
+        }
+        if (w == W - 1) r &= mask_for(bits);
+        out[(size_t)w * N + i] = r;
+    }
+}
+
+inline dim3 grid_for(int N) { return dim3((N + kThreads - 1) / kThreads); }
+
+int64_t inv_mod_pow2(int64_t k, int64_t n2) {
+    uint64_t x = (uint64_t)k, inv = x;
+    for (int it = 0; it < 6; ++it) inv *= 2 - x * inv;
+    return (int64_t)(inv & (uint64_t)(n2 - 1));
+}
+
+}  // namespace
+
+// ---- internal entry points (used by the fused drivers in hg_rns.cu) --------------------------
+int hg_ew_add(hg_ctx* ctx, uint32_t* out, const uint32_t* a, const uint32_t* b, int bits,
+              bool subtract, cudaStream_t st) {
+    int W = words_for_bits(bits);
+    if (subtract)
+        add_kernel<true><<<grid_for(ctx->N), kThreads, 0, st>>>(out, a, b, W, bits, ctx->N);
+    else
+        add_kernel<false><<<grid_for(ctx->N), kThreads, 0, st>>>(out, a, b, W, bits, ctx->N);
+    HG_LAUNCH_CHECK(ctx);
+    return HG_OK;
+}
+
+int hg_ew_divide_round(hg_ctx* ctx, uint32_t* out, int out_bits, const uint32_t* a, int in_bits,
+                       int shift, cudaStream_t st) {
+    divide_round_kernel<<<grid_for(ctx->N), kThreads, 0, st>>>(out, out_bits, a, in_bits, shift,
+                                                               ctx->N);
+    HG_LAUNCH_CHECK(ctx);
+    return HG_OK;
+}
+
+int hg_ew_automorphism(hg_ctx* ctx, uint32_t* out, const uint32_t* a, int bits, int64_t k,
+                       cudaStream_t st) {
+    int64_t n2 = 2ll * ctx->N;
+    int64_t kk = ((k % n2) + n2) % n2;
+    if ((kk & 1) == 0) return hg_fail(HG_EINVAL, "automorphism exponent must be odd");
+    automorphism_kernel<<<grid_for(ctx->N), kThreads, 0, st>>>(out, a, words_for_bits(bits), bits,
+                                                               ctx->N, inv_mod_pow2(kk, n2));
+    HG_LAUNCH_CHECK(ctx);
+    return HG_OK;
+}
+
+// ---- C-ABI -------------------------------------------------------------------------------------
+#define HG_CHECK_ARGS(cond, msg) \
+    do {                          \
+        if (!(cond)) return hg_fail(HG_EINVAL, msg); \
+    } while (0)
+
+extern "C" int hg_poly_add(hg_ctx* ctx, uint32_t* out, const uint32_t* a, const uint32_t* b,
+                           int bits, void* stream) {
+    HG_CHECK_ARGS(ctx && out && a && b && bits >= 1, "hg_poly_add: bad arguments");
+    return hg_ew_add(ctx, out, a, b, bits, false, (cudaStream_t)stream);
+}
+
+extern "C" int hg_poly_sub(hg_ctx* ctx, uint32_t* out, const uint32_t* a, const uint32_t* b,
+                           int bits, void* stream) {
+    HG_CHECK_ARGS(ctx && out && a && b && bits >= 1, "hg_poly_sub: bad arguments");
+    return hg_ew_add(ctx, out, a, b, bits, true, (cudaStream_t)stream);
+}
+
+extern "C" int hg_poly_neg(hg_ctx* ctx, uint32_t* out, const uint32_t* a, int bits,
+                           void* stream) {
+    HG_CHECK_ARGS(ctx && out && a && bits >= 1, "hg_poly_neg: bad arguments");
+    neg_kernel<<<grid_for(ctx->N), kThreads, 0, (cudaStream_t)stream>>>(out, a, words_for_bits(bits),
+                                                                        bits, ctx->N);
+    HG_LAUNCH_CHECK(ctx);
+    return HG_OK;
+}
+
+extern "C" int hg_poly_scalar_mul(hg_ctx* ctx, uint32_t* out, const uint32_t* a, int bits,
+                                  const uint32_t* k_words_host, int kw, void* stream) {
+    HG_CHECK_ARGS(ctx && out && a && bits >= 1 && k_words_host && kw >= 1,
+                  "hg_poly_scalar_mul: bad arguments");
+    int W = words_for_bits(bits);
+    HG_CHECK_ARGS(kw <= W && W <= HG_MODUP_WMAX, "hg_poly_scalar_mul: scalar wider than the ring");
+    ScalarWords ks{};
+    for (int j = 0; j < kw; ++j) ks.k[j] = k_words_host[j];
+    // an out-of-place product: `out` must not alias `a` (columns read lower words)
+    HG_CHECK_ARGS(out != a || kw == 1, "hg_poly_scalar_mul: in-place needs a one-word scalar");
+    scalar_mul_kernel<<<grid_for(ctx->N), kThreads, 0, (cudaStream_t)stream>>>(out, a, W, bits,
+                                                                               ctx->N, ks, kw);
+    HG_LAUNCH_CHECK(ctx);
+    return HG_OK;
+}
+
+extern "C" int hg_poly_reduce_to(hg_ctx* ctx, uint32_t* out, int out_bits, const uint32_t* a,
+                                 int in_bits, void* stream) {
+    HG_CHECK_ARGS(ctx && out && a && out_bits >= 1 && out_bits <= in_bits,
+                  "hg_poly_reduce_to: bad arguments");
+    resize_kernel<false><<<grid_for(ctx->N), kThreads, 0, (cudaStream_t)stream>>>(out, out_bits, a,
+                                                                                  in_bits, ctx->N);
+    HG_LAUNCH_CHECK(ctx);
+    return HG_OK;
+}
+
+extern "C" int hg_poly_lift_centered(hg_ctx* ctx, uint32_t* out, int out_bits, const uint32_t* a,
+                                     int in_bits, void* stream) {
+    HG_CHECK_ARGS(ctx && out && a && in_bits >= 1 && out_bits >= in_bits,
+                  "hg_poly_lift_centered: bad arguments");
+    resize_kernel<true><<<grid_for(ctx->N), kThreads, 0, (cudaStream_t)stream>>>(out, out_bits, a,
+                                                                                 in_bits, ctx->N);
+    HG_LAUNCH_CHECK(ctx);
+    return HG_OK;
+}
+
+extern "C" int hg_poly_divide_round(hg_ctx* ctx, uint32_t* out, int out_bits, const uint32_t* a,
+                                    int in_bits, int shift, void* stream) {
+    HG_CHECK_ARGS(ctx && out && a && out_bits >= 1 && in_bits >= 1 && shift >= 0,
+                  "hg_poly_divide_round: bad arguments");
+    HG_CHECK_ARGS(out != a, "hg_poly_divide_round: out must not alias the input");
+    return hg_ew_divide_round(ctx, out, out_bits, a, in_bits, shift, (cudaStream_t)stream);
+}
+
+extern "C" int hg_poly_automorphism(hg_ctx* ctx, uint32_t* out, const uint32_t* a, int bits,
+                                    int64_t k, void* stream) {
+    HG_CHECK_ARGS(ctx && out && a && bits >= 1 && out != a, "hg_poly_automorphism: bad arguments");
+    return hg_ew_automorphism(ctx, out, a, bits, k, (cudaStream_t)stream);
+}

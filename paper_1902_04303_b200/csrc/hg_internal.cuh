@@ -1,0 +1,135 @@
+// hg_internal.cuh -- shared definitions for the sm_100a evaluator library.
+//
+// Arithmetic model: ring elements of Z_{2^l}[x]/(x^N+1) are stored
+// limb-major in radix 2^32.  An exact negacyclic product (the reference's Kronecker
+// big-int multiply, ring.py:46-58) is computed in an RNS basis of 30-bit NTT primes
+// p = 1 mod 2^18:  ModUp (radix-2^32 -> residues), forward negacyclic NTT, pointwise
+// Montgomery product, inverse NTT, and an exact CRT back to radix 2^32 that emits any
+// bit window [shift, shift+bits) of (c + 2^(shift-1)) -- i.e. mod 2^k reduction and the
+// divide_round of ckks._keyswitch / rescale fused into the reconstruction.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+#include <atomic>
+
+#include "../../include/hegwas_b200.h"
+
+#define HG_MAX_PRIMES 320
+#define HG_MODUP_WMAX 192   // operands up to 6144 bits
+#define HG_PRIME_SHIFT 18   // primes are 1 mod 2^18: negacyclic NTT up to N = 2^17
+
+struct PrimeInfo {
+    uint32_t p;         // the prime (< 2^30)
+    uint32_t pinv_neg;  // -p^{-1} mod 2^32 (Montgomery)
+    uint32_t c32;       // 2^32 mod p
+    uint32_t c30;       // 2^30 mod p
+    uint32_t c30_sh;    // floor(c30 * 2^32 / p) (Shoup companion)
+    uint32_t ninv;      // N^{-1} mod p (unused by the fused CRT; kept for the raw iNTT)
+    uint32_t ninv_sh;
+    uint32_t pad;
+};
+
+// Per-P CRT reconstruction tables (P = number of primes of the basis prefix).
+struct CrtTable {
+    int P = 0;
+    int P4 = 0;          // P rounded up to a multiple of 4 (row pitch of M)
+    int W = 0;           // column words available
+    uint32_t* d_M = nullptr;      // [W][P4]: word t of (Q/p_j mod 2^(32W)); zero padded
+    uint32_t* d_negQ = nullptr;   // [W]: word t of (-Q mod 2^(32W))
+    uint32_t* d_cinv = nullptr;   // [P]: (Q/p_j)^{-1} * N^{-1} * 2^32 mod p_j
+    uint32_t* d_cinv_sh = nullptr;
+    double* d_invp = nullptr;     // [P]: 1/p_j
+};
+
+struct hg_ctx {
+    int log_n = 0;
+    int N = 0;
+    int device = 0;
+    int nprimes = 0;
+    std::vector<uint32_t> primes;       // descending
+    std::vector<double> prefix_bits;    // prefix_bits[P] = sum_{j<P} log2 p_j
+    PrimeInfo* d_pinfo = nullptr;       // [nprimes]
+    uint32_t* d_modup = nullptr;        // [nprimes][HG_MODUP_WMAX] : 2^(32w) mod p_j
+    // twiddles, lazily materialised for the first `tw_ready` primes: [nprimes][N]
+    uint32_t* d_psi = nullptr;
+    uint32_t* d_psi_sh = nullptr;
+    uint32_t* d_ipsi = nullptr;
+    uint32_t* d_ipsi_sh = nullptr;
+    int tw_ready = 0;
+    std::map<int, CrtTable> crt;
+    std::mutex mu;
+    std::atomic<long long> launches{0};
+};
+
+struct hg_key {
+    hg_ctx* ctx = nullptr;
+    int level = 0;      // input level l
+    int big_l = 0;      // L
+    int P = 0;          // primes of the keyswitch basis
+    uint32_t* d_kb = nullptr;   // [P][N] NTT residues of kb mod 2^(l+L) (centered), in [0,p)
+    uint32_t* d_ka = nullptr;
+    size_t bytes = 0;
+};
+
+// ---- error plumbing ------------------------------------------------------------------
+void hg_set_error(const std::string& msg);
+int hg_fail(int code, const std::string& msg);
+#define HG_CUDA_TRY(expr)                                                              \
+    do {                                                                               \
+        cudaError_t _e = (expr);                                                       \
+        if (_e != cudaSuccess)                                                         \
+            return hg_fail(HG_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+#define HG_LAUNCH_CHECK(ctx)                                                           \
+    do {                                                                               \
+        (ctx)->launches.fetch_add(1, std::memory_order_relaxed);                       \
+        cudaError_t _e = cudaGetLastError();                                           \
+        if (_e != cudaSuccess)                                                         \
+            return hg_fail(HG_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(_e)); \
+    } while (0)
+
+static inline int words_for_bits(int bits) { return (bits + 31) >> 5; }
+
+// ---- host-side helpers (hg_context.cu) ----------------------------------------------
+int hg_ensure_twiddles(hg_ctx* ctx, int P);
+int hg_get_crt(hg_ctx* ctx, int P, const CrtTable** out);
+int hg_primes_for_bits(const hg_ctx* ctx, double bits);   // -1 if too wide
+
+// ---- device arithmetic --------------------------------------------------------------
+// Shoup product a*w mod p for any a < 2^32, result in [0, 2p).
+__device__ __forceinline__ uint32_t mul_shoup_lazy(uint32_t a, uint32_t w, uint32_t wsh,
+                                                   uint32_t p) {
+    uint32_t q = __umulhi(a, wsh);
+    return a * w - q * p;
+}
+__device__ __forceinline__ uint32_t reduce_2p(uint32_t a, uint32_t p) {
+    return a >= p ? a - p : a;
+}
+__device__ __forceinline__ uint32_t reduce_4p(uint32_t a, uint32_t p) {
+    uint32_t p2 = p << 1;
+    a = a >= p2 ? a - p2 : a;
+    return a >= p ? a - p : a;
+}
+// Montgomery product a*b*2^-32 mod p; requires a*b < p*2^32; result in [0, 2p).
+__device__ __forceinline__ uint32_t mont_mul(uint32_t a, uint32_t b, uint32_t p,
+                                             uint32_t pinv_neg) {
+    uint64_t t = (uint64_t)a * b;
+    uint32_t m = (uint32_t)t * pinv_neg;
+    uint64_t u = t + (uint64_t)m * p;
+    return (uint32_t)(u >> 32);
+}
+// Reduce a 64-bit accumulator (any value) to [0, p) using 2^32 and 2^30 folds.
+__device__ __forceinline__ uint32_t reduce_u64(uint64_t acc, const PrimeInfo& pi) {
+    // fold 1: < 2^62 + 2^32 ; fold 2: < 2^61
+    acc = (uint64_t)(uint32_t)(acc >> 32) * pi.c32 + (uint32_t)acc;
+    acc = (uint64_t)(uint32_t)(acc >> 32) * pi.c32 + (uint32_t)acc;
+    uint32_t a = (uint32_t)(acc >> 30);
+    uint32_t b = (uint32_t)acc & 0x3fffffffu;
+    uint32_t r = mul_shoup_lazy(a, pi.c30, pi.c30_sh, pi.p) + b;  // < 2p + 2^30 < 4p
+    return reduce_4p(r, pi.p);
+}

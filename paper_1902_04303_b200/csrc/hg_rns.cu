@@ -1,0 +1,515 @@
+// hg_rns.cu -- the exact product engine: ModUp (radix 2^32 -> RNS residues), pointwise
+// Montgomery products in the NTT domain, and the CRT reconstruction that emits a bit window
+// of the exact negacyclic convolution.  Also the key-switch / ciphertext-multiply drivers.
+//
+// Reference semantics replaced here:
+//   ring.negacyclic_mul / RingElement.mul / mul_mod     ring.py:46-65, 140-150
+//   ckks._keyswitch                                     ckks.py:187-194
+//   ckks.mult (tensor + relinearise) + rescale          ckks.py:166-184, 197-224, 310-313
+//   ckks._apply_automorphism                            ckks.py:247-253
+#include "hg_internal.cuh"
+
+#include <cmath>
+
+int hg_ntt_launch(hg_ctx* ctx, uint32_t* data, int rows, int P, int prime_offset, bool forward,
+                  cudaStream_t stream);
+int hg_ew_add(hg_ctx* ctx, uint32_t* out, const uint32_t* a, const uint32_t* b, int bits,
+              bool subtract, cudaStream_t stream);
+int hg_ew_divide_round(hg_ctx* ctx, uint32_t* out, int out_bits, const uint32_t* a,
+                       int in_bits, int shift, cudaStream_t stream);
+int hg_ew_automorphism(hg_ctx* ctx, uint32_t* out, const uint32_t* a, int bits, int64_t k,
+                       cudaStream_t stream);
+
+namespace {
+
+constexpr int kModupThreads = 128;
+constexpr int kCrtThreads = 64;
+
+struct OperandSet {
+    const uint32_t* words[4];
+    int bits[4];
+    int is_signed[4];
+};
+struct OutSet {
+    uint32_t* out[4];
+};
+
+// ---- ModUp ---------------------------------------------------------------------------------
+// One thread per coefficient; the coefficient's W words are staged in shared memory
+// ([W][threads], conflict-free), then reduced mod each prime with a 64-bit multiply-
+// accumulate against 2^(32w) mod p (folded every 2 products to stay below 2^64).
+// gridDim.y selects the operand; output rows [y][P][N].  If automorph_kinv != 0 the
+// coefficient order is permuted on load: out[i] = (+/-) in[i * kinv mod 2N] (x -> x^k).
+__global__ void __launch_bounds__(kModupThreads) modup_kernel(
+    OperandSet ops, int N, int log_n, const PrimeInfo* __restrict__ pinfo,
+    const uint32_t* __restrict__ modup_tab, int P, uint32_t* __restrict__ out,
+    int64_t automorph_kinv) {
+    extern __shared__ uint32_t ws[];
+    const int op = blockIdx.y;
+    const uint32_t* in = ops.words[op];
+    const int bits = ops.bits[op];
+    const int is_signed = ops.is_signed[op];
+    const int W = (bits + 31) >> 5;
+    const int TB = blockDim.x;
+    const int i = blockIdx.x * TB + threadIdx.x;
+    const uint32_t top_mask = (bits & 31) ? ((1u << (bits & 31)) - 1u) : 0xffffffffu;
+    int src = i;
+    bool negate = false;
+    if (automorph_kinv != 0) {
+        int64_t j = ((int64_t)i * automorph_kinv) & ((2ll * N) - 1);
+        if (j >= N) { negate = true; j -= N; }
+        src = (int)j;
+    }
+    uint32_t any = 0;
+    for (int w = 0; w < W; ++w) {
+        uint32_t v = in[(size_t)w * N + src];
+        if (w == W - 1) v &= top_mask;
+        any |= v;
+        ws[w * TB + threadIdx.x] = v;
+    }
+    const bool sign = is_signed && ((ws[(W - 1) * TB + threadIdx.x] >> ((bits - 1) & 31)) & 1u);
+    uint32_t* outp = out + (size_t)op * P * N;
+    for (int j = 0; j < P; ++j) {
+        const PrimeInfo pi = pinfo[j];
+        const uint32_t* C = modup_tab + (size_t)j * HG_MODUP_WMAX;
+        uint64_t acc = 0;
+        int w = 0;
+        for (; w + 1 < W; w += 2) {
+            acc += (uint64_t)ws[w * TB + threadIdx.x] * C[w];
+            acc += (uint64_t)ws[(w + 1) * TB + threadIdx.x] * C[w + 1];
+            acc = (uint64_t)(uint32_t)(acc >> 32) * pi.c32 + (uint32_t)acc;
+        }
+        if (w < W) acc += (uint64_t)ws[w * TB + threadIdx.x] * C[w];
+        uint32_t r = reduce_u64(acc, pi);
+        // 2^bits mod p for the two's complement / negation corrections
+        uint32_t pw = 0;
+        if (sign || negate) {
+            uint64_t t = (uint64_t)C[bits >> 5] << (bits & 31);  // < 2^61
+            pw = reduce_u64(t, pi);
+        }
+        if (sign) r = r >= pw ? r - pw : r + pi.p - pw;           // value - 2^bits
+        if (negate && any) {                                       // (2^bits - x) mod 2^bits
+            // for signed operands negation is plain -x; for unsigned it is 2^bits - x
+            if (is_signed) r = r ? pi.p - r : 0;
+            else r = pw >= r ? pw - r : pw + pi.p - r;
+        }
+        outp[(size_t)j * N + i] = r;
+    }
+}
+
+// ---- pointwise products ------------------------------------------------------------------
+// a, b: forward-NTT outputs in [0, 4p) (or keys in [0, p)); result mont(a,b) in [0, 2p).
+__global__ void pw_mul_kernel(uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
+                              int P, int N, const PrimeInfo* __restrict__ pinfo) {
+    const int j = blockIdx.y;
+    const PrimeInfo pi = pinfo[j];
+    const size_t off = (size_t)j * N;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+        uint32_t x = a[off + i], y = b[off + i];
+        uint32_t p2 = pi.p << 1;
+        x = x >= p2 ? x - p2 : x;
+        y = y >= p2 ? y - p2 : y;
+        uint32_t r = mont_mul(x, y, pi.p, pi.pinv_neg);
+        a[off + i] = r >= pi.p ? r - pi.p : r;
+    }
+}
+
+// buf = [A0 | A1 | B0 | B1] each [P][N] -> [D0 | D1 | D2] in place (rows 0..2).
+__global__ void pw_tensor_kernel(uint32_t* __restrict__ buf, int P, int N,
+                                 const PrimeInfo* __restrict__ pinfo) {
+    const int j = blockIdx.y;
+    const PrimeInfo pi = pinfo[j];
+    const size_t stride = (size_t)P * N;
+    const size_t off = (size_t)j * N;
+    const uint32_t p2 = pi.p << 1;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+        size_t o = off + i;
+        uint32_t a0 = buf[o], a1 = buf[o + stride], b0 = buf[o + 2 * stride], b1 = buf[o + 3 * stride];
+        a0 = a0 >= p2 ? a0 - p2 : a0;
+        a1 = a1 >= p2 ? a1 - p2 : a1;
+        b0 = b0 >= p2 ? b0 - p2 : b0;
+        b1 = b1 >= p2 ? b1 - p2 : b1;
+        uint32_t d0 = mont_mul(a0, b0, pi.p, pi.pinv_neg);
+        uint32_t d1 = mont_mul(a0, b1, pi.p, pi.pinv_neg) + mont_mul(a1, b0, pi.p, pi.pinv_neg);
+        uint32_t d2 = mont_mul(a1, b1, pi.p, pi.pinv_neg);
+        d0 = d0 >= pi.p ? d0 - pi.p : d0;
+        d1 = d1 >= p2 ? d1 - p2 : d1;
+        d1 = d1 >= pi.p ? d1 - pi.p : d1;
+        d2 = d2 >= pi.p ? d2 - pi.p : d2;
+        buf[o] = d0;
+        buf[o + stride] = d1;
+        buf[o + 2 * stride] = d2;
+    }
+}
+
+// buf = [X | T0 | T1] each [P][N]: T0 = X*KB, T1 = X*KA (Montgomery), keys in [0, p).
+__global__ void pw_key2_kernel(uint32_t* __restrict__ buf, const uint32_t* __restrict__ kb,
+                               const uint32_t* __restrict__ ka, int P, int N,
+                               const PrimeInfo* __restrict__ pinfo) {
+    const int j = blockIdx.y;
+    const PrimeInfo pi = pinfo[j];
+    const size_t stride = (size_t)P * N;
+    const size_t off = (size_t)j * N;
+    const uint32_t p2 = pi.p << 1;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+        size_t o = off + i;
+        uint32_t x = buf[o];
+        x = x >= p2 ? x - p2 : x;
+        uint32_t t0 = mont_mul(x, kb[o], pi.p, pi.pinv_neg);
+        uint32_t t1 = mont_mul(x, ka[o], pi.p, pi.pinv_neg);
+        buf[o + stride] = t0 >= pi.p ? t0 - pi.p : t0;
+        buf[o + 2 * stride] = t1 >= pi.p ? t1 - pi.p : t1;
+    }
+}
+
+__global__ void reduce_rows_kernel(uint32_t* __restrict__ a, int N,
+                                   const PrimeInfo* __restrict__ pinfo) {
+    const int j = blockIdx.y;
+    const uint32_t p = pinfo[j].p;
+    const size_t off = (size_t)j * N;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x)
+        a[off + i] = reduce_4p(a[off + i], p);
+}
+
+// ---- CRT reconstruction -----------------------------------------------------------------------
+// Exact c = sum_j y_j Q/p_j - v Q with y_j = r_j (Q/p_j)^-1 N^-1 2^32 mod p_j and
+// v = round(sum_j y_j / p_j) (|c| < Q/8 by the prime-count margin, so the float64 estimate
+// is exact).  Column t of c mod 2^(32T) is sum_j y_j M[t][j] + v negQ[t] + carry, scanned
+// low to high; the kernel emits bits [shift, shift + out_bits) of c + 2^(shift-1).
+__global__ void __launch_bounds__(kCrtThreads) crt_kernel(
+    const uint32_t* __restrict__ res, int P, int P4, int N, const PrimeInfo* __restrict__ pinfo,
+    const uint32_t* __restrict__ Mtab, const uint32_t* __restrict__ negQ,
+    const uint32_t* __restrict__ cinv, const uint32_t* __restrict__ cinv_sh,
+    const double* __restrict__ invp, int shift, int out_bits, OutSet outs) {
+    extern __shared__ uint32_t ys[];  // [P4][kCrtThreads]
+    const int TB = blockDim.x;
+    const int i = blockIdx.x * TB + threadIdx.x;
+    const uint32_t* r = res + (size_t)blockIdx.y * P * N;
+    uint32_t* out = outs.out[blockIdx.y];
+    double S = 0.0;
+    for (int j = 0; j < P; ++j) {
+        uint32_t p = pinfo[j].p;
+        uint32_t x = r[(size_t)j * N + i];
+        uint32_t y = reduce_2p(mul_shoup_lazy(x, cinv[j], cinv_sh[j], p), p);
+        ys[j * TB + threadIdx.x] = y;
+        S += (double)y * invp[j];
+    }
+    for (int j = P; j < P4; ++j) ys[j * TB + threadIdx.x] = 0;
+    const uint32_t v = (uint32_t)floor(S + 0.5);
+    const int sw = shift >> 5, sb = shift & 31;
+    const int out_w = (out_bits + 31) >> 5;
+    const uint32_t top_mask = (out_bits & 31) ? ((1u << (out_bits & 31)) - 1u) : 0xffffffffu;
+    const int T = sw + out_w + (sb ? 1 : 0);
+    const int round_col = shift > 0 ? ((shift - 1) >> 5) : -1;
+    const uint32_t round_bit = shift > 0 ? (1u << ((shift - 1) & 31)) : 0u;
+    uint64_t carry = 0;
+    uint32_t prev = 0;
+    for (int t = 0; t < T; ++t) {
+        uint64_t acc = (uint32_t)carry;
+        uint64_t top = carry >> 32;
+        acc += (uint64_t)v * negQ[t];
+        if (t == round_col) acc += round_bit;
+        top += acc >> 32;
+        acc = (uint32_t)acc;
+        const uint4* Mrow = reinterpret_cast<const uint4*>(Mtab + (size_t)t * P4);
+        for (int j4 = 0; j4 < P4 / 4; ++j4) {
+            uint4 m = Mrow[j4];
+            const uint32_t* y = ys + (j4 * 4) * TB + threadIdx.x;
+            acc += (uint64_t)y[0] * m.x;
+            acc += (uint64_t)y[TB] * m.y;
+            acc += (uint64_t)y[2 * TB] * m.z;
+            acc += (uint64_t)y[3 * TB] * m.w;
+            top += acc >> 32;
+            acc = (uint32_t)acc;
+        }
+        const uint32_t word = (uint32_t)acc;
+        carry = top;
+        // emit
+        if (sb == 0) {
+            if (t >= sw) {
+                int u = t - sw;
+                uint32_t o = word;
+                if (u == out_w - 1) o &= top_mask;
+                out[(size_t)u * N + i] = o;
+            }
+        } else if (t > sw) {
+            int u = t - sw - 1;
+            uint32_t o = (prev >> sb) | (word << (32 - sb));
+            if (u == out_w - 1) o &= top_mask;
+            out[(size_t)u * N + i] = o;
+        }
+        prev = word;
+    }
+}
+
+// ---- device scratch ------------------------------------------------------------------------
+struct Scratch {
+    void* p = nullptr;
+    cudaStream_t s;
+    explicit Scratch(cudaStream_t st) : s(st) {}
+    cudaError_t alloc(size_t bytes) { return cudaMallocAsync(&p, bytes, s); }
+    ~Scratch() {
+        if (p) cudaFreeAsync(p, s);
+    }
+    uint32_t* u32() { return static_cast<uint32_t*>(p); }
+};
+
+int launch_modup(hg_ctx* ctx, const OperandSet& ops, int nops, int P, uint32_t* out,
+                 int64_t kinv, cudaStream_t st) {
+    int maxw = 0;
+    for (int k = 0; k < nops; ++k) {
+        int w = words_for_bits(ops.bits[k]);
+        if (w > maxw) maxw = w;
+        if (ops.bits[k] < 1 || w > HG_MODUP_WMAX - 1)
+            return hg_fail(HG_EINVAL, "operand width out of range");
+    }
+    size_t smem = (size_t)maxw * kModupThreads * 4;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(modup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(crt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        attr_set = true;
+    }
+    const int N = ctx->N;
+    int threads = N < kModupThreads ? N : kModupThreads;
+    smem = (size_t)maxw * threads * 4;
+    dim3 grid(N / threads, nops);
+    modup_kernel<<<grid, threads, smem, st>>>(ops, N, ctx->log_n, ctx->d_pinfo, ctx->d_modup, P,
+                                              out, kinv);
+    HG_LAUNCH_CHECK(ctx);
+    return HG_OK;
+}
+
+int launch_crt(hg_ctx* ctx, const uint32_t* res, int nouts, int P, int shift, int out_bits,
+               const OutSet& outs, cudaStream_t st) {
+    const CrtTable* tab = nullptr;
+    int rc = hg_get_crt(ctx, P, &tab);
+    if (rc) return rc;
+    int sw = shift >> 5;
+    int T = sw + words_for_bits(out_bits) + ((shift & 31) ? 1 : 0);
+    if (T > tab->W) return hg_fail(HG_ERANGE, "CRT window exceeds table width");
+    const int N = ctx->N;
+    const int threads = N < kCrtThreads ? N : kCrtThreads;
+    size_t smem = (size_t)tab->P4 * threads * 4;
+    dim3 grid(N / threads, nouts);
+    crt_kernel<<<grid, threads, smem, st>>>(res, P, tab->P4, N, ctx->d_pinfo, tab->d_M,
+                                                tab->d_negQ, tab->d_cinv, tab->d_cinv_sh,
+                                                tab->d_invp, shift, out_bits, outs);
+    HG_LAUNCH_CHECK(ctx);
+    return HG_OK;
+}
+
+dim3 pw_grid(int N, int rows) { return dim3((N + 255) / 256 < 64 ? (N + 255) / 256 : 64, rows); }
+
+int magnitude_bits(const hg_operand& o) { return o.signed_rep ? o.bits - 1 : o.bits; }
+
+int primes_for_product(hg_ctx* ctx, double mag_bits, int window_bits) {
+    // |c| <= N 2^mag ; need Q > 8|c| (2 bits of margin beyond the sign)
+    (void)window_bits;  // CRT tables are at least HG_MODUP_WMAX words wide
+    return hg_primes_for_bits(ctx, mag_bits + ctx->log_n + 3.0);
+}
+
+}  // namespace
+
+// ---- public product API --------------------------------------------------------------------------
+extern "C" int hg_poly_mul(hg_ctx* ctx, uint32_t* out, int out_bits, hg_operand a,
+                           hg_operand b, void* stream) {
+    if (!ctx || !out || !a.words || !b.words || out_bits < 1)
+        return hg_fail(HG_EINVAL, "hg_poly_mul: bad arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int N = ctx->N;
+    int P = primes_for_product(ctx, magnitude_bits(a) + magnitude_bits(b), out_bits);
+    if (P < 0) return hg_fail(HG_ERANGE, "product exceeds the NTT prime basis");
+    Scratch buf(st);
+    HG_CUDA_TRY(buf.alloc((size_t)2 * P * N * 4));
+    OperandSet ops{};
+    ops.words[0] = a.words; ops.bits[0] = a.bits; ops.is_signed[0] = a.signed_rep;
+    ops.words[1] = b.words; ops.bits[1] = b.bits; ops.is_signed[1] = b.signed_rep;
+    int rc = launch_modup(ctx, ops, 2, P, buf.u32(), 0, st);
+    if (rc) return rc;
+    rc = hg_ntt_launch(ctx, buf.u32(), 2 * P, P, 0, true, st);
+    if (rc) return rc;
+    pw_mul_kernel<<<pw_grid(N, P), 256, 0, st>>>(buf.u32(), buf.u32() + (size_t)P * N, P, N,
+                                                 ctx->d_pinfo);
+    HG_LAUNCH_CHECK(ctx);
+    rc = hg_ntt_launch(ctx, buf.u32(), P, P, 0, false, st);
+    if (rc) return rc;
+    OutSet outs{};
+    outs.out[0] = out;
+    return launch_crt(ctx, buf.u32(), 1, P, 0, out_bits, outs, st);
+}
+
+extern "C" int hg_poly_tensor(hg_ctx* ctx, uint32_t* d0, uint32_t* d1, uint32_t* d2,
+                              int out_bits, hg_operand a0, hg_operand a1, hg_operand b0,
+                              hg_operand b1, void* stream) {
+    if (!ctx || !d0 || !d1 || !d2 || out_bits < 1)
+        return hg_fail(HG_EINVAL, "hg_poly_tensor: bad arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int N = ctx->N;
+    int ma = magnitude_bits(a0) > magnitude_bits(a1) ? magnitude_bits(a0) : magnitude_bits(a1);
+    int mb = magnitude_bits(b0) > magnitude_bits(b1) ? magnitude_bits(b0) : magnitude_bits(b1);
+    int P = primes_for_product(ctx, ma + mb + 1, out_bits);  // +1: d1 is a sum of two products
+    if (P < 0) return hg_fail(HG_ERANGE, "tensor product exceeds the NTT prime basis");
+    Scratch buf(st);
+    HG_CUDA_TRY(buf.alloc((size_t)4 * P * N * 4));
+    OperandSet ops{};
+    const hg_operand in[4] = {a0, a1, b0, b1};
+    for (int k = 0; k < 4; ++k) {
+        ops.words[k] = in[k].words; ops.bits[k] = in[k].bits; ops.is_signed[k] = in[k].signed_rep;
+    }
+    int rc = launch_modup(ctx, ops, 4, P, buf.u32(), 0, st);
+    if (rc) return rc;
+    rc = hg_ntt_launch(ctx, buf.u32(), 4 * P, P, 0, true, st);
+    if (rc) return rc;
+    pw_tensor_kernel<<<pw_grid(N, P), 256, 0, st>>>(buf.u32(), P, N, ctx->d_pinfo);
+    HG_LAUNCH_CHECK(ctx);
+    rc = hg_ntt_launch(ctx, buf.u32(), 3 * P, P, 0, false, st);
+    if (rc) return rc;
+    OutSet outs{};
+    outs.out[0] = d0; outs.out[1] = d1; outs.out[2] = d2;
+    return launch_crt(ctx, buf.u32(), 3, P, 0, out_bits, outs, st);
+}
+
+// ---- keys and key switching ------------------------------------------------------------------------
+extern "C" int hg_key_prepare(hg_ctx* ctx, const uint32_t* kb, const uint32_t* ka, int key_bits,
+                              int level, int big_l, void* stream, hg_key** out) {
+    if (!ctx || !kb || !ka || !out || level < 1 || big_l < 1 || level + big_l > key_bits)
+        return hg_fail(HG_EINVAL, "hg_key_prepare: bad arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int N = ctx->N;
+    const int kbits = level + big_l;
+    // x canonical (level bits) times centered key (kbits-1 magnitude); window [L, L+level)
+    int P = primes_for_product(ctx, (double)level + (kbits - 1), kbits + 1);
+    if (P < 0) return hg_fail(HG_ERANGE, "key switch exceeds the NTT prime basis");
+    hg_key* key = new hg_key();
+    key->ctx = ctx;
+    key->level = level;
+    key->big_l = big_l;
+    key->P = P;
+    key->bytes = (size_t)2 * P * N * 4;
+    if (cudaMalloc(&key->d_kb, key->bytes) != cudaSuccess) {
+        delete key;
+        return hg_fail(HG_ENOMEM, "key allocation failed");
+    }
+    key->d_ka = key->d_kb + (size_t)P * N;
+    OperandSet ops{};
+    ops.words[0] = kb; ops.bits[0] = kbits; ops.is_signed[0] = 1;   // reduce_to(l+L), centered
+    ops.words[1] = ka; ops.bits[1] = kbits; ops.is_signed[1] = 1;
+    int rc = launch_modup(ctx, ops, 2, P, key->d_kb, 0, st);
+    if (!rc) rc = hg_ntt_launch(ctx, key->d_kb, 2 * P, P, 0, true, st);
+    if (!rc) {
+        reduce_rows_kernel<<<pw_grid(N, P), 256, 0, st>>>(key->d_kb, N, ctx->d_pinfo);
+        ctx->launches++;
+        reduce_rows_kernel<<<pw_grid(N, P), 256, 0, st>>>(key->d_ka, N, ctx->d_pinfo);
+        HG_LAUNCH_CHECK(ctx);
+    }
+    if (rc) {
+        cudaFree(key->d_kb);
+        delete key;
+        return rc;
+    }
+    *out = key;
+    return HG_OK;
+}
+
+extern "C" int hg_key_destroy(hg_key* key) {
+    if (!key) return HG_OK;
+    cudaFree(key->d_kb);
+    delete key;
+    return HG_OK;
+}
+
+extern "C" size_t hg_key_device_bytes(const hg_key* key) { return key ? key->bytes : 0; }
+
+static int64_t inverse_mod_2n(int64_t k, int64_t n2) {
+    // k odd, n2 a power of two: Newton iteration for the inverse mod 2^64, then reduce
+    uint64_t x = (uint64_t)k;
+    uint64_t inv = x;
+    for (int it = 0; it < 6; ++it) inv *= 2 - x * inv;
+    return (int64_t)(inv & (uint64_t)(n2 - 1));
+}
+
+extern "C" int hg_keyswitch(hg_ctx* ctx, const hg_key* key, const uint32_t* x,
+                            int64_t automorph_k, uint32_t* out0, uint32_t* out1, void* stream) {
+    if (!ctx || !key || !x || !out0 || !out1 || key->ctx != ctx)
+        return hg_fail(HG_EINVAL, "hg_keyswitch: bad arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int N = ctx->N;
+    const int P = key->P;
+    int64_t kinv = 0;
+    if (automorph_k != 1) {
+        int64_t n2 = 2ll * N;
+        int64_t k = ((automorph_k % n2) + n2) % n2;
+        if ((k & 1) == 0) return hg_fail(HG_EINVAL, "automorphism exponent must be odd");
+        kinv = inverse_mod_2n(k, n2);
+    }
+    Scratch buf(st);
+    HG_CUDA_TRY(buf.alloc((size_t)3 * P * N * 4));
+    OperandSet ops{};
+    ops.words[0] = x; ops.bits[0] = key->level; ops.is_signed[0] = 0;  // canonical rep
+    int rc = launch_modup(ctx, ops, 1, P, buf.u32(), kinv, st);
+    if (rc) return rc;
+    rc = hg_ntt_launch(ctx, buf.u32(), P, P, 0, true, st);
+    if (rc) return rc;
+    pw_key2_kernel<<<pw_grid(N, P), 256, 0, st>>>(buf.u32(), key->d_kb, key->d_ka, P, N,
+                                                  ctx->d_pinfo);
+    HG_LAUNCH_CHECK(ctx);
+    uint32_t* t = buf.u32() + (size_t)P * N;
+    rc = hg_ntt_launch(ctx, t, 2 * P, P, 0, false, st);
+    if (rc) return rc;
+    OutSet outs{};
+    outs.out[0] = out0; outs.out[1] = out1;
+    return launch_crt(ctx, t, 2, P, key->big_l, key->level, outs, st);
+}
+
+// ---- fused scheme ops ------------------------------------------------------------------------------
+extern "C" int hg_ct_mult(hg_ctx* ctx, const hg_key* evk, const uint32_t* a0, const uint32_t* a1,
+                          const uint32_t* b0, const uint32_t* b1, int level, int rescale_bits,
+                          uint32_t* out0, uint32_t* out1, void* stream) {
+    if (!ctx || !evk || evk->level != level || rescale_bits < 0 || rescale_bits >= level)
+        return hg_fail(HG_EINVAL, "hg_ct_mult: bad arguments (evk must be prepared at the level)");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int N = ctx->N;
+    const int W = words_for_bits(level);
+    Scratch buf(st);
+    HG_CUDA_TRY(buf.alloc((size_t)5 * W * N * 4));
+    uint32_t* d0 = buf.u32();
+    uint32_t* d1 = d0 + (size_t)W * N;
+    uint32_t* d2 = d1 + (size_t)W * N;
+    uint32_t* e0 = d2 + (size_t)W * N;
+    uint32_t* e1 = e0 + (size_t)W * N;
+    hg_operand o[4] = {{a0, level, 1}, {a1, level, 1}, {b0, level, 1}, {b1, level, 1}};
+    int rc = hg_poly_tensor(ctx, d0, d1, d2, level, o[0], o[1], o[2], o[3], stream);
+    if (rc) return rc;
+    rc = hg_keyswitch(ctx, evk, d2, 1, e0, e1, stream);
+    if (rc) return rc;
+    if (rescale_bits == 0) {
+        rc = hg_ew_add(ctx, out0, d0, e0, level, false, st);
+        if (!rc) rc = hg_ew_add(ctx, out1, d1, e1, level, false, st);
+        return rc;
+    }
+    rc = hg_ew_add(ctx, d0, d0, e0, level, false, st);
+    if (!rc) rc = hg_ew_add(ctx, d1, d1, e1, level, false, st);
+    if (!rc) rc = hg_ew_divide_round(ctx, out0, level - rescale_bits, d0, level, rescale_bits, st);
+    if (!rc) rc = hg_ew_divide_round(ctx, out1, level - rescale_bits, d1, level, rescale_bits, st);
+    return rc;
+}
+
+extern "C" int hg_ct_automorph(hg_ctx* ctx, const hg_key* key, const uint32_t* c0,
+                               const uint32_t* c1, int level, int64_t k, uint32_t* out0,
+                               uint32_t* out1, void* stream) {
+    if (!ctx || !key || key->level != level)
+        return hg_fail(HG_EINVAL, "hg_ct_automorph: bad arguments (key must be prepared at the level)");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int N = ctx->N;
+    const int W = words_for_bits(level);
+    Scratch buf(st);
+    HG_CUDA_TRY(buf.alloc((size_t)2 * W * N * 4));
+    uint32_t* a0 = buf.u32();
+    uint32_t* e0 = a0 + (size_t)W * N;
+    int rc = hg_ew_automorphism(ctx, a0, c0, level, k, st);
+    if (rc) return rc;
+    rc = hg_keyswitch(ctx, key, c1, k, e0, out1, stream);
+    if (rc) return rc;
+    return hg_ew_add(ctx, out0, a0, e0, level, false, st);
+}

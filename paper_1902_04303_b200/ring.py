@@ -1,0 +1,346 @@
+"""Device-resident ring elements of Z_{2^mod_bits}[x]/(x^N + 1).
+
+Mirrors the reference's ``RingElement`` (hegwas/ring.py:68-209): same constructor,
+same canonical representatives in [0, 2^mod_bits), same method names and semantics.
+The coefficients live in HBM as a limb-major ``[W][N]`` uint32 array (stored in an
+int32 torch tensor, W = ceil(mod_bits/32)); every arithmetic method is one or more
+sm_100a kernels behind the C-ABI (include/hegwas_b200.h).  Reading ``coeffs``
+downloads to Python ints (test / client use only).
+
+The exact negacyclic product that the reference computes by Kronecker substitution
+into one big integer (ring.py:46-58) is computed by the native RNS/NTT engine.  A
+ring element may also carry a *compact* view: a two's-complement copy of its centered
+representative at a small width (plaintexts, secrets, ephemerals), which lets products
+mod 2^k use far fewer NTT primes (mod-2^k products are representative independent,
+SURVEY §8a R3).
+
+The host-side samplers and ``derive_rng`` restate ring.py:214-255 draw for draw, so
+keys and ciphertexts generated from a ``random.Random`` are identical to the reference's.
+"""
+from __future__ import annotations
+
+import hashlib
+import math
+import random
+
+import numpy as np
+
+from . import _lib
+from .errors import ParameterError
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def words_for(bits: int) -> int:
+    return (bits + 31) >> 5
+
+
+def ints_to_words(coeffs, bits: int) -> np.ndarray:
+    """Python ints (any sign) -> [W][N] uint32, reduced mod 2^bits."""
+    w = words_for(bits)
+    mask = (1 << bits) - 1
+    width = 4 * w
+    buf = b"".join((c & mask).to_bytes(width, "little") for c in coeffs)
+    arr = np.frombuffer(buf, dtype="<u4").reshape(len(coeffs), w)
+    return np.ascontiguousarray(arr.T)
+
+
+def words_to_ints(arr: np.ndarray) -> list[int]:
+    """[W][N] uint32 -> list of N nonnegative Python ints."""
+    arr = np.asarray(arr, dtype=np.uint32)
+    w, n = arr.shape
+    raw = np.ascontiguousarray(arr.T).astype("<u4").tobytes()
+    width = 4 * w
+    return [int.from_bytes(raw[i * width:(i + 1) * width], "little") for i in range(n)]
+
+
+def _device():
+    torch = _torch()
+    if not torch.cuda.is_available():
+        raise _lib.DeviceError("no CUDA device: the B200 evaluator has no CPU fallback")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def upload_words(arr: np.ndarray):
+    torch = _torch()
+    host = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.uint32).view(np.int32))
+    return host.to(_device(), non_blocking=False)
+
+
+def download_words(t) -> np.ndarray:
+    return t.detach().cpu().numpy().view(np.uint32)
+
+
+def empty_words(bits: int, n: int):
+    torch = _torch()
+    return torch.empty((words_for(bits), n), dtype=torch.int32, device=_device())
+
+
+def _ctx(n: int) -> _lib.Context:
+    return _lib.get_context(n.bit_length() - 1)
+
+
+class RingElement:
+    """Element of Z_{2^mod_bits}[x]/(x^n + 1), resident in device memory."""
+
+    __slots__ = ("n", "mod_bits", "words", "compact_words", "compact_bits", "__weakref__")
+
+    def __init__(self, n: int, mod_bits: int, coeffs=None, *, _reduced: bool = False,
+                 words=None, compact=None):
+        if n & (n - 1) or n < 1:
+            raise ParameterError(f"ring degree {n} is not a power of two")
+        if mod_bits < 1:
+            raise ParameterError("modulus must be at least 2^1")
+        self.n = n
+        self.mod_bits = mod_bits
+        self.compact_words = None
+        self.compact_bits = 0
+        if words is not None:
+            if tuple(words.shape) != (words_for(mod_bits), n):
+                raise ParameterError(f"word array shape {tuple(words.shape)} != ({words_for(mod_bits)}, {n})")
+            self.words = words
+        else:
+            if coeffs is None or len(coeffs) != n:
+                raise ParameterError(f"expected {n} coefficients, got {0 if coeffs is None else len(coeffs)}")
+            self.words = upload_words(ints_to_words(coeffs, mod_bits))
+        if compact is not None:
+            self.compact_words, self.compact_bits = compact
+
+    # -- constructors -----------------------------------------------------------------
+    @classmethod
+    def zero(cls, n: int, mod_bits: int) -> "RingElement":
+        torch = _torch()
+        w = torch.zeros((words_for(mod_bits), n), dtype=torch.int32, device=_device())
+        return cls(n, mod_bits, words=w)
+
+    @classmethod
+    def from_signed(cls, n: int, mod_bits: int, signed) -> "RingElement":
+        """Element with the given signed coefficients; small values also get a compact view."""
+        signed = list(signed)
+        if len(signed) != n:
+            raise ParameterError(f"expected {n} coefficients, got {len(signed)}")
+        top = max((abs(c) for c in signed), default=0)
+        el = cls(n, mod_bits, signed)
+        cb = top.bit_length() + 1  # two's complement width holding every value
+        if cb < mod_bits:
+            el.compact_words = upload_words(ints_to_words(signed, cb))
+            el.compact_bits = cb
+        return el
+
+    @classmethod
+    def from_words(cls, n: int, mod_bits: int, words) -> "RingElement":
+        return cls(n, mod_bits, words=words)
+
+    # -- host views ----------------------------------------------------------------------
+    @property
+    def coeffs(self) -> list[int]:
+        return words_to_ints(download_words(self.words))
+
+    def centered(self) -> list[int]:
+        """Signed representatives in (-2^(bits-1), 2^(bits-1)] (ring.py:106-110)."""
+        half = 1 << (self.mod_bits - 1)
+        full = 1 << self.mod_bits
+        return [c - full if c > half else c for c in self.coeffs]
+
+    def numpy_words(self) -> np.ndarray:
+        return download_words(self.words)
+
+    # -- helpers ---------------------------------------------------------------------------
+    def _require_same(self, other: "RingElement"):
+        if self.n != other.n or self.mod_bits != other.mod_bits:
+            raise ParameterError(
+                f"ring mismatch: (n={self.n}, bits={self.mod_bits}) vs "
+                f"(n={other.n}, bits={other.mod_bits})"
+            )
+
+    def _new(self, bits: int | None = None) -> "RingElement":
+        bits = self.mod_bits if bits is None else bits
+        return RingElement(self.n, bits, words=empty_words(bits, self.n))
+
+    def operand(self, out_bits: int) -> _lib.Operand:
+        """Narrowest legal view of this element for a product reduced mod 2^out_bits."""
+        if self.compact_words is not None and out_bits <= self.mod_bits:
+            return _lib.operand(self.compact_words, self.compact_bits, True)
+        if out_bits <= self.mod_bits:
+            return _lib.operand(self.words, self.mod_bits, True)   # centered representative
+        return _lib.operand(self.words, self.mod_bits, False)      # canonical representative
+
+    # -- arithmetic (ring.py:114-196) -----------------------------------------------------
+    def add(self, other: "RingElement") -> "RingElement":
+        self._require_same(other)
+        out = self._new()
+        ctx = _ctx(self.n)
+        _lib.check(ctx.lib.hg_poly_add(ctx.handle, out.words.data_ptr(), self.words.data_ptr(),
+                                       other.words.data_ptr(), self.mod_bits, ctx.stream()))
+        return out
+
+    def sub(self, other: "RingElement") -> "RingElement":
+        self._require_same(other)
+        out = self._new()
+        ctx = _ctx(self.n)
+        _lib.check(ctx.lib.hg_poly_sub(ctx.handle, out.words.data_ptr(), self.words.data_ptr(),
+                                       other.words.data_ptr(), self.mod_bits, ctx.stream()))
+        return out
+
+    def neg(self) -> "RingElement":
+        out = self._new()
+        ctx = _ctx(self.n)
+        _lib.check(ctx.lib.hg_poly_neg(ctx.handle, out.words.data_ptr(), self.words.data_ptr(),
+                                       self.mod_bits, ctx.stream()))
+        if self.compact_words is not None:
+            pass  # negation of a compact view is not cached
+        return out
+
+    def scalar_mul(self, k: int) -> "RingElement":
+        out = self._new()
+        scalar_mul_into(out.words, self.words, self.mod_bits, k, self.n)
+        return out
+
+    def mul(self, other: "RingElement") -> "RingElement":
+        self._require_same(other)
+        return self.mul_mod(other, self.mod_bits)
+
+    def mul_mod(self, other: "RingElement", out_bits: int) -> "RingElement":
+        """Product reduced mod 2^out_bits; operands may carry different moduli (ring.py:145)."""
+        if self.n != other.n:
+            raise ParameterError("ring degree mismatch")
+        out = self._new(out_bits)
+        ctx = _ctx(self.n)
+        _lib.check(ctx.lib.hg_poly_mul(ctx.handle, out.words.data_ptr(), out_bits,
+                                       self.operand(out_bits), other.operand(out_bits),
+                                       ctx.stream()))
+        return out
+
+    def automorphism(self, k: int) -> "RingElement":
+        """x -> x^k for odd k (ring.py:152-166)."""
+        if k % 2 == 0:
+            raise ParameterError("automorphism exponent must be odd")
+        out = self._new()
+        ctx = _ctx(self.n)
+        _lib.check(ctx.lib.hg_poly_automorphism(ctx.handle, out.words.data_ptr(),
+                                                self.words.data_ptr(), self.mod_bits,
+                                                int(k % (2 * self.n)), ctx.stream()))
+        return out
+
+    def reduce_to(self, bits: int) -> "RingElement":
+        if bits > self.mod_bits:
+            raise ParameterError(f"cannot reduce modulus upward ({self.mod_bits} -> {bits})")
+        if bits == self.mod_bits:
+            return self
+        out = self._new(bits)
+        ctx = _ctx(self.n)
+        _lib.check(ctx.lib.hg_poly_reduce_to(ctx.handle, out.words.data_ptr(), bits,
+                                             self.words.data_ptr(), self.mod_bits, ctx.stream()))
+        if self.compact_words is not None and self.compact_bits < bits:
+            out.compact_words, out.compact_bits = self.compact_words, self.compact_bits
+        return out
+
+    def lift_centered_to(self, bits: int) -> "RingElement":
+        if bits < self.mod_bits:
+            raise ParameterError("lift target smaller than current modulus")
+        out = self._new(bits)
+        ctx = _ctx(self.n)
+        _lib.check(ctx.lib.hg_poly_lift_centered(ctx.handle, out.words.data_ptr(), bits,
+                                                 self.words.data_ptr(), self.mod_bits,
+                                                 ctx.stream()))
+        if self.compact_words is not None:
+            out.compact_words, out.compact_bits = self.compact_words, self.compact_bits
+        return out
+
+    def divide_round(self, shift: int, out_bits: int) -> "RingElement":
+        """((c + 2^(shift-1)) >> shift) mod 2^out_bits (ring.py:184-196)."""
+        out = self._new(out_bits)
+        ctx = _ctx(self.n)
+        _lib.check(ctx.lib.hg_poly_divide_round(ctx.handle, out.words.data_ptr(), out_bits,
+                                                self.words.data_ptr(), self.mod_bits, shift,
+                                                ctx.stream()))
+        return out
+
+    # -- dunder ------------------------------------------------------------------------------
+    def __eq__(self, other):
+        if not isinstance(other, RingElement):
+            return False
+        if self.n != other.n or self.mod_bits != other.mod_bits:
+            return False
+        return bool(_torch().equal(self.words, other.words))
+
+    def __hash__(self):
+        return id(self)
+
+    def __repr__(self):
+        return f"RingElement(n={self.n}, mod_bits={self.mod_bits}, device)"
+
+
+def scalar_mul_into(out_words, a_words, bits: int, k: int, n: int):
+    """out = a * k mod 2^bits for an arbitrary Python integer k."""
+    kk = k & ((1 << bits) - 1)
+    kw = max(1, words_for(kk.bit_length()))
+    arr = (_lib.ctypes.c_uint32 * kw)(*[(kk >> (32 * i)) & 0xFFFFFFFF for i in range(kw)])
+    ctx = _ctx(n)
+    if out_words.data_ptr() == a_words.data_ptr() and kw > 1:
+        raise ParameterError("in-place scalar multiply needs a one-word scalar")
+    _lib.check(ctx.lib.hg_poly_scalar_mul(ctx.handle, out_words.data_ptr(), a_words.data_ptr(),
+                                          bits, arr, kw, ctx.stream()))
+
+
+# -- coefficient samplers (host; restate ring.py:214-246 draw for draw) ------------------------
+
+def sample_uniform(n: int, bits: int, rng: random.Random) -> list[int]:
+    return [rng.getrandbits(bits) for _ in range(n)]
+
+
+def sample_gaussian(n: int, sigma: float, rng: random.Random) -> list[int]:
+    """Rounded N(0, sigma^2), redrawing anything beyond 6 sigma."""
+    cut = 6.0 * sigma
+    out: list[int] = []
+    gauss = rng.gauss
+    while len(out) < n:
+        x = gauss(0.0, sigma)
+        if abs(x) <= cut:
+            out.append(round(x))
+    return out
+
+
+def sample_hamming(n: int, h: int, rng: random.Random) -> list[int]:
+    """Exactly h nonzero coefficients in {-1, +1} at distinct positions."""
+    if h > n:
+        raise ParameterError(f"Hamming weight {h} exceeds degree {n}")
+    out = [0] * n
+    for pos in rng.sample(range(n), h):
+        out[pos] = 1 if rng.getrandbits(1) else -1
+    return out
+
+
+def sample_ternary(n: int, rng: random.Random) -> list[int]:
+    """{-1, 0, 1} with probabilities 1/4, 1/2, 1/4 from two random bits each."""
+    table = (1, 0, 0, -1)
+    return [table[rng.getrandbits(2)] for _ in range(n)]
+
+
+def derive_rng(seed: int, *labels) -> random.Random:
+    """Child generator for (seed, labels), seeded from a 64-bit blake2b digest."""
+    tag = "/".join(str(x) for x in labels)
+    digest = hashlib.blake2b(f"{seed}:{tag}".encode(), digest_size=8).digest()
+    return random.Random(int.from_bytes(digest, "little"))
+
+
+def negacyclic_mul_host(a: list[int], b: list[int], n: int) -> list[int]:
+    """Host negacyclic product for tiny rings (n <= 8), used only by client helpers."""
+    out = [0] * n
+    for i, x in enumerate(a):
+        for j, y in enumerate(b):
+            if i + j < n:
+                out[i + j] += x * y
+            else:
+                out[i + j - n] -= x * y
+    return out
+
+
+__all__ = [
+    "RingElement", "sample_uniform", "sample_gaussian", "sample_hamming", "sample_ternary",
+    "derive_rng", "ints_to_words", "words_to_ints", "words_for", "math",
+]
