@@ -163,7 +163,7 @@ int hg_ntt_launch(hg_ctx* ctx, uint32_t* data, int rows, int P, int prime_offset
     const int chunk = 1 << k2;
     const int lo_threads = chunk / 2 < 256 ? (chunk / 2 < 32 ? 32 : chunk / 2) : 256;
     dim3 glo(N / chunk, rows);
-    dim3 ghi(k1 > 0 ? N / (kTile >> k1) : 1, rows);
+    dim3 ghi(k1 > 0 ? N / kTile : 1, rows);  // 2^k2 columns / (kTile >> k1) per tile
     const uint32_t* tw = forward ? ctx->d_psi : ctx->d_ipsi;
     const uint32_t* twsh = forward ? ctx->d_psi_sh : ctx->d_ipsi_sh;
     if (forward) {

@@ -67,7 +67,10 @@ def _device():
 
 def upload_words(arr: np.ndarray):
     torch = _torch()
-    host = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.uint32).view(np.int32))
+    arr = np.ascontiguousarray(arr, dtype=np.uint32)
+    if not arr.flags.writeable:
+        arr = arr.copy()
+    host = torch.from_numpy(arr.view(np.int32))
     return host.to(_device(), non_blocking=False)
 
 

@@ -47,7 +47,7 @@ def main():
             allok &= check(f"automorphism k={k} n={n}", A.automorphism(k).coeffs, R.automorphism(a, k, bits))
         allok &= check(f"reduce_to n={n}", A.reduce_to(bits - 37).coeffs, R.reduce_to(a, bits - 37))
         allok &= check(f"lift n={n}", A.lift_centered_to(bits + 77).coeffs, R.lift_centered_to(a, bits, bits + 77))
-        for sh in (0, 1, 45, 64, 30):
+        for sh in [s for s in (0, 1, 45, 64, 30) if s < bits]:
             allok &= check(f"divide_round sh={sh} n={n}", A.divide_round(sh, bits - sh).coeffs,
                            R.divide_round(a, sh, bits - sh))
         t = time.time()
