@@ -1,0 +1,123 @@
+"""Pin the CPU oracle against golden vectors produced by the reference package itself.
+
+Every case recomputes a reference output from the golden inputs with oracle/ and demands
+bit equality (these run without a GPU)."""
+import pytest
+
+from oracle import ckks_oracle as C
+from oracle import ring_oracle as R
+
+
+def _ct(g, name):
+    c0, lv = g.ints(name + ".c0")
+    c1, _ = g.ints(name + ".c1")
+    return c0, c1, lv
+
+
+@pytest.fixture(params=["unit_ops", "deep_ops"])
+def case(request, golden):
+    g = golden(request.param)
+    log_n, log_l, log_p, log_p_small, h = g.params_tuple()
+    return g, log_n, log_l, log_p, log_p_small
+
+
+def _keys(g, log_n, log_l):
+    if "evk.b" in g:
+        return {k: g.ints(k)[0] for k in ("evk.b", "evk.a", "rot1.b", "rot1.a", "conj.b", "conj.a")}
+    return None
+
+
+def test_kronecker_matches_schoolbook_known_answer():
+    # ring.py:29-58 property at the reference's test sizes (test_ring.py:23-36)
+    import random
+
+    for n, bits in ((16, 1), (32, 77), (64, 200), (64, 2400)):
+        rng = random.Random(n * bits)
+        a = [rng.getrandbits(bits) for _ in range(n)]
+        b = [rng.getrandbits(bits) for _ in range(n)]
+        assert R.negacyclic_mul(a, b, n, bits, bits) == R.schoolbook_negacyclic(a, b, n)
+
+
+def test_wraparound_sign():
+    n = 16
+    a = [0] * n
+    a[n - 1] = 1
+    b = [0] * n
+    b[1] = 1
+    out = R.schoolbook_negacyclic(a, b, n)
+    assert out[0] == -1 and not any(out[1:])
+
+
+def test_oracle_rescale_and_moddown(case):
+    g, log_n, log_l, log_p, _ = case
+    a0, a1, lv = _ct(g, "ct_a")
+    r0, r1 = C.rescale(a0, a1, 30, lv)
+    assert (r0, r1) == (g.ints("rescale30.c0")[0], g.ints("rescale30.c1")[0])
+    md0, md1, md_lv = _ct(g, "mod_down")
+    assert R.reduce_to(a0, md_lv) == md0 and R.reduce_to(a1, md_lv) == md1
+
+
+def test_oracle_integer_and_negation(case):
+    g, *_ = case
+    a0, a1, lv = _ct(g, "ct_a")
+    assert R.scalar_mul(a0, 4, lv) == g.ints("mult_int_4.c0")[0]
+    assert R.scalar_mul(a1, -1, lv) == g.ints("mult_int_m1.c1")[0]
+
+
+def test_oracle_mult_and_keyswitch_unit(golden):
+    g = golden("unit_ops")
+    log_n, log_l, log_p, _, _ = g.params_tuple()
+    n = 1 << log_n
+    a0, a1, lv = _ct(g, "ct_a")
+    b0, b1, _ = _ct(g, "ct_b")
+    evb, _ = g.ints("evk.b")
+    eva, _ = g.ints("evk.a")
+    e0, e1 = C.keyswitch(a1, evb, eva, lv, log_l, n)
+    assert e0 == g.ints("keyswitch.e0")[0] and e1 == g.ints("keyswitch.e1")[0]
+    m0, m1 = C.mult(a0, a1, b0, b1, lv, evb, eva, log_l, n)
+    assert (m0, m1) == (g.ints("mult_raw.c0")[0], g.ints("mult_raw.c1")[0])
+    r0, r1 = C.engine_mult(a0, a1, b0, b1, lv, evb, eva, log_l, log_p, n)
+    assert (r0, r1) == (g.ints("eng_mult.c0")[0], g.ints("eng_mult.c1")[0])
+
+
+def test_oracle_rotations_unit(golden):
+    g = golden("unit_ops")
+    log_n, log_l, *_ = g.params_tuple()
+    n = 1 << log_n
+    a0, a1, lv = _ct(g, "ct_a")
+    kb, _ = g.ints("rot1.b")
+    ka, _ = g.ints("rot1.a")
+    k = C.rotation_exponent(log_n, 1)
+    o = C.apply_automorphism(a0, a1, k, kb, ka, lv, log_l, n)
+    assert o == (g.ints("rot1.c0")[0], g.ints("rot1.c1")[0])
+    cb, _ = g.ints("conj.b")
+    ca, _ = g.ints("conj.a")
+    o = C.apply_automorphism(a0, a1, 2 * n - 1, cb, ca, lv, log_l, n)
+    assert o == (g.ints("conj.c0")[0], g.ints("conj.c1")[0])
+    # composite right rotation by 5 = 1 then 4 (ckks.py:264-272)
+    k4b, _ = g.ints("rot4.b")
+    k4a, _ = g.ints("rot4.a")
+    c0, c1 = C.apply_automorphism(a0, a1, k, kb, ka, lv, log_l, n)
+    c0, c1 = C.apply_automorphism(c0, c1, C.rotation_exponent(log_n, 4), k4b, k4a, lv, log_l, n)
+    assert (c0, c1) == (g.ints("rot5.c0")[0], g.ints("rot5.c1")[0])
+
+
+def test_oracle_mult_plain_mask(case):
+    g, log_n, log_l, log_p, log_p_small = case
+    n = 1 << log_n
+    a0, a1, lv = _ct(g, "ct_a")
+    m, mbits = g.ints("mask_slot3")
+    p0, p1 = C.mult_plain(a0, a1, m, mbits, lv, n)
+    r0, r1 = C.rescale(p0, p1, log_p_small, lv)
+    assert (r0, r1) == (g.ints("mult_plain_mask.c0")[0], g.ints("mult_plain_mask.c1")[0])
+
+
+def test_oracle_decrypt_unit(golden):
+    g = golden("unit_ops")
+    log_n, *_ = g.params_tuple()
+    n = 1 << log_n
+    c0, c1, lv = _ct(g, "eng_mult")
+    s, sbits = g.ints("sk.s")
+    s_l = R.reduce_to(s, lv)
+    m = R.add(c0, R.mul(c1, s_l, lv, n), lv)
+    assert m == g.ints("decrypt_eng_mult")[0]
