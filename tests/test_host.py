@@ -1,0 +1,152 @@
+"""CPU-only tests: the native library's exported surface, host logic (params, counters,
+GWAS configuration), and host-side algorithms that must be bit-identical to the
+reference (encoding, samplers) checked against the golden fixtures."""
+import math
+import os
+import random
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_every_header_symbol():
+    import ctypes
+
+    from paper_1902_04303_b200 import _lib
+
+    header = open(os.path.join(ROOT, "include", "hegwas_b200.h")).read()
+    declared = set(re.findall(r"\b(hg_[a-z0-9_]+)\s*\(", header))
+    assert len(declared) >= 25
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    for name in sorted(declared):
+        assert hasattr(lib, name), f"{name} declared in the header but not exported"
+    assert set(_lib.SIGNATURES) == declared
+    assert _lib.load_library().hg_version() == 1
+
+
+def test_params_validation_and_json():
+    from paper_1902_04303_b200 import CkksParams, ParameterError, P17, security_status
+
+    with pytest.raises(ParameterError):
+        CkksParams(log_n=4, log_l=120, log_p=45, log_p_small=10, h=99)
+    with pytest.raises(ParameterError):
+        CkksParams(log_n=21, log_l=120)
+    with pytest.raises(ParameterError):
+        CkksParams(log_n=8, log_l=40, log_p=45)
+    assert CkksParams.from_json(P17.to_json()) == P17
+    with pytest.raises(ParameterError):
+        CkksParams.from_json('{"log_n": 8, "log_l": 100, "bogus": 1}')
+    assert security_status(P17)[0] == "accepted"
+    assert security_status(CkksParams(log_n=17, log_l=2440))[0] == "warn"
+
+
+def test_op_counter_nesting():
+    from paper_1902_04303_b200 import instrument
+
+    with instrument.track_ops() as outer:
+        instrument.record(ct_mults=1, keyswitches=1)
+        with instrument.track_ops() as inner:
+            instrument.record(rotations=1, keyswitches=1, rotation_amounts=[4])
+    assert outer.snapshot()["keyswitches"] == 2 and inner.snapshot()["keyswitches"] == 1
+    assert outer.rotation_amounts == [4] and outer.all_rotations_power_of_two()
+    c = instrument.OpCounter()
+    c.merge(outer)
+    assert c.snapshot() == outer.snapshot()
+
+
+def test_gwas_config_capacity_rules():
+    from paper_1902_04303_b200 import CkksParams, ParameterError
+    from paper_1902_04303_b200.gwas import GwasConfig, default_tau
+
+    # n=245 does not fit at log_n=16 (256 x 245 > 32768 slots)
+    with pytest.raises(ParameterError):
+        GwasConfig(n=245, d=4, k=256).resolve(CkksParams(log_n=16, log_l=1700, log_p_small=30))
+    p17 = CkksParams(log_n=17, log_l=1700, log_p_small=30)
+    cfg = GwasConfig(n=245, d=4, k=10643).resolve(p17)
+    assert cfg.tau == default_tau(p17, 245) == 512
+    assert cfg.num_batches == 21 and cfg.cols_per_batch == 256
+    # n=6000 is beyond any supported ring
+    with pytest.raises(ParameterError):
+        GwasConfig(n=6000, d=4, k=100000).resolve(CkksParams(log_n=20, log_l=1700, log_p_small=30))
+
+
+def test_fuse_snp_pairs_and_assemble():
+    from paper_1902_04303_b200.gwas import assemble_result, fuse_snp_pairs
+
+    s = np.arange(15, dtype=float).reshape(3, 5)
+    f = fuse_snp_pairs(s)
+    assert f.shape == (3, 3)
+    assert np.array_equal(f.real, s[:, 0::2]) and np.array_equal(f.imag[:, :2], s[:, 1::2])
+    assert np.all(f.imag[:, 2] == 0)
+    res = assemble_result(np.array([1.0, 2.0, 3.0]), np.array([4.0, 0.0, -1.0]))
+    assert res.effects[0] == 0.25 and math.isnan(res.effects[1]) and math.isnan(res.p_values[2])
+    assert res.p_values[0] == pytest.approx(math.erfc(0.25 * 2 / math.sqrt(2)))
+
+
+def test_words_roundtrip():
+    from paper_1902_04303_b200.ring import ints_to_words, words_to_ints
+
+    rng = random.Random(3)
+    for bits in (1, 31, 32, 33, 350, 1700):
+        vals = [rng.getrandbits(bits) for _ in range(17)] + [0, (1 << bits) - 1]
+        w = ints_to_words(vals, bits)
+        assert w.shape == ((bits + 31) // 32, 19)
+        assert words_to_ints(w) == vals
+    assert words_to_ints(ints_to_words([-1, -5], 40)) == [(1 << 40) - 1, (1 << 40) - 5]
+
+
+@pytest.mark.parametrize("name", ["unit_ops", "deep_ops"])
+def test_encoding_bit_identical_to_reference(golden, name):
+    from paper_1902_04303_b200 import CkksParams
+    from paper_1902_04303_b200.encoding import decode_coefficients, encode_coefficients
+    from paper_1902_04303_b200.ring import ints_to_words
+
+    g = golden(name)
+    log_n, log_l, log_p, log_p_small, h = g.params_tuple()
+    params = CkksParams(log_n=log_n, log_l=log_l, log_p=log_p, log_p_small=log_p_small, h=h)
+    want, bits = g.words("encode_a")
+    got = ints_to_words(encode_coefficients(g.arr("vec_a"), log_p, params), bits)
+    assert np.array_equal(got, want)
+    vec = np.zeros(params.slot_count)
+    vec[3] = 1.0
+    want, bits = g.words("mask_slot3")
+    assert np.array_equal(ints_to_words(encode_coefficients(vec, log_p_small, params), bits), want)
+    # decode of the reference's decrypted product
+    m, mbits = g.ints("decrypt_eng_mult")
+    half, full = 1 << (mbits - 1), 1 << mbits
+    cen = [c - full if c > half else c for c in m]
+    scale = int(g.meta("eng_mult")["scale_bits"])
+    assert np.array_equal(decode_coefficients(cen, scale, params.n), g.arr("decoded_eng_mult"))
+
+
+def test_samplers_reproduce_reference_keys(golden):
+    """Secret and uniform key parts involve no products: check the host RNG restatement."""
+    from paper_1902_04303_b200.ring import derive_rng, ints_to_words, sample_hamming, sample_uniform
+
+    g = golden("unit_ops")
+    log_n, log_l, log_p, log_p_small, h = g.params_tuple()
+    n = 1 << log_n
+    seed = int(g.arr("key_seed"))
+    s = sample_hamming(n, h, derive_rng(seed, "secret"))
+    want, bits = g.words("sk.s")
+    assert np.array_equal(ints_to_words(s, bits), want)
+    a_pk = sample_uniform(n, log_l, derive_rng(seed, "public"))
+    want, bits = g.words("pk.a")
+    assert np.array_equal(ints_to_words(a_pk, bits), want)
+    a_rot = sample_uniform(n, 2 * log_l, derive_rng(seed, "switch", "rot2"))
+    want, bits = g.words("rot2.a")
+    assert np.array_equal(ints_to_words(a_rot, bits), want)
+
+
+def test_synthetic_dataset_shapes():
+    from paper_1902_04303_b200.data import synth_gwas_dataset
+
+    ds = synth_gwas_dataset(245, 4, 256, seed=0)
+    assert ds.X.shape == (245, 5) and ds.S.shape == (245, 256) and ds.y.shape == (245,)
+    assert np.allclose(ds.X[:, 0], 1.0)
+    assert np.allclose(ds.X[:, 1:].mean(axis=0), 0.0, atol=1e-12)
+    assert set(np.unique(ds.y)) <= {0.0, 1.0}
+    assert 0.2 < ds.y.mean() < 0.8
