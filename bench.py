@@ -1,0 +1,423 @@
+"""Benchmark of the encrypted semi-parallel GWAS hot path on B200.
+
+Workload (config.workload): the paper-scale job (BASELINE.json config 3: n=245 samples,
+d=4 covariates, 10643 SNPs, complex-packed 512 SNPs per batch) at the parity preset P17
+(N=2^17, log_l=1700, log_p=45, log_p_small=30).  A *step* is one SNP batch
+of the per-batch hot loop (gwas.py:314-331): the CP x REP projection M S_i (245 fused
+ciphertext multiplies at level 1550) plus the batch statistics (5 ct-mults, 1 pt-mult,
+67 rotations, 1 conjugation).  The setup (logistic regression, w^-1, z, M, z', M_dup) runs
+once before the timed region and is timed separately; `whole_job` combines both into the
+config-3 end-to-end rate.  Inputs are seeded synthetic data with the paper's shapes
+(the iDASH dataset is not distributed); ciphertexts are encrypted with device RNG.
+
+  value : SNPs/s over K timed steps with the batch ciphertexts resident in HBM
+  e2e   : the same steps through the public API with the batch's 245 input ciphertexts
+          copied from pinned host memory every step and the 3 result ciphertexts read back
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+N_SAMPLES, N_COV, K_PAPER = 245, 4, 10643
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--log-n", type=int, default=17)
+    ap.add_argument("--log-l", type=int, default=1700)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (the recipe's clocks line)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[4:8]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        loaded = [s for s in sm if mx and s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------------------------
+def dist_setup():
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and not dist.is_initialized():
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(local)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def load_peaks() -> dict:
+    try:
+        with open(PEAKS_PATH) as f:
+            return json.load(f)
+    except OSError:
+        return {"hbm_gbs": 6650.0, "source": "fallback"}
+
+
+# ---------------------------------------------------------------------------------------------
+def probe_integer_peaks(ctx, torch):
+    """Register-resident probes of the exact instruction mixes the kernels execute."""
+    sink = torch.zeros(4, dtype=torch.int32, device="cuda")
+    out = {}
+    for name, fn, iters in (("butterflies_per_s", ctx.lib.hg_bench_modmul, 8192),
+                            ("macs_per_s", ctx.lib.hg_bench_mac, 4096)):
+        ops = ctypes.c_double()
+        best = 0.0
+        for _ in range(3):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            fn(ctx.handle, iters, ctypes.c_void_p(sink.data_ptr()), ctypes.byref(ops), ctx.stream())
+            e.record()
+            torch.cuda.synchronize()
+            best = max(best, ops.value / (s.elapsed_time(e) / 1e3))
+        out[name] = best
+    return out
+
+
+def run_ours(args, world, rank, local):
+    import numpy as np
+    import torch
+
+    import paper_1902_04303_b200 as hg
+    from paper_1902_04303_b200 import _lib
+    from paper_1902_04303_b200.data import synth_gwas_dataset
+    from paper_1902_04303_b200.gwas import (
+        EncryptedGwasInputs,
+        GwasConfig,
+        SnpBatch,
+        build_snp_batch,
+        compute_batch,
+        compute_setup,
+        encrypt_gwas_inputs,
+    )
+    from paper_1902_04303_b200.matrix import REPMatrix
+    from paper_1902_04303_b200.ring import RingElement
+
+    params = hg.CkksParams(log_n=args.log_n, log_l=args.log_l, log_p=45, log_p_small=30)
+    t_wall0 = time.time()
+    sk, pk, evk, rot = hg.keygen(params, 1000 + rank, device_rng=True)
+    engine = hg.HeEngine(params, evk, rot)
+    ctx = _lib.get_context(params.log_n)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(7 + rank)
+    tau = 2 * params.slot_count // 256
+    ds = synth_gwas_dataset(N_SAMPLES, N_COV, tau, seed=rank)
+    config = GwasConfig(n=N_SAMPLES, d=N_COV, k=K_PAPER).resolve(params)
+    inputs = encrypt_gwas_inputs(ds, GwasConfig(n=N_SAMPLES, d=N_COV, k=tau), params, pk, gen,
+                                 lazy_batches=True)
+    torch.cuda.synchronize()
+    t_keys_inputs = time.time() - t_wall0
+
+    # -- setup (once, timed on the device) ------------------------------------------------------
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    beta, p_prev, inter, m_dup = compute_setup(engine, inputs)
+    e.record()
+    torch.cuda.synchronize()
+    t_setup = s.elapsed_time(e) / 1e3
+
+    # -- one batch of SNP ciphertexts, resident + a pinned host copy --------------------------------
+    batch = build_snp_batch(ds.S, 0, inputs.config, params, pk, gen)
+    rows = batch.S_packed.rows_ct
+    torch.cuda.synchronize()
+    host_rows = []
+    if not args.no_e2e:
+        for ct in rows:
+            host_rows.append((ct.c0.words.cpu().pin_memory(), ct.c1.words.cpu().pin_memory()))
+
+    def step_resident():
+        return compute_batch(engine, inputs, inter, m_dup, batch)
+
+    for _ in range(args.warmup):
+        step_resident()
+    torch.cuda.synchronize()
+
+    # -- timed: K resident steps ----------------------------------------------------------------------
+    launches0 = _lib.total_launches()
+    ctx.set_kernel_timing(True)
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        s.record()
+        outs = [step_resident() for _ in range(args.steps)]
+        e.record()
+        torch.cuda.synchronize()
+    t_steps = s.elapsed_time(e) / 1e3
+    barrier(world)
+    launches = _lib.total_launches() - launches0
+    kstats = {k: ctx.kernel_stats(k) for k in ("crt", "modup", "ntt")}
+    ctx.set_kernel_timing(False)
+    t_steps = max_over_ranks(t_steps, world)
+    del outs
+
+    # -- e2e: host -> device inputs, device -> host results, through the public API ------------------
+    e2e = None
+    if not args.no_e2e:
+        n = params.n
+
+        def step_e2e():
+            dev_rows = []
+            for (h0, h1), ct in zip(host_rows, rows):
+                c0 = RingElement(n, ct.level_bits, words=h0.to("cuda", non_blocking=True))
+                c1 = RingElement(n, ct.level_bits, words=h1.to("cuda", non_blocking=True))
+                dev_rows.append(hg.Ciphertext(c0=c0, c1=c1, level_bits=ct.level_bits,
+                                              scale_bits=ct.scale_bits, slots=ct.slots,
+                                              params=params))
+            b = SnpBatch(index=0, S_packed=REPMatrix(rows_ct=dev_rows, repeat=batch.S_packed.repeat,
+                                                     rows=batch.S_packed.rows,
+                                                     cols_logical=batch.S_packed.cols_logical),
+                         snp_offset=0, snp_count=batch.snp_count, complex_packing=True)
+            out = compute_batch(engine, inputs, inter, m_dup, b)
+            res = [out.num_ct, out.den_even_ct, out.den_odd_ct]
+            host = [(c.c0.words.cpu(), c.c1.words.cpu()) for c in res]
+            return sum(int(a.numel() + b.numel()) * 4 for a, b in host)
+
+        step_e2e()
+        torch.cuda.synchronize()
+        barrier(world)
+        s.record()
+        d2h = 0
+        for _ in range(args.steps):
+            d2h = step_e2e()
+        e.record()
+        torch.cuda.synchronize()
+        t_e2e = max_over_ranks(s.elapsed_time(e) / 1e3, world)
+        h2d = sum(int(a.numel() + b.numel()) * 4 for a, b in host_rows)
+        e2e = {"value": round(tau * args.steps * world / t_e2e, 3), "unit": "SNP/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": round(1e3 * t_e2e / args.steps, 2)}
+
+    peaks = probe_integer_peaks(ctx, torch)
+    return {
+        "params": params, "tau": tau, "t_setup": t_setup, "t_steps": t_steps,
+        "launches": launches, "kstats": kstats, "clocks": clocks.summary(), "e2e": e2e,
+        "peaks": peaks, "t_keys_inputs": t_keys_inputs,
+        "key_cache_gb": round(__import__("paper_1902_04303_b200.ckks", fromlist=["KEY_CACHE"]).KEY_CACHE.bytes / 1e9, 2),
+    }
+
+
+# ---------------------------------------------------------------------------------------------
+def cpu_mult_sample(log_n: int, level: int, big_l: int, log_p: int, seed: int = 0):
+    """Time one HeEngine.mult at (N, level) with the CPU oracle port (gmp-backed exact
+    products) -- the reference algorithm restated, single thread."""
+    import random
+
+    from oracle import ckks_oracle as C
+
+    n = 1 << log_n
+    rng = random.Random(seed)
+    a0, a1, b0, b1 = ([rng.getrandbits(level) for _ in range(n)] for _ in range(4))
+    kb = [rng.getrandbits(2 * big_l) for _ in range(n)]
+    ka = [rng.getrandbits(2 * big_l) for _ in range(n)]
+    t = time.perf_counter()
+    C.engine_mult(a0, a1, b0, b1, level, kb, ka, big_l, log_p, n)
+    return time.perf_counter() - t
+
+
+def cpu_snp_rate(t_mult: float, tau: int, n_mults: int = N_SAMPLES + 5) -> float:
+    """SNP/s of the CPU port on one batch: op-count extrapolation from the dominant op
+    (the batch's ct-mults at level ~1550; rotations and the rest are left out, so this is
+    an upper bound on CPU throughput)."""
+    return tau / (n_mults * t_mult)
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the reference algorithm (CPU oracle port; the reference is pure
+    Python and cannot travel) on all host cores, bounded samples of the same step."""
+    if rank != 0:
+        return None
+    from concurrent.futures import ProcessPoolExecutor
+
+    cores = os.cpu_count() or 1
+    level = args.log_l - 150
+    tau = 2 * (1 << (args.log_n - 1)) // 256
+    times = []
+    total_w = args.warmup + args.steps
+    with ProcessPoolExecutor(max_workers=cores) as ex:
+        # each step: one batch-sized sample = `cores` concurrent mults at level 1550
+        for i in range(total_w):
+            t = time.perf_counter()
+            list(ex.map(cpu_mult_sample, [args.log_n] * cores, [level] * cores,
+                        [args.log_l] * cores, [45] * cores, range(cores)))
+            dt = time.perf_counter() - t
+            if i >= args.warmup:
+                times.append(dt)
+    per_mult = statistics.median(times) / cores  # throughput-equivalent seconds per mult
+    value = cpu_snp_rate(per_mult, tau)
+    line = {
+        "impl": "reference", "metric": "encrypted semi-parallel GWAS SNPs/s", "value": value,
+        "unit": "SNP/s", "higher_is_better": True, "n_gpus": 0, "steps": args.steps,
+        "warmup": args.warmup, "dtype": "u32", "data": "synthetic",
+        "ms_per_step": round(1e3 * statistics.median(times), 1),
+        "config": {"workload": f"config3 per-batch step, P17 (N=2^{args.log_n}, log_l={args.log_l}), "
+                               f"{tau} SNPs/batch, n=245", "scaling": "n/a"},
+        "cpu_baseline": {"value": value, "unit": "SNP/s", "cores": cores, "kind": "port",
+                         "sample": f"{cores} concurrent HeEngine.mult at level {level} per step via "
+                                   "oracle/ (gmp Kronecker products); SNP/s = tau / (250 x t_mult), "
+                                   "rotations excluded (upper bound)"},
+        "e2e": {"value": value, "unit": "SNP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    return line
+
+
+# ---------------------------------------------------------------------------------------------
+def main():
+    args = parse()
+    world, rank, local = dist_setup() if args.impl == "ours" else (
+        int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0)
+    if args.impl == "reference":
+        line = run_reference(args, world, rank)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
+    r = run_ours(args, world, rank, local)
+    if rank != 0:
+        return
+    peaks_file = load_peaks()
+    tau, steps, params = r["tau"], args.steps, r["params"]
+    value = tau * steps * world / r["t_steps"]
+    ms_step = 1e3 * r["t_steps"] / steps
+    nb = math.ceil(K_PAPER / tau)
+    whole = K_PAPER / (r["t_setup"] + nb * r["t_steps"] / steps)
+    ks = r["kstats"]
+    # roofline of the dominant kernel class (integer pipe: CRT reconstruction MACs)
+    dom = max(ks, key=lambda k: ks[k]["ms"])
+    step_ms_total = 1e3 * r["t_steps"]
+    peak_key = "butterflies_per_s" if dom == "ntt" else "macs_per_s"
+    achieved = ks[dom]["work"] / (ks[dom]["ms"] / 1e3) if ks[dom]["ms"] else 0.0
+    roofline = {
+        "bound": "int32", "kernel": {"crt": "crt_kernel", "modup": "modup_kernel",
+                                     "ntt": "ntt_lo/hi_kernel"}[dom],
+        "achieved": round(achieved / 1e9, 1), "peak": round(r["peaks"][peak_key] / 1e9, 1),
+        "unit": "G" + ("butterflies" if dom == "ntt" else "MAC") + "/s",
+        "frac": round(achieved / r["peaks"][peak_key], 4) if r["peaks"][peak_key] else None,
+        "traffic": None,
+        "peak_source": "measured in-run: register-resident probe of the kernel's own instruction mix "
+                       "(MEASURED_PEAKS.json has no integer-pipe figure)",
+        "share_of_step": round(ks[dom]["ms"] / step_ms_total, 3) if step_ms_total else None,
+        "kernel_classes": {k: {"ms_per_step": round(v["ms"] / steps, 2), "launches": v["launches"],
+                               "G_work_per_s": round(v["work"] / (v["ms"] / 1e3) / 1e9, 1) if v["ms"] else 0}
+                           for k, v in ks.items()},
+        "hbm_peak_gbs": peaks_file.get("hbm_gbs"),
+    }
+    cpu = None
+    if not args.no_cpu_baseline and world >= 1:
+        t_cpu = cpu_mult_sample(params.log_n, params.log_l - 150, params.log_l, params.log_p)
+        cpu = {"value": round(cpu_snp_rate(t_cpu, tau), 6), "unit": "SNP/s", "cores": 1, "kind": "port",
+               "sample": f"one HeEngine.mult at N=2^{params.log_n}, level {params.log_l - 150} via oracle/ "
+                         f"({t_cpu:.1f}s, gmp Kronecker); SNP/s = {tau} / (250 x t_mult), rotations excluded"}
+    line = {
+        "metric": "encrypted semi-parallel GWAS SNPs/s", "value": round(value, 3), "unit": "SNP/s",
+        "n_gpus": world, "steps": steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 2),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic (seeded; config-3 shapes, device-RNG encryption)",
+        "config": {"workload": f"config3 per-batch step: n=245, d=4, {tau} SNPs/batch, "
+                               f"P17 (N=2^{params.log_n}, log_l={params.log_l}, log_p=45, log_p_small=30)",
+                   "global_batch_snps": tau * world, "parallelism": f"snp-batch sharding x{world}",
+                   "l2": "inputs > L2 (13 GB of batch ciphertexts per step)"},
+        "whole_job": {"snps": K_PAPER, "batches": nb, "setup_s": round(r["t_setup"], 2),
+                      "value": round(whole, 3), "unit": "SNP/s",
+                      "note": "config-3 end to end on device: setup once + 21 batch steps"},
+        "e2e": r["e2e"], "gpu_launches": r["launches"], "roofline": roofline, "cpu_baseline": cpu,
+        "clocks": r["clocks"], "int_peaks": {k: round(v / 1e9, 1) for k, v in r["peaks"].items()},
+        "key_cache_gb": r["key_cache_gb"], "prep_s": round(r["t_keys_inputs"], 1),
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

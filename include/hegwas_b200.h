@@ -131,8 +131,19 @@ int hg_ntt_inverse(hg_ctx* ctx, uint32_t* data, int count, int prime_offset, voi
 /* Integer-pipe peak microbenchmark: runs the NTT butterfly modmul sequence register-
  * resident on all SMs; returns butterflies executed (host) for `iters`.              */
 int hg_bench_modmul(hg_ctx* ctx, int iters, uint32_t* sink, double* ops_out, void* stream);
+/* Base-conversion MAC probe: the exact fold-every-4 32x32->64 multiply-accumulate of the
+ * ModUp/CRT kernels, register resident; returns MACs executed.                       */
+int hg_bench_mac(hg_ctx* ctx, int iters, uint32_t* sink, double* ops_out, void* stream);
 /* Number of kernel launches issued by this library since context creation. */
 long long hg_launch_count(const hg_ctx* ctx);
+/* Live kernel timing: when enabled, CUDA events bracket every launch of the
+ * instrumented kernel classes (0 = CRT, 1 = ModUp, 2 = NTT, 3 = pointwise,
+ * 4 = elementwise) on the launching stream.  hg_kernel_stats synchronises the recorded
+ * events and returns, for one class, the summed device milliseconds, the number of
+ * launches and the algorithmic work (MACs for CRT/ModUp, butterflies for NTT, bytes
+ * for pointwise/elementwise).  Enabling resets the counters.                        */
+int hg_set_kernel_timing(hg_ctx* ctx, int enabled);
+int hg_kernel_stats(hg_ctx* ctx, int kind, double* ms, long long* launches, double* work);
 
 #ifdef __cplusplus
 }

@@ -65,8 +65,14 @@ SIGNATURES = {
     "hg_ntt_forward": (_i, [_vp, _vp, _i, _i, _vp]),
     "hg_ntt_inverse": (_i, [_vp, _vp, _i, _i, _vp]),
     "hg_bench_modmul": (_i, [_vp, _i, _vp, ctypes.POINTER(ctypes.c_double), _vp]),
+    "hg_bench_mac": (_i, [_vp, _i, _vp, ctypes.POINTER(ctypes.c_double), _vp]),
     "hg_launch_count": (ctypes.c_longlong, [_vp]),
+    "hg_set_kernel_timing": (_i, [_vp, _i]),
+    "hg_kernel_stats": (_i, [_vp, _i, ctypes.POINTER(ctypes.c_double),
+                             ctypes.POINTER(ctypes.c_longlong), ctypes.POINTER(ctypes.c_double)]),
 }
+
+KERNEL_KINDS = {"crt": 0, "modup": 1, "ntt": 2, "pointwise": 3, "elementwise": 4}
 
 _lib = None
 _lock = threading.RLock()
@@ -134,6 +140,16 @@ class Context:
 
     def launches(self) -> int:
         return int(self.lib.hg_launch_count(self.handle))
+
+    def set_kernel_timing(self, enabled: bool):
+        check(self.lib.hg_set_kernel_timing(self.handle, 1 if enabled else 0))
+
+    def kernel_stats(self, kind: str) -> dict:
+        """{'ms', 'launches', 'work'} of the events recorded since timing was enabled."""
+        ms, n, work = ctypes.c_double(), ctypes.c_longlong(), ctypes.c_double()
+        check(self.lib.hg_kernel_stats(self.handle, KERNEL_KINDS[kind], ctypes.byref(ms),
+                                       ctypes.byref(n), ctypes.byref(work)))
+        return {"ms": ms.value, "launches": n.value, "work": work.value}
 
     def __del__(self):  # pragma: no cover - interpreter shutdown ordering
         try:

@@ -47,3 +47,49 @@ extern "C" int hg_bench_modmul(hg_ctx* ctx, int iters, uint32_t* sink, double* o
     if (ops_out) *ops_out = (double)blocks * threads * 8.0 * iters;
     return HG_OK;
 }
+
+// ---- base-conversion MAC probe: 32x32->64 multiply-accumulate with the CRT kernel's
+// fold-every-4 exact accumulation, 8 independent accumulators per thread. ---------------
+namespace {
+__global__ void __launch_bounds__(256) mac_probe_kernel(int iters, uint32_t* sink) {
+    uint64_t acc[8];
+    uint64_t top[8];
+    uint32_t y[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        acc[k] = 0;
+        top[k] = 0;
+        y[k] = (threadIdx.x * 2654435761u + k * 40503u) & 0x3fffffffu;
+    }
+    uint32_t m = blockIdx.x * 97u + 12345u;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) acc[k] += (uint64_t)y[k] * (m + r);
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            top[k] += acc[k] >> 32;
+            acc[k] = (uint32_t)acc[k];
+        }
+        m = m * 1664525u + 1013904223u;
+    }
+    uint64_t s = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s ^= acc[k] ^ top[k];
+    if ((uint32_t)s == 0x12345678u) sink[0] = (uint32_t)s;
+}
+}  // namespace
+
+extern "C" int hg_bench_mac(hg_ctx* ctx, int iters, uint32_t* sink, double* ops_out,
+                            void* stream) {
+    if (!ctx || !sink || iters < 1) return hg_fail(HG_EINVAL, "hg_bench_mac: bad arguments");
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+    const int blocks = sms * 8, threads = 256;
+    mac_probe_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(iters, sink);
+    HG_LAUNCH_CHECK(ctx);
+    if (ops_out) *ops_out = (double)blocks * threads * 8.0 * 4.0 * iters;
+    return HG_OK;
+}

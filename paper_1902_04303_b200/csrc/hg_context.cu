@@ -161,6 +161,64 @@ extern "C" int hg_ctx_primes(const hg_ctx* ctx, uint32_t* out) {
 }
 extern "C" long long hg_launch_count(const hg_ctx* ctx) { return ctx ? ctx->launches.load() : 0; }
 
+// ---- live kernel timing ----------------------------------------------------------------------
+int hg_timer_begin(hg_ctx* ctx, cudaStream_t st) {
+    if (!ctx->timing) return -1;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    hg_ctx::Timer t;
+    if (!ctx->spare.empty()) {
+        t = ctx->spare.back();
+        ctx->spare.pop_back();
+    } else {
+        cudaEventCreate(&t.a);
+        cudaEventCreate(&t.b);
+    }
+    cudaEventRecord(t.a, st);
+    ctx->timers.push_back(t);
+    return (int)ctx->timers.size() - 1;
+}
+
+void hg_timer_end(hg_ctx* ctx, int idx, cudaStream_t st, int kind, double work) {
+    if (idx < 0) return;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (idx >= (int)ctx->timers.size()) return;
+    hg_ctx::Timer& t = ctx->timers[idx];
+    cudaEventRecord(t.b, st);
+    t.kind = kind;
+    t.work = work;
+}
+
+extern "C" int hg_set_kernel_timing(hg_ctx* ctx, int enabled) {
+    if (!ctx) return hg_fail(HG_EINVAL, "null context");
+    HG_CUDA_TRY(cudaDeviceSynchronize());
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    for (auto& t : ctx->timers) ctx->spare.push_back(t);
+    ctx->timers.clear();
+    ctx->timing = enabled != 0;
+    return HG_OK;
+}
+
+extern "C" int hg_kernel_stats(hg_ctx* ctx, int kind, double* ms, long long* launches,
+                               double* work) {
+    if (!ctx || !ms || !launches || !work) return hg_fail(HG_EINVAL, "null argument");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    double tot = 0.0, w = 0.0;
+    long long n = 0;
+    for (auto& t : ctx->timers) {
+        if (t.kind != kind) continue;
+        HG_CUDA_TRY(cudaEventSynchronize(t.b));
+        float e = 0.f;
+        HG_CUDA_TRY(cudaEventElapsedTime(&e, t.a, t.b));
+        tot += e;
+        w += t.work;
+        ++n;
+    }
+    *ms = tot;
+    *launches = n;
+    *work = w;
+    return HG_OK;
+}
+
 extern "C" int hg_sync(hg_ctx* ctx, void* stream) {
     (void)ctx;
     HG_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));

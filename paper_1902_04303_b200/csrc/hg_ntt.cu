@@ -166,6 +166,7 @@ int hg_ntt_launch(hg_ctx* ctx, uint32_t* data, int rows, int P, int prime_offset
     dim3 ghi(k1 > 0 ? N / kTile : 1, rows);  // 2^k2 columns / (kTile >> k1) per tile
     const uint32_t* tw = forward ? ctx->d_psi : ctx->d_ipsi;
     const uint32_t* twsh = forward ? ctx->d_psi_sh : ctx->d_ipsi_sh;
+    HgTimed tm(ctx, stream, HG_K_NTT, (double)rows * (N / 2) * log_n);
     if (forward) {
         if (k1 > 0) {
             ntt_hi_kernel<true><<<ghi, 256, 0, stream>>>(data, log_n, k1, P, prime_offset,

@@ -274,8 +274,13 @@ int launch_modup(hg_ctx* ctx, const OperandSet& ops, int nops, int P, uint32_t* 
     int threads = N < kModupThreads ? N : kModupThreads;
     smem = (size_t)maxw * threads * 4;
     dim3 grid(N / threads, nops);
-    modup_kernel<<<grid, threads, smem, st>>>(ops, N, ctx->log_n, ctx->d_pinfo, ctx->d_modup, P,
-                                              out, kinv);
+    double macs = 0.0;
+    for (int k = 0; k < nops; ++k) macs += (double)words_for_bits(ops.bits[k]) * P * N;
+    {
+        HgTimed tm(ctx, st, HG_K_MODUP, macs);
+        modup_kernel<<<grid, threads, smem, st>>>(ops, N, ctx->log_n, ctx->d_pinfo, ctx->d_modup,
+                                                  P, out, kinv);
+    }
     HG_LAUNCH_CHECK(ctx);
     return HG_OK;
 }
@@ -292,9 +297,12 @@ int launch_crt(hg_ctx* ctx, const uint32_t* res, int nouts, int P, int shift, in
     const int threads = N < kCrtThreads ? N : kCrtThreads;
     size_t smem = (size_t)tab->P4 * threads * 4;
     dim3 grid(N / threads, nouts);
-    crt_kernel<<<grid, threads, smem, st>>>(res, P, tab->P4, N, ctx->d_pinfo, tab->d_M,
+    {
+        HgTimed tm(ctx, st, HG_K_CRT, (double)nouts * N * (double)P * T);
+        crt_kernel<<<grid, threads, smem, st>>>(res, P, tab->P4, N, ctx->d_pinfo, tab->d_M,
                                                 tab->d_negQ, tab->d_cinv, tab->d_cinv_sh,
                                                 tab->d_invp, shift, out_bits, outs);
+    }
     HG_LAUNCH_CHECK(ctx);
     return HG_OK;
 }

@@ -331,6 +331,55 @@ def derive_rng(seed: int, *labels) -> random.Random:
     return random.Random(int.from_bytes(digest, "little"))
 
 
+# -- device samplers (benchmark-scale inputs; not reference-reproducible) ---------------------
+
+def small_element(n: int, bits: int, values) -> RingElement:
+    """Element from small signed integers in a device tensor, with an 8-bit compact view."""
+    torch = _torch()
+    vals = values.to(torch.int64)
+    w = words_for(bits)
+    out = torch.empty((w, n), dtype=torch.int32, device=vals.device)
+    low = vals & 0xFFFFFFFF
+    out[0] = torch.where(low >= 2 ** 31, low - 2 ** 32, low).to(torch.int32)
+    if w > 1:
+        out[1:] = torch.where(vals < 0, -1, 0).to(torch.int32).unsqueeze(0)
+    rem = bits & 31
+    if rem:
+        top = out[w - 1].to(torch.int64) & ((1 << rem) - 1)
+        out[w - 1] = top.to(torch.int32)
+    el = RingElement(n, bits, words=out)
+    el.compact_words, el.compact_bits = (vals & 0xFF).to(torch.int32).unsqueeze(0), 8
+    return el
+
+
+def uniform_element(n: int, bits: int, gen) -> RingElement:
+    """Uniform residues mod 2^bits drawn on the device."""
+    torch = _torch()
+    w = words_for(bits)
+    out = torch.randint(-2 ** 31, 2 ** 31, (w, n), dtype=torch.int32, generator=gen, device=gen.device)
+    rem = bits & 31
+    if rem:
+        out[w - 1] &= (1 << rem) - 1
+    return RingElement(n, bits, words=out)
+
+
+def device_ternary(n: int, gen):
+    torch = _torch()
+    t = torch.randint(0, 4, (n,), generator=gen, device=gen.device)
+    return torch.where(t == 0, 1, torch.where(t == 3, -1, 0))
+
+
+def device_gaussian(n: int, sigma: float, gen):
+    """Rounded N(0, sigma^2) with the 6-sigma tail redrawn (same law as sample_gaussian)."""
+    torch = _torch()
+    x = torch.randn(n, generator=gen, device=gen.device, dtype=torch.float64) * sigma
+    bad = x.abs() > 6.0 * sigma
+    while bool(bad.any()):
+        x[bad] = torch.randn(int(bad.sum()), generator=gen, device=gen.device, dtype=torch.float64) * sigma
+        bad = x.abs() > 6.0 * sigma
+    return torch.round(x).to(torch.int64)
+
+
 def negacyclic_mul_host(a: list[int], b: list[int], n: int) -> list[int]:
     """Host negacyclic product for tiny rings (n <= 8), used only by client helpers."""
     out = [0] * n
