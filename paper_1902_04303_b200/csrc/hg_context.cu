@@ -293,7 +293,9 @@ int hg_get_crt(hg_ctx* ctx, int P, const CrtTable** out) {
     t.P4 = (P + 3) & ~3;
     t.W = (int)std::ceil(ctx->prefix_bits[P] / 32.0) + 2;
     if (t.W < HG_MODUP_WMAX) t.W = HG_MODUP_WMAX;  // any emitted window up to 6144 bits
+    t.W = (t.W + 7) & ~7;                          // 8-column blocks of the CRT kernel
     const int W = t.W;
+    // M is prime-major: row j holds the words of Q/p_j mod 2^(32W) (rows >= P are zero)
     std::vector<uint32_t> M((size_t)W * t.P4, 0u), negQ(W, 0u), cinv(P), cinv_sh(P);
     std::vector<double> invp(P);
     // Q mod 2^(32W) and Q/p_j mod 2^(32W)
@@ -319,7 +321,7 @@ int hg_get_crt(hg_ctx* ctx, int P, const CrtTable** out) {
             mul_small_trunc(Qj, ctx->primes[i]);
             qmodp = mulmod64(qmodp, ctx->primes[i] % pj, pj);
         }
-        for (int w = 0; w < W; ++w) M[(size_t)w * t.P4 + j] = Qj[w];
+        for (int w = 0; w < W; ++w) M[(size_t)j * W + w] = Qj[w];
         uint64_t inv = powmod(qmodp, pj - 2, pj);
         uint64_t ninv = powmod(ctx->N % pj, pj - 2, pj);
         uint64_t r32 = (1ull << 32) % pj;

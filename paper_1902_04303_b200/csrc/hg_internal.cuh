@@ -38,8 +38,8 @@ struct PrimeInfo {
 struct CrtTable {
     int P = 0;
     int P4 = 0;          // P rounded up to a multiple of 4 (row pitch of M)
-    int W = 0;           // column words available
-    uint32_t* d_M = nullptr;      // [W][P4]: word t of (Q/p_j mod 2^(32W)); zero padded
+    int W = 0;           // column words available (multiple of 8)
+    uint32_t* d_M = nullptr;      // [P4][W]: word t of (Q/p_j mod 2^(32W)); zero padded
     uint32_t* d_negQ = nullptr;   // [W]: word t of (-Q mod 2^(32W))
     uint32_t* d_cinv = nullptr;   // [P]: (Q/p_j)^{-1} * N^{-1} * 2^32 mod p_j
     uint32_t* d_cinv_sh = nullptr;

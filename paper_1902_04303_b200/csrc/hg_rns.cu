@@ -46,9 +46,11 @@ __global__ void __launch_bounds__(kModupThreads) modup_kernel(
     int64_t automorph_kinv) {
     extern __shared__ uint32_t ws[];
     const int op = blockIdx.y;
-    const uint32_t* in = ops.words[op];
-    const int bits = ops.bits[op];
-    const int is_signed = ops.is_signed[op];
+    // select, not index: a dynamic index into the parameter struct spills it to the stack
+    const uint32_t* in = op == 0 ? ops.words[0] : op == 1 ? ops.words[1] : op == 2 ? ops.words[2] : ops.words[3];
+    const int bits = op == 0 ? ops.bits[0] : op == 1 ? ops.bits[1] : op == 2 ? ops.bits[2] : ops.bits[3];
+    const int is_signed = op == 0 ? ops.is_signed[0] : op == 1 ? ops.is_signed[1]
+                        : op == 2 ? ops.is_signed[2] : ops.is_signed[3];
     const int W = (bits + 31) >> 5;
     const int TB = blockDim.x;
     const int i = blockIdx.x * TB + threadIdx.x;
@@ -92,6 +94,76 @@ __global__ void __launch_bounds__(kModupThreads) modup_kernel(
             // for signed operands negation is plain -x; for unsigned it is 2^bits - x
             if (is_signed) r = r ? pi.p - r : 0;
             else r = pw >= r ? pw - r : pw + pi.p - r;
+        }
+        outp[(size_t)j * N + i] = r;
+    }
+}
+
+// Register-resident ModUp for operands of at most WB words: the W words of one coefficient
+// stay in registers (zero padded to WB, so no per-word predicate), every prime's constants
+// 2^(32w) mod p are read as warp-uniform 16-byte loads, and the 64-bit accumulator is folded
+// through 2^32 mod p every two products after the first four.
+template <int WB>
+__global__ void __launch_bounds__(128) modup_reg_kernel(
+    OperandSet ops, int N, const PrimeInfo* __restrict__ pinfo,
+    const uint32_t* __restrict__ modup_tab, int P, uint32_t* __restrict__ out,
+    int64_t automorph_kinv) {
+    const int op = blockIdx.y;
+    // select, not index: a dynamic index into the parameter struct spills it to the stack
+    const uint32_t* in = op == 0 ? ops.words[0] : op == 1 ? ops.words[1] : op == 2 ? ops.words[2] : ops.words[3];
+    const int bits = op == 0 ? ops.bits[0] : op == 1 ? ops.bits[1] : op == 2 ? ops.bits[2] : ops.bits[3];
+    const int is_signed = op == 0 ? ops.is_signed[0] : op == 1 ? ops.is_signed[1]
+                        : op == 2 ? ops.is_signed[2] : ops.is_signed[3];
+    const int W = (bits + 31) >> 5;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t top_mask = (bits & 31) ? ((1u << (bits & 31)) - 1u) : 0xffffffffu;
+    int src = i;
+    bool negate = false;
+    if (automorph_kinv != 0) {
+        int64_t j = ((int64_t)i * automorph_kinv) & ((2ll * N) - 1);
+        if (j >= N) { negate = true; j -= N; }
+        src = (int)j;
+    }
+    uint32_t a[WB];
+    uint32_t any = 0;
+#pragma unroll
+    for (int w = 0; w < WB; ++w) {
+        uint32_t v = 0;
+        if (w < W) {
+            v = in[(size_t)w * N + src];
+            if (w == W - 1) v &= top_mask;
+        }
+        any |= v;
+        a[w] = v;
+    }
+    bool sign = false;
+#pragma unroll
+    for (int w = 0; w < WB; ++w)
+        if (w == W - 1) sign = is_signed && ((a[w] >> ((bits - 1) & 31)) & 1u);
+    uint32_t* outp = out + (size_t)op * P * N;
+    for (int j = 0; j < P; ++j) {
+        const PrimeInfo pi = pinfo[j];
+        const uint4* C4 = reinterpret_cast<const uint4*>(modup_tab + (size_t)j * HG_MODUP_WMAX);
+        uint64_t acc = 0;
+#pragma unroll
+        for (int w4 = 0; w4 < WB / 4; ++w4) {
+            const uint4 c = C4[w4];
+            acc += (uint64_t)a[4 * w4] * c.x;
+            acc += (uint64_t)a[4 * w4 + 1] * c.y;
+            if (w4) acc = (uint64_t)(uint32_t)(acc >> 32) * pi.c32 + (uint32_t)acc;
+            acc += (uint64_t)a[4 * w4 + 2] * c.z;
+            acc += (uint64_t)a[4 * w4 + 3] * c.w;
+            acc = (uint64_t)(uint32_t)(acc >> 32) * pi.c32 + (uint32_t)acc;
+        }
+        uint32_t r = reduce_u64(acc, pi);
+        if (sign || negate) {
+            uint32_t pw = reduce_u64((uint64_t)modup_tab[(size_t)j * HG_MODUP_WMAX + (bits >> 5)]
+                                         << (bits & 31), pi);
+            if (sign) r = r >= pw ? r - pw : r + pi.p - pw;
+            if (negate && any) {
+                if (is_signed) r = r ? pi.p - r : 0;
+                else r = pw >= r ? pw - r : pw + pi.p - r;
+            }
         }
         outp[(size_t)j * N + i] = r;
     }
@@ -176,16 +248,96 @@ __global__ void reduce_rows_kernel(uint32_t* __restrict__ a, int N,
 // v = round(sum_j y_j / p_j) (|c| < Q/8 by the prime-count margin, so the float64 estimate
 // is exact).  Column t of c mod 2^(32T) is sum_j y_j M[t][j] + v negQ[t] + carry, scanned
 // low to high; the kernel emits bits [shift, shift + out_bits) of c + 2^(shift-1).
+constexpr int kCrtCols = 8;  // columns accumulated per pass (register blocking)
+
+// Scan columns [tb0, T) of c + round, 8 at a time: every y_j (shared memory) meets 8 column
+// constants (two broadcast 16-byte loads of row j of M) -> 8 exact 32x32->64 MACs; the
+// accumulators are folded every 4 primes so a 64-bit register never overflows.  Emits bits
+// [shift, shift+out_bits).  Returns true if the columns below shift/32 (present only when
+// tb0 > 0, the truncated "fraction" window) are too close to a carry to be trusted.
+__device__ __forceinline__ bool crt_scan(const uint32_t* __restrict__ ys, int TB, int P4,
+                                         const uint32_t* __restrict__ Mtab, int W,
+                                         const uint32_t* __restrict__ negQ, uint32_t v, int tb0,
+                                         int shift, int out_bits, uint32_t* __restrict__ out,
+                                         int N, int i) {
+    const int sw = shift >> 5, sb = shift & 31;
+    const int out_w = (out_bits + 31) >> 5;
+    const uint32_t top_mask = (out_bits & 31) ? ((1u << (out_bits & 31)) - 1u) : 0xffffffffu;
+    const int T = sw + out_w + (sb ? 1 : 0);
+    const int round_col = shift > 0 ? ((shift - 1) >> 5) : -1;
+    const uint32_t round_bit = shift > 0 ? (1u << ((shift - 1) & 31)) : 0u;
+    uint64_t carry = 0;
+    uint32_t prev = 0;
+    bool amb = false;
+    const uint32_t* y_base = ys + threadIdx.x;
+    for (int tb = tb0; tb < T; tb += kCrtCols) {
+        uint64_t acc[kCrtCols], top[kCrtCols];
+#pragma unroll
+        for (int g = 0; g < kCrtCols; ++g) {
+            uint64_t x = (uint64_t)v * negQ[tb + g] + ((tb + g) == round_col ? round_bit : 0u);
+            acc[g] = (uint32_t)x;
+            top[g] = x >> 32;
+        }
+        const uint32_t* mrow = Mtab + tb;
+        for (int j = 0; j < P4; j += 4) {
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+                const uint64_t y = y_base[(j + jj) * TB];
+                const uint4 m0 = *reinterpret_cast<const uint4*>(mrow + (size_t)(j + jj) * W);
+                const uint4 m1 = *reinterpret_cast<const uint4*>(mrow + (size_t)(j + jj) * W + 4);
+                acc[0] += y * m0.x;
+                acc[1] += y * m0.y;
+                acc[2] += y * m0.z;
+                acc[3] += y * m0.w;
+                acc[4] += y * m1.x;
+                acc[5] += y * m1.y;
+                acc[6] += y * m1.z;
+                acc[7] += y * m1.w;
+            }
+#pragma unroll
+            for (int g = 0; g < kCrtCols; ++g) {
+                top[g] += acc[g] >> 32;
+                acc[g] &= 0xffffffffull;
+            }
+        }
+#pragma unroll
+        for (int g = 0; g < kCrtCols; ++g) {
+            const int t = tb + g;
+            if (t < T) {
+                const uint64_t s = acc[g] + (carry & 0xffffffffull);
+                const uint32_t word = (uint32_t)s;
+                carry = top[g] + (s >> 32) + (carry >> 32);
+                if (t < sw) {
+                    // truncated window: ambiguous if an unseen carry of < 2^39 units of
+                    // column tb0 could still ripple into column sw
+                    if (t == tb0 + 1) amb = word >= 0xFFFFFF00u;
+                    else if (t > tb0 + 1) amb = amb && (word == 0xffffffffu);
+                } else if (sb == 0) {
+                    const int u = t - sw;
+                    out[(size_t)u * N + i] = (u == out_w - 1) ? (word & top_mask) : word;
+                } else if (t > sw) {
+                    const int u = t - sw - 1;
+                    const uint32_t o = (prev >> sb) | (word << (32 - sb));
+                    out[(size_t)u * N + i] = (u == out_w - 1) ? (o & top_mask) : o;
+                }
+                prev = word;
+            }
+        }
+    }
+    return tb0 > 0 && amb;
+}
+
 __global__ void __launch_bounds__(kCrtThreads) crt_kernel(
     const uint32_t* __restrict__ res, int P, int P4, int N, const PrimeInfo* __restrict__ pinfo,
-    const uint32_t* __restrict__ Mtab, const uint32_t* __restrict__ negQ,
+    const uint32_t* __restrict__ Mtab, int W, const uint32_t* __restrict__ negQ,
     const uint32_t* __restrict__ cinv, const uint32_t* __restrict__ cinv_sh,
-    const double* __restrict__ invp, int shift, int out_bits, OutSet outs) {
-    extern __shared__ uint32_t ys[];  // [P4][kCrtThreads]
+    const double* __restrict__ invp, int shift, int out_bits, int tb0, OutSet outs) {
+    extern __shared__ uint32_t ys[];  // [P4][TB]
     const int TB = blockDim.x;
     const int i = blockIdx.x * TB + threadIdx.x;
     const uint32_t* r = res + (size_t)blockIdx.y * P * N;
-    uint32_t* out = outs.out[blockIdx.y];
+    const int oy = blockIdx.y;
+    uint32_t* out = oy == 0 ? outs.out[0] : oy == 1 ? outs.out[1] : oy == 2 ? outs.out[2] : outs.out[3];
     double S = 0.0;
     for (int j = 0; j < P; ++j) {
         uint32_t p = pinfo[j].p;
@@ -196,50 +348,8 @@ __global__ void __launch_bounds__(kCrtThreads) crt_kernel(
     }
     for (int j = P; j < P4; ++j) ys[j * TB + threadIdx.x] = 0;
     const uint32_t v = (uint32_t)floor(S + 0.5);
-    const int sw = shift >> 5, sb = shift & 31;
-    const int out_w = (out_bits + 31) >> 5;
-    const uint32_t top_mask = (out_bits & 31) ? ((1u << (out_bits & 31)) - 1u) : 0xffffffffu;
-    const int T = sw + out_w + (sb ? 1 : 0);
-    const int round_col = shift > 0 ? ((shift - 1) >> 5) : -1;
-    const uint32_t round_bit = shift > 0 ? (1u << ((shift - 1) & 31)) : 0u;
-    uint64_t carry = 0;
-    uint32_t prev = 0;
-    for (int t = 0; t < T; ++t) {
-        uint64_t acc = (uint32_t)carry;
-        uint64_t top = carry >> 32;
-        acc += (uint64_t)v * negQ[t];
-        if (t == round_col) acc += round_bit;
-        top += acc >> 32;
-        acc = (uint32_t)acc;
-        const uint4* Mrow = reinterpret_cast<const uint4*>(Mtab + (size_t)t * P4);
-        for (int j4 = 0; j4 < P4 / 4; ++j4) {
-            uint4 m = Mrow[j4];
-            const uint32_t* y = ys + (j4 * 4) * TB + threadIdx.x;
-            acc += (uint64_t)y[0] * m.x;
-            acc += (uint64_t)y[TB] * m.y;
-            acc += (uint64_t)y[2 * TB] * m.z;
-            acc += (uint64_t)y[3 * TB] * m.w;
-            top += acc >> 32;
-            acc = (uint32_t)acc;
-        }
-        const uint32_t word = (uint32_t)acc;
-        carry = top;
-        // emit
-        if (sb == 0) {
-            if (t >= sw) {
-                int u = t - sw;
-                uint32_t o = word;
-                if (u == out_w - 1) o &= top_mask;
-                out[(size_t)u * N + i] = o;
-            }
-        } else if (t > sw) {
-            int u = t - sw - 1;
-            uint32_t o = (prev >> sb) | (word << (32 - sb));
-            if (u == out_w - 1) o &= top_mask;
-            out[(size_t)u * N + i] = o;
-        }
-        prev = word;
-    }
+    if (crt_scan(ys, TB, P4, Mtab, W, negQ, v, tb0, shift, out_bits, out, N, i))
+        crt_scan(ys, TB, P4, Mtab, W, negQ, v, 0, shift, out_bits, out, N, i);  // exact rescan
 }
 
 // ---- device scratch ------------------------------------------------------------------------
@@ -278,8 +388,19 @@ int launch_modup(hg_ctx* ctx, const OperandSet& ops, int nops, int P, uint32_t* 
     for (int k = 0; k < nops; ++k) macs += (double)words_for_bits(ops.bits[k]) * P * N;
     {
         HgTimed tm(ctx, st, HG_K_MODUP, macs);
-        modup_kernel<<<grid, threads, smem, st>>>(ops, N, ctx->log_n, ctx->d_pinfo, ctx->d_modup,
-                                                  P, out, kinv);
+        if (maxw <= 8)
+            modup_reg_kernel<8><<<grid, threads, 0, st>>>(ops, N, ctx->d_pinfo, ctx->d_modup, P, out, kinv);
+        else if (maxw <= 16)
+            modup_reg_kernel<16><<<grid, threads, 0, st>>>(ops, N, ctx->d_pinfo, ctx->d_modup, P, out, kinv);
+        else if (maxw <= 32)
+            modup_reg_kernel<32><<<grid, threads, 0, st>>>(ops, N, ctx->d_pinfo, ctx->d_modup, P, out, kinv);
+        else if (maxw <= 48)
+            modup_reg_kernel<48><<<grid, threads, 0, st>>>(ops, N, ctx->d_pinfo, ctx->d_modup, P, out, kinv);
+        else if (maxw <= 64)
+            modup_reg_kernel<64><<<grid, threads, 0, st>>>(ops, N, ctx->d_pinfo, ctx->d_modup, P, out, kinv);
+        else
+            modup_kernel<<<grid, threads, smem, st>>>(ops, N, ctx->log_n, ctx->d_pinfo, ctx->d_modup,
+                                                      P, out, kinv);
     }
     HG_LAUNCH_CHECK(ctx);
     return HG_OK;
@@ -293,15 +414,18 @@ int launch_crt(hg_ctx* ctx, const uint32_t* res, int nouts, int P, int shift, in
     int sw = shift >> 5;
     int T = sw + words_for_bits(out_bits) + ((shift & 31) ? 1 : 0);
     if (T > tab->W) return hg_fail(HG_ERANGE, "CRT window exceeds table width");
+    // columns below shift/32 only feed the carry: keep two of them (plus alignment) as a
+    // truncated fixed-point window instead of scanning all of them (exact rescan on doubt)
+    const int tb0 = sw >= 2 ? ((sw - 2) & ~(kCrtCols - 1)) : 0;
     const int N = ctx->N;
     const int threads = N < kCrtThreads ? N : kCrtThreads;
     size_t smem = (size_t)tab->P4 * threads * 4;
     dim3 grid(N / threads, nouts);
     {
-        HgTimed tm(ctx, st, HG_K_CRT, (double)nouts * N * (double)P * T);
+        HgTimed tm(ctx, st, HG_K_CRT, (double)nouts * N * (double)P * (T - tb0));
         crt_kernel<<<grid, threads, smem, st>>>(res, P, tab->P4, N, ctx->d_pinfo, tab->d_M,
-                                                tab->d_negQ, tab->d_cinv, tab->d_cinv_sh,
-                                                tab->d_invp, shift, out_bits, outs);
+                                                tab->W, tab->d_negQ, tab->d_cinv, tab->d_cinv_sh,
+                                                tab->d_invp, shift, out_bits, tb0, outs);
     }
     HG_LAUNCH_CHECK(ctx);
     return HG_OK;

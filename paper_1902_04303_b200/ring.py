@@ -49,6 +49,23 @@ def ints_to_words(coeffs, bits: int) -> np.ndarray:
     return np.ascontiguousarray(arr.T)
 
 
+def int64_to_words(vals: np.ndarray, bits: int) -> np.ndarray:
+    """Signed int64 values -> [W][N] uint32 two's complement mod 2^bits (vectorised)."""
+    vals = np.asarray(vals, dtype=np.int64)
+    w = words_for(bits)
+    out = np.empty((w, vals.shape[0]), dtype=np.uint32)
+    u = vals.view(np.uint64)
+    out[0] = (u & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+    if w > 1:
+        out[1] = (u >> np.uint64(32)).astype(np.uint32)
+    if w > 2:
+        out[2:] = np.where(vals < 0, np.uint32(0xFFFFFFFF), np.uint32(0))[None, :]
+    rem = bits & 31
+    if rem:
+        out[w - 1] &= np.uint32((1 << rem) - 1)
+    return out
+
+
 def words_to_ints(arr: np.ndarray) -> list[int]:
     """[W][N] uint32 -> list of N nonnegative Python ints."""
     arr = np.asarray(arr, dtype=np.uint32)
@@ -131,6 +148,21 @@ class RingElement:
         cb = top.bit_length() + 1  # two's complement width holding every value
         if cb < mod_bits:
             el.compact_words = upload_words(ints_to_words(signed, cb))
+            el.compact_bits = cb
+        return el
+
+    @classmethod
+    def from_int64(cls, n: int, mod_bits: int, vals: np.ndarray) -> "RingElement":
+        """Element with small signed coefficients given as an int64 array (|c| < 2^62),
+        identical to from_signed on the same values but without Python ints."""
+        vals = np.asarray(vals, dtype=np.int64)
+        if vals.shape != (n,):
+            raise ParameterError(f"expected {n} coefficients, got {vals.shape}")
+        top = int(np.max(np.abs(vals))) if n else 0
+        el = cls(n, mod_bits, words=upload_words(int64_to_words(vals, mod_bits)))
+        cb = top.bit_length() + 1
+        if cb < mod_bits:
+            el.compact_words = upload_words(int64_to_words(vals, cb))
             el.compact_bits = cb
         return el
 
