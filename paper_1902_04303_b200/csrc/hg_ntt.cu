@@ -195,8 +195,9 @@ __device__ __forceinline__ void round8_dispatch(uint32_t (&x)[8], int R, int s0,
     else round8<FWD, 1>(x, s0, pos_base, b, twp, twsp, p);
 }
 
-// smem swizzle: element i -> i + 4 * ((i >> 5) & 7) (spreads the strided round patterns)
-__device__ __forceinline__ int swz(int i) { return i + (((i >> 5) & 7) << 2); }
+// smem swizzle (a bijection on [0, 2048)): bits 2-4 ^= bits 5-7, so the stride-32 groups of
+// the b = 2 round and the stride-1 warps of the b = 5 round both hit 32 distinct banks
+__device__ __forceinline__ int swz(int i) { return i ^ (((i >> 5) & 7) << 2); }
 
 // Grid: x = chunk index, y = prime-major row (rows sharing a prime are adjacent so their
 // twiddles are re-read from L2).  Block = chunk/8 threads, 8 elements each.
