@@ -145,6 +145,7 @@ extern "C" int hg_ctx_destroy(hg_ctx* ctx) {
         cudaFree(kv.second.d_cinv);
         cudaFree(kv.second.d_cinv_sh);
         cudaFree(kv.second.d_invp);
+        cudaFree(kv.second.d_Bfrag);
     }
     delete ctx;
     return HG_OK;
@@ -340,10 +341,18 @@ int hg_get_crt(hg_ctx* ctx, int P, const CrtTable** out) {
     HG_CUDA_TRY(cudaMemcpy(t.d_cinv, cinv.data(), P * 4, cudaMemcpyHostToDevice));
     HG_CUDA_TRY(cudaMemcpy(t.d_cinv_sh, cinv_sh.data(), P * 4, cudaMemcpyHostToDevice));
     HG_CUDA_TRY(cudaMemcpy(t.d_invp, invp.data(), P * 8, cudaMemcpyHostToDevice));
+    t.P32 = (P + 31) & ~31;
+    {
+        std::vector<uint32_t> frag;
+        hg_crt_build_fragments(t, P, t.P32, frag, M);
+        HG_CUDA_TRY(cudaMalloc(&t.d_Bfrag, frag.size() * 4));
+        HG_CUDA_TRY(cudaMemcpy(t.d_Bfrag, frag.data(), frag.size() * 4, cudaMemcpyHostToDevice));
+    }
     std::lock_guard<std::mutex> lk(ctx->mu);
     auto ins = ctx->crt.emplace(P, t);
     if (!ins.second) {  // another thread won the race
         cudaFree(t.d_M); cudaFree(t.d_negQ); cudaFree(t.d_cinv); cudaFree(t.d_cinv_sh); cudaFree(t.d_invp);
+        cudaFree(t.d_Bfrag);
     }
     *out = &ins.first->second;
     return HG_OK;

@@ -44,6 +44,8 @@ struct CrtTable {
     uint32_t* d_cinv = nullptr;   // [P]: (Q/p_j)^{-1} * N^{-1} * 2^32 mod p_j
     uint32_t* d_cinv_sh = nullptr;
     double* d_invp = nullptr;     // [P]: 1/p_j
+    int P32 = 0;                  // P rounded up to 32 (mma K dimension)
+    uint2* d_Bfrag = nullptr;     // byte-split M in mma B-fragment order (hg_crt_mma.cu)
 };
 
 struct hg_ctx {
@@ -125,6 +127,10 @@ static inline int words_for_bits(int bits) { return (bits + 31) >> 5; }
 int hg_ensure_twiddles(hg_ctx* ctx, int P);
 int hg_get_crt(hg_ctx* ctx, int P, const CrtTable** out);
 int hg_primes_for_bits(const hg_ctx* ctx, double bits);   // -1 if too wide
+int hg_crt_build_fragments(const CrtTable& t, int P, int P32, std::vector<uint32_t>& out,
+                           const std::vector<uint32_t>& M);
+int hg_crt_mma_launch(hg_ctx* ctx, const CrtTable* tab, const uint32_t* res, int nouts, int P,
+                      int shift, int out_bits, int tb0, uint32_t* const* outs, cudaStream_t st);
 
 // ---- device arithmetic --------------------------------------------------------------
 // Shoup product a*w mod p for any a < 2^32, result in [0, 2p).
