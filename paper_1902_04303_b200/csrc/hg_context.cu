@@ -139,6 +139,7 @@ extern "C" int hg_ctx_destroy(hg_ctx* ctx) {
     cudaFree(ctx->d_psi_sh);
     cudaFree(ctx->d_ipsi);
     cudaFree(ctx->d_ipsi_sh);
+    cudaFree(ctx->d_modup_frag);
     for (auto& kv : ctx->crt) {
         cudaFree(kv.second.d_M);
         cudaFree(kv.second.d_negQ);

@@ -96,24 +96,38 @@ __global__ void __launch_bounds__(kWarps * 32) crt_mma_kernel(
         const int n = tid & 63, jg = tid >> 6;
         const int mt = n >> 2, nl = n & 3;
         double S = 0.0;
-        for (int j4 = jg * 4; j4 < P32; j4 += 16) {
-            uint32_t y[4];
+        // 4 quads (16 residues) per thread in flight before any of them is consumed
+        for (int jb = jg * 4; jb < P32; jb += 64) {
+            uint32_t xr[4][4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int j = j4 + u;
-                y[u] = 0;
-                if (j < P) {
-                    const uint32_t p = pinfo[j].p;
-                    const uint32_t x = r[(size_t)j * N + cb + n];
-                    y[u] = reduce_2p(mul_shoup_lazy(x, cinv[j], cinv_sh[j], p), p);
-                    S += (double)y[u] * invp[j];
+            for (int qd = 0; qd < 4; ++qd)
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int j = jb + 16 * qd + u;
+                    xr[qd][u] = j < P ? __ldcs(r + (size_t)j * N + cb + n) : 0u;
                 }
-            }
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const uint32_t w = ((y[0] >> (8 * q)) & 0xffu) | (((y[1] >> (8 * q)) & 0xffu) << 8) |
-                                   (((y[2] >> (8 * q)) & 0xffu) << 16) | (((y[3] >> (8 * q)) & 0xffu) << 24);
-                yb[((mt * 4 + q) * 4 + nl) * rs_words + (j4 >> 2)] = w;
+            for (int qd = 0; qd < 4; ++qd) {
+                const int j4 = jb + 16 * qd;
+                if (j4 >= P32) break;
+                uint32_t y[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int j = j4 + u;
+                    y[u] = 0;
+                    if (j < P) {
+                        const uint32_t p = pinfo[j].p;
+                        y[u] = reduce_2p(mul_shoup_lazy(xr[qd][u], cinv[j], cinv_sh[j], p), p);
+                        S += (double)y[u] * invp[j];
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint32_t w = __byte_perm(__byte_perm(y[0] >> (8 * q), y[1] >> (8 * q), 0x0040),
+                                                   __byte_perm(y[2] >> (8 * q), y[3] >> (8 * q), 0x0040),
+                                                   0x5410);
+                    yb[((mt * 4 + q) * 4 + nl) * rs_words + (j4 >> 2)] = w;
+                }
             }
         }
         ssm[jg * kCoefs + n] = S;
@@ -184,19 +198,34 @@ __global__ void __launch_bounds__(kWarps * 32) crt_mma_kernel(
                 wpart[(cw * kColBlock + ti) * 4 + s0] = val;
             }
         __syncwarp();
+        // parallel combine: lane -> (coefficient lane/4, columns 2(lane%4), +1); each column
+        // value becomes (lo32, hi) with value = hi * 2^32 + lo32 (hi < 2^43)
+        {
+            const int cw = lane >> 2;
+            const uint32_t cv = vsm[warp * 8 + cw];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int ti = (lane & 3) * 2 + h;
+                const int t = tb + ti;
+                uint64_t* pp = wpart + (size_t)(cw * kColBlock + ti) * 4;
+                const uint64_t x0 = pp[0] + (pp[1] << 8);   // < 2^57
+                const uint64_t x1 = pp[2] + (pp[3] << 8);   // weight 2^16
+                const uint64_t extra = (uint64_t)cv * negQ[t] + (t == round_col ? round_bit : 0u);
+                const uint64_t lo = (x0 & 0xffffffffull) + ((x1 & 0xffffull) << 16) + (extra & 0xffffffffull);
+                pp[0] = lo & 0xffffffffull;
+                pp[1] = (lo >> 32) + (x0 >> 32) + (x1 >> 16) + (extra >> 32);
+            }
+        }
+        __syncwarp();
         if (lane < 8) {
             const uint64_t* pp = wpart + (size_t)lane * kColBlock * 4;
 #pragma unroll 1
             for (int ti = 0; ti < kColBlock; ++ti) {
                 const int t = tb + ti;
                 if (t >= T) break;
-                const uint64_t x0 = pp[ti * 4 + 0] + (pp[ti * 4 + 1] << 8);   // < 2^57
-                const uint64_t x1 = pp[ti * 4 + 2] + (pp[ti * 4 + 3] << 8);   // weight 2^16
-                const uint64_t extra = (uint64_t)my_v * negQ[t] + (t == round_col ? round_bit : 0u);
-                const uint64_t lo = (x0 & 0xffffffffull) + ((x1 & 0xffffull) << 16) +
-                                    (carry & 0xffffffffull) + (extra & 0xffffffffull);
+                const uint64_t lo = pp[ti * 4] + (carry & 0xffffffffull);
                 const uint32_t word = (uint32_t)lo;
-                carry = (lo >> 32) + (x0 >> 32) + (x1 >> 16) + (carry >> 32) + (extra >> 32);
+                carry = pp[ti * 4 + 1] + (lo >> 32) + (carry >> 32);
                 if (t < sw) {
                     if (t == tb0 + 1) amb = word >= 0xFFFFFF00u;
                     else if (t > tb0 + 1) amb = amb && (word == 0xffffffffu);

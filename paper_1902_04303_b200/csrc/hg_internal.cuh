@@ -11,6 +11,8 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <algorithm>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <string>
@@ -63,6 +65,8 @@ struct hg_ctx {
     uint32_t* d_ipsi = nullptr;
     uint32_t* d_ipsi_sh = nullptr;
     int tw_ready = 0;
+    uint32_t* d_modup_frag = nullptr;   // ModUp-on-tensor-cores B fragments (hg_modup_mma.cu)
+    int modup_frag_ks = 0;
     std::map<int, CrtTable> crt;
     std::mutex mu;
     std::atomic<long long> launches{0};
@@ -131,6 +135,9 @@ int hg_crt_build_fragments(const CrtTable& t, int P, int P32, std::vector<uint32
                            const std::vector<uint32_t>& M);
 int hg_crt_mma_launch(hg_ctx* ctx, const CrtTable* tab, const uint32_t* res, int nouts, int P,
                       int shift, int out_bits, int tb0, uint32_t* const* outs, cudaStream_t st);
+int hg_modup_mma_launch(hg_ctx* ctx, const uint32_t* const* words, const int* bits,
+                        const int* is_signed, int nops, int P, uint32_t* out, int64_t kinv,
+                        cudaStream_t st);
 
 // ---- device arithmetic --------------------------------------------------------------
 // Shoup product a*w mod p for any a < 2^32, result in [0, 2p).
