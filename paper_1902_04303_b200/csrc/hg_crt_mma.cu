@@ -84,6 +84,7 @@ __global__ void __launch_bounds__(kWarps * 32) crt_mma_kernel(
     uint64_t* part = reinterpret_cast<uint64_t*>(smem + (size_t)kCoefs * 4 * rs_bytes);  // [8][8][8][4]
     uint32_t* vsm = reinterpret_cast<uint32_t*>(part + kWarps * 8 * kColBlock * 4);
     double* ssm = reinterpret_cast<double*>(vsm + kCoefs);  // [4][64]
+    uint2* bsm = reinterpret_cast<uint2*>(ssm + 4 * kCoefs);  // B fragments of one column block
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int cb = blockIdx.x * kCoefs;
@@ -164,7 +165,14 @@ __global__ void __launch_bounds__(kWarps * 32) crt_mma_kernel(
             for (int i = 0; i < 4; ++i)
 #pragma unroll
                 for (int e = 0; e < 4; ++e) acc[m][i][e] = 0;
-        const uint2* bt = Bfrag + (size_t)(tb >> 1) * nks * 32 + lane;
+        // stage this column block's B fragments (4 n-tiles x nks x 32 lanes) in shared memory
+        __syncthreads();
+        {
+            const uint2* src = Bfrag + (size_t)(tb >> 1) * nks * 32;
+            for (int e = tid; e < 4 * nks * 32; e += kWarps * 32) bsm[e] = __ldg(src + e);
+        }
+        __syncthreads();
+        const uint2* bt = bsm + lane;
         for (int ks = 0; ks < nks; ++ks) {
             uint32_t a[2][4];
 #pragma unroll
@@ -179,7 +187,7 @@ __global__ void __launch_bounds__(kWarps * 32) crt_mma_kernel(
             }
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                const uint2 b = __ldg(bt + ((size_t)i * nks + ks) * 32);
+                const uint2 b = bt[(i * nks + ks) * 32];
                 mma_u8(acc[0][i], a[0], b);
                 mma_u8(acc[1][i], a[1], b);
             }
@@ -284,7 +292,7 @@ int hg_crt_mma_launch(hg_ctx* ctx, const CrtTable* tab, const uint32_t* res, int
     int rs_words = P32 / 4;
     rs_words += (4 - rs_words) & 31;
     const size_t smem = (size_t)kCoefs * 4 * rs_words * 4 + (size_t)kWarps * 8 * kColBlock * 4 * 8 +
-                        kCoefs * 4 + 4 * kCoefs * 8;
+                        kCoefs * 4 + 4 * kCoefs * 8 + (size_t)4 * (P32 / 32) * 32 * 8;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(crt_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);

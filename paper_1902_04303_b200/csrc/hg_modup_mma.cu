@@ -90,17 +90,31 @@ __global__ void __launch_bounds__(kWarps * 32) modup_mma_kernel(
 
     uint32_t* outp = out + (size_t)op * P * N;
     const int ntiles = (P + 1) >> 1;
+    // B fragments of n-tile nt+1 are loaded while n-tile nt is multiplied (register double
+    // buffer): the L2 latency of the constant table hides behind the mma and the epilogue
+    uint2 bnext[KS];
+    {
+        const uint2* bp = Bm + lane;
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) bnext[ks] = __ldg(bp + ks * 32);
+    }
     for (int nt = 0; nt < ntiles; ++nt) {
+        uint2 bcur[KS];
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) bcur[ks] = bnext[ks];
+        if (nt + 1 < ntiles) {
+            const uint2* bp = Bm + (size_t)(nt + 1) * ks_stride * 32 + lane;
+#pragma unroll
+            for (int ks = 0; ks < KS; ++ks) bnext[ks] = __ldg(bp + ks * 32);
+        }
         int acc[kMt][4];
 #pragma unroll
         for (int m = 0; m < kMt; ++m) acc[m][0] = acc[m][1] = acc[m][2] = acc[m][3] = 0;
-        const uint2* bp = Bm + (size_t)nt * ks_stride * 32 + lane;
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
-            if (8 * ks >= W) break;
-            const uint2 b = __ldg(bp + ks * 32);
 #pragma unroll
-            for (int m = 0; m < kMt; ++m) mma_u8(acc[m], a[m][ks][0], a[m][ks][1], a[m][ks][2], a[m][ks][3], b);
+            for (int m = 0; m < kMt; ++m)
+                mma_u8(acc[m], a[m][ks][0], a[m][ks][1], a[m][ks][2], a[m][ks][3], bcur[ks]);
         }
         // lane: prime j = 2nt + (lane&3)/2, bytes r0 = 2(lane&1), +1; rows n, n+8
         const int j = 2 * nt + ((lane & 3) >> 1);
@@ -195,14 +209,23 @@ int hg_modup_mma_launch(hg_ctx* ctx, const uint32_t* const* words, const int* bi
     dim3 grid(ctx->N / kCoefs, nops);
     const uint2* Bm = reinterpret_cast<const uint2*>(ctx->d_modup_frag);
     const int kss = ctx->modup_frag_ks;
-    if (maxw <= 16)
-        modup_mma_kernel<2><<<grid, kWarps * 32, 0, st>>>(o, ctx->N, ctx->d_pinfo, ctx->d_modup, Bm, kss, P, out, kinv);
-    else if (maxw <= 32)
-        modup_mma_kernel<4><<<grid, kWarps * 32, 0, st>>>(o, ctx->N, ctx->d_pinfo, ctx->d_modup, Bm, kss, P, out, kinv);
-    else if (maxw <= 48)
-        modup_mma_kernel<6><<<grid, kWarps * 32, 0, st>>>(o, ctx->N, ctx->d_pinfo, ctx->d_modup, Bm, kss, P, out, kinv);
-    else
-        modup_mma_kernel<8><<<grid, kWarps * 32, 0, st>>>(o, ctx->N, ctx->d_pinfo, ctx->d_modup, Bm, kss, P, out, kinv);
+#define HG_MODUP_CASE(K)                                                                     \
+    case K:                                                                                  \
+        modup_mma_kernel<K><<<grid, kWarps * 32, 0, st>>>(o, ctx->N, ctx->d_pinfo, ctx->d_modup, \
+                                                          Bm, kss, P, out, kinv);            \
+        break;
+    switch ((maxw + 7) / 8) {  // exact k-step count: no padded mma, no early-exit branches
+        HG_MODUP_CASE(1)
+        HG_MODUP_CASE(2)
+        HG_MODUP_CASE(3)
+        HG_MODUP_CASE(4)
+        HG_MODUP_CASE(5)
+        HG_MODUP_CASE(6)
+        HG_MODUP_CASE(7)
+        HG_MODUP_CASE(8)
+        default: return 0;
+    }
+#undef HG_MODUP_CASE
     ctx->launches.fetch_add(1, std::memory_order_relaxed);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return -hg_fail(HG_ECUDA, std::string("modup_mma launch: ") + cudaGetErrorString(e));
