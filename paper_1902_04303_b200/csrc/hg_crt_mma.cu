@@ -226,14 +226,23 @@ __global__ void __launch_bounds__(kWarps * 32) crt_mma_kernel(
         }
         __syncwarp();
         if (lane < 8) {
-            const uint64_t* pp = wpart + (size_t)lane * kColBlock * 4;
-#pragma unroll 1
+            const ulonglong2* pp = reinterpret_cast<const ulonglong2*>(wpart + (size_t)lane * kColBlock * 4);
+            ulonglong2 cv[kColBlock];
+#pragma unroll
+            for (int ti = 0; ti < kColBlock; ++ti) cv[ti] = pp[2 * ti];   // all loads first
+            uint32_t words[kColBlock];
+#pragma unroll
+            for (int ti = 0; ti < kColBlock; ++ti) {   // the serial part: 3 adds per column
+                const uint64_t lo = cv[ti].x + (carry & 0xffffffffull);
+                words[ti] = (uint32_t)lo;
+                carry = cv[ti].y + (lo >> 32) + (carry >> 32);
+            }
+            // columns past T carried garbage into `carry`; it is never used after the last block
+#pragma unroll
             for (int ti = 0; ti < kColBlock; ++ti) {
                 const int t = tb + ti;
                 if (t >= T) break;
-                const uint64_t lo = pp[ti * 4] + (carry & 0xffffffffull);
-                const uint32_t word = (uint32_t)lo;
-                carry = pp[ti * 4 + 1] + (lo >> 32) + (carry >> 32);
+                const uint32_t word = words[ti];
                 if (t < sw) {
                     if (t == tb0 + 1) amb = word >= 0xFFFFFF00u;
                     else if (t > tb0 + 1) amb = amb && (word == 0xffffffffu);

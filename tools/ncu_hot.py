@@ -28,3 +28,22 @@ def main(path, top=40):
 
 if __name__ == "__main__":
     main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 40)
+
+
+def opcode_mix(path):
+    lines = open(path).read().splitlines()
+    start = next(i for i, l in enumerate(lines) if l.startswith('"Address"'))
+    rows = [r for r in csv.DictReader(io.StringIO("\n".join(lines[start:]))) if r["Address"] != "Address"]
+    mix = Counter()
+    samp = Counter()
+    for r in rows:
+        op = r["Source"].strip()
+        if op.startswith("@"):
+            op = op.split(None, 1)[1] if " " in op else op
+        op = op.split()[0] if op else "?"
+        mix[op] += int(r["Instructions Executed"] or 0)
+        samp[op] += int(r["Warp Stall Sampling (All Samples)"] or 0)
+    tot = sum(mix.values())
+    print("warp-instructions executed", tot)
+    for op, v in mix.most_common(25):
+        print(f"  {op:24s} {v:12d} {100 * v / tot:5.1f}%  samples {samp[op]}")
