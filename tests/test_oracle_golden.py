@@ -121,3 +121,17 @@ def test_oracle_decrypt_unit(golden):
     s_l = R.reduce_to(s, lv)
     m = R.add(c0, R.mul(c1, s_l, lv, n), lv)
     assert m == g.ints("decrypt_eng_mult")[0]
+
+
+def test_replay_oracle_matches_reference_encrypted_run(golden):
+    """The float64 replay of the approximate circuit (oracle/replay.py) agrees with the
+    reference's decrypted encrypted-GWAS statistics (~1e-8)."""
+    import numpy as np
+
+    from oracle.replay import replay_gwas
+
+    g = golden("gwas_toy")
+    rep = replay_gwas(g.arr("X"), g.arr("y"), g.arr("S"))
+    num, den = g.arr("num"), g.arr("den")
+    assert np.max(np.abs(rep["numerator"] - num)) < 1e-6
+    assert np.max(np.abs(rep["denominator"] - den)) < 1e-6
