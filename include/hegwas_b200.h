@@ -118,6 +118,17 @@ int hg_keyswitch(hg_ctx* ctx, const hg_key* key, const uint32_t* x, int64_t auto
 int hg_ct_mult(hg_ctx* ctx, const hg_key* evk, const uint32_t* a0, const uint32_t* a1,
                const uint32_t* b0, const uint32_t* b1, int level, int rescale_bits,
                uint32_t* out0, uint32_t* out1, void* stream);
+/* Resident left operand for repeated products (the 245 duplicated projector columns of the
+ * per-batch loop, gwas.py:310/325): forward-NTT residues of (c0, c1) at `level`, kept in HBM. */
+typedef struct hg_ctprep hg_ctprep;
+int hg_ct_prepare(hg_ctx* ctx, const uint32_t* c0, const uint32_t* c1, int level, void* stream,
+                  hg_ctprep** out);
+int hg_ctprep_destroy(hg_ctprep* prep);
+size_t hg_ctprep_device_bytes(const hg_ctprep* prep);
+/* hg_ct_mult with the left operand prepared (same output, bit for bit). */
+int hg_ct_mult_prepared(hg_ctx* ctx, const hg_key* evk, const hg_ctprep* a, const uint32_t* b0,
+                        const uint32_t* b1, int level, int rescale_bits, uint32_t* out0,
+                        uint32_t* out1, void* stream);
 /* _apply_automorphism (ckks.py:247-253): out = (phi_k(c0) + e0, e1), (e0, e1) =
  * keyswitch(phi_k(c1)).  Used by rotate (ckks.py:256-273) and conjugate (:276-279). */
 int hg_ct_automorph(hg_ctx* ctx, const hg_key* key, const uint32_t* c0, const uint32_t* c1,

@@ -62,6 +62,10 @@ SIGNATURES = {
     "hg_keyswitch": (_i, [_vp, _vp, _vp, _i64, _vp, _vp, _vp]),
     "hg_ct_mult": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _vp, _vp, _vp]),
     "hg_ct_automorph": (_i, [_vp, _vp, _vp, _vp, _i, _i64, _vp, _vp, _vp]),
+    "hg_ct_prepare": (_i, [_vp, _vp, _vp, _i, _vp, ctypes.POINTER(_vp)]),
+    "hg_ctprep_destroy": (_i, [_vp]),
+    "hg_ctprep_device_bytes": (ctypes.c_size_t, [_vp]),
+    "hg_ct_mult_prepared": (_i, [_vp, _vp, _vp, _vp, _vp, _i, _i, _vp, _vp, _vp]),
     "hg_ntt_forward": (_i, [_vp, _vp, _i, _i, _vp]),
     "hg_ntt_inverse": (_i, [_vp, _vp, _i, _i, _vp]),
     "hg_bench_modmul": (_i, [_vp, _i, _vp, ctypes.POINTER(ctypes.c_double), _vp]),

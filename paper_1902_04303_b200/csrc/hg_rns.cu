@@ -444,6 +444,36 @@ int launch_crt(hg_ctx* ctx, const uint32_t* res, int nouts, int P, int shift, in
 
 dim3 pw_grid(int N, int rows) { return dim3((N + 255) / 256 < 64 ? (N + 255) / 256 : 64, rows); }
 
+// Tensor with a resident (prepared) left operand: A0, A1 = NTT residues [P][N] in [0, 4p);
+// buf = [B0 | B1 | (D2)] each [P][N] -> [D0 | D1 | D2].
+__global__ void pw_tensor_prep_kernel(const uint32_t* __restrict__ A0, const uint32_t* __restrict__ A1,
+                                      uint32_t* __restrict__ buf, int P, int N,
+                                      const PrimeInfo* __restrict__ pinfo) {
+    const int j = blockIdx.y;
+    const PrimeInfo pi = pinfo[j];
+    const size_t stride = (size_t)P * N;
+    const size_t off = (size_t)j * N;
+    const uint32_t p2 = pi.p << 1;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+        const size_t o = off + i;
+        uint32_t a0 = A0[o], a1 = A1[o], b0 = buf[o], b1 = buf[o + stride];
+        a0 = a0 >= p2 ? a0 - p2 : a0;
+        a1 = a1 >= p2 ? a1 - p2 : a1;
+        b0 = b0 >= p2 ? b0 - p2 : b0;
+        b1 = b1 >= p2 ? b1 - p2 : b1;
+        uint32_t d0 = mont_mul(a0, b0, pi.p, pi.pinv_neg);
+        uint32_t d1 = mont_mul(a0, b1, pi.p, pi.pinv_neg) + mont_mul(a1, b0, pi.p, pi.pinv_neg);
+        uint32_t d2 = mont_mul(a1, b1, pi.p, pi.pinv_neg);
+        d0 = d0 >= pi.p ? d0 - pi.p : d0;
+        d1 = d1 >= p2 ? d1 - p2 : d1;
+        d1 = d1 >= pi.p ? d1 - pi.p : d1;
+        d2 = d2 >= pi.p ? d2 - pi.p : d2;
+        buf[o] = d0;
+        buf[o + stride] = d1;
+        buf[o + 2 * stride] = d2;
+    }
+}
+
 int magnitude_bits(const hg_operand& o) { return o.signed_rep ? o.bits - 1 : o.bits; }
 
 int primes_for_product(hg_ctx* ctx, double mag_bits, int window_bits) {
@@ -606,6 +636,24 @@ extern "C" int hg_keyswitch(hg_ctx* ctx, const hg_key* key, const uint32_t* x,
 }
 
 // ---- fused scheme ops ------------------------------------------------------------------------------
+// relinearise d2 with evk, add to (d0, d1), rescale (or not) into (out0, out1)
+static int ct_mult_finish(hg_ctx* ctx, const hg_key* evk, uint32_t* d0, uint32_t* d1,
+                          uint32_t* d2, uint32_t* e0, uint32_t* e1, int level, int rescale_bits,
+                          uint32_t* out0, uint32_t* out1, cudaStream_t st) {
+    int rc = hg_keyswitch(ctx, evk, d2, 1, e0, e1, st);
+    if (rc) return rc;
+    if (rescale_bits == 0) {
+        rc = hg_ew_add(ctx, out0, d0, e0, level, false, st);
+        if (!rc) rc = hg_ew_add(ctx, out1, d1, e1, level, false, st);
+        return rc;
+    }
+    rc = hg_ew_add(ctx, d0, d0, e0, level, false, st);
+    if (!rc) rc = hg_ew_add(ctx, d1, d1, e1, level, false, st);
+    if (!rc) rc = hg_ew_divide_round(ctx, out0, level - rescale_bits, d0, level, rescale_bits, st);
+    if (!rc) rc = hg_ew_divide_round(ctx, out1, level - rescale_bits, d1, level, rescale_bits, st);
+    return rc;
+}
+
 extern "C" int hg_ct_mult(hg_ctx* ctx, const hg_key* evk, const uint32_t* a0, const uint32_t* a1,
                           const uint32_t* b0, const uint32_t* b1, int level, int rescale_bits,
                           uint32_t* out0, uint32_t* out1, void* stream) {
@@ -624,18 +672,97 @@ extern "C" int hg_ct_mult(hg_ctx* ctx, const hg_key* evk, const uint32_t* a0, co
     hg_operand o[4] = {{a0, level, 1}, {a1, level, 1}, {b0, level, 1}, {b1, level, 1}};
     int rc = hg_poly_tensor(ctx, d0, d1, d2, level, o[0], o[1], o[2], o[3], stream);
     if (rc) return rc;
-    rc = hg_keyswitch(ctx, evk, d2, 1, e0, e1, stream);
-    if (rc) return rc;
-    if (rescale_bits == 0) {
-        rc = hg_ew_add(ctx, out0, d0, e0, level, false, st);
-        if (!rc) rc = hg_ew_add(ctx, out1, d1, e1, level, false, st);
+    return ct_mult_finish(ctx, evk, d0, d1, d2, e0, e1, level, rescale_bits, out0, out1, st);
+}
+
+// ---- resident (prepared) left operands ----------------------------------------------------------
+struct hg_ctprep {
+    hg_ctx* ctx = nullptr;
+    int level = 0;
+    int P = 0;
+    uint32_t* d_res = nullptr;   // [2][P][N] forward-NTT residues of c0, c1 (centered reps)
+    size_t bytes = 0;
+};
+
+static int tensor_primes(hg_ctx* ctx, int level) {
+    // both operands centered at `level` bits, d1 is a sum of two products
+    return primes_for_product(ctx, 2.0 * (level - 1) + 1, level);
+}
+
+extern "C" int hg_ct_prepare(hg_ctx* ctx, const uint32_t* c0, const uint32_t* c1, int level,
+                             void* stream, hg_ctprep** out) {
+    if (!ctx || !c0 || !c1 || !out || level < 2) return hg_fail(HG_EINVAL, "hg_ct_prepare: bad arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int N = ctx->N;
+    const int P = tensor_primes(ctx, level);
+    if (P < 0) return hg_fail(HG_ERANGE, "tensor product exceeds the NTT prime basis");
+    hg_ctprep* pr = new hg_ctprep();
+    pr->ctx = ctx;
+    pr->level = level;
+    pr->P = P;
+    pr->bytes = (size_t)2 * P * N * 4;
+    if (cudaMalloc(&pr->d_res, pr->bytes) != cudaSuccess) {
+        delete pr;
+        return hg_fail(HG_ENOMEM, "prepared operand allocation failed");
+    }
+    OperandSet ops{};
+    ops.words[0] = c0; ops.bits[0] = level; ops.is_signed[0] = 1;
+    ops.words[1] = c1; ops.bits[1] = level; ops.is_signed[1] = 1;
+    int rc = launch_modup(ctx, ops, 2, P, pr->d_res, 0, st);
+    if (!rc) rc = hg_ntt_launch(ctx, pr->d_res, 2 * P, P, 0, true, st);
+    if (rc) {
+        cudaFree(pr->d_res);
+        delete pr;
         return rc;
     }
-    rc = hg_ew_add(ctx, d0, d0, e0, level, false, st);
-    if (!rc) rc = hg_ew_add(ctx, d1, d1, e1, level, false, st);
-    if (!rc) rc = hg_ew_divide_round(ctx, out0, level - rescale_bits, d0, level, rescale_bits, st);
-    if (!rc) rc = hg_ew_divide_round(ctx, out1, level - rescale_bits, d1, level, rescale_bits, st);
-    return rc;
+    *out = pr;
+    return HG_OK;
+}
+
+extern "C" int hg_ctprep_destroy(hg_ctprep* pr) {
+    if (!pr) return HG_OK;
+    cudaFree(pr->d_res);
+    delete pr;
+    return HG_OK;
+}
+
+extern "C" size_t hg_ctprep_device_bytes(const hg_ctprep* pr) { return pr ? pr->bytes : 0; }
+
+extern "C" int hg_ct_mult_prepared(hg_ctx* ctx, const hg_key* evk, const hg_ctprep* a,
+                                   const uint32_t* b0, const uint32_t* b1, int level,
+                                   int rescale_bits, uint32_t* out0, uint32_t* out1, void* stream) {
+    if (!ctx || !evk || !a || a->ctx != ctx || a->level != level || evk->level != level ||
+        rescale_bits < 0 || rescale_bits >= level)
+        return hg_fail(HG_EINVAL, "hg_ct_mult_prepared: operand/key level mismatch");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int N = ctx->N;
+    const int W = words_for_bits(level);
+    const int P = a->P;
+    Scratch res(st), buf(st);
+    HG_CUDA_TRY(res.alloc((size_t)3 * P * N * 4));
+    HG_CUDA_TRY(buf.alloc((size_t)5 * W * N * 4));
+    OperandSet ops{};
+    ops.words[0] = b0; ops.bits[0] = level; ops.is_signed[0] = 1;
+    ops.words[1] = b1; ops.bits[1] = level; ops.is_signed[1] = 1;
+    int rc = launch_modup(ctx, ops, 2, P, res.u32(), 0, st);
+    if (rc) return rc;
+    rc = hg_ntt_launch(ctx, res.u32(), 2 * P, P, 0, true, st);
+    if (rc) return rc;
+    pw_tensor_prep_kernel<<<pw_grid(N, P), 256, 0, st>>>(a->d_res, a->d_res + (size_t)P * N,
+                                                         res.u32(), P, N, ctx->d_pinfo);
+    HG_LAUNCH_CHECK(ctx);
+    rc = hg_ntt_launch(ctx, res.u32(), 3 * P, P, 0, false, st);
+    if (rc) return rc;
+    uint32_t* d0 = buf.u32();
+    uint32_t* d1 = d0 + (size_t)W * N;
+    uint32_t* d2 = d1 + (size_t)W * N;
+    uint32_t* e0 = d2 + (size_t)W * N;
+    uint32_t* e1 = e0 + (size_t)W * N;
+    OutSet outs{};
+    outs.out[0] = d0; outs.out[1] = d1; outs.out[2] = d2;
+    rc = launch_crt(ctx, res.u32(), 3, P, 0, level, outs, st);
+    if (rc) return rc;
+    return ct_mult_finish(ctx, evk, d0, d1, d2, e0, e1, level, rescale_bits, out0, out1, st);
 }
 
 extern "C" int hg_ct_automorph(hg_ctx* ctx, const hg_key* key, const uint32_t* c0,
