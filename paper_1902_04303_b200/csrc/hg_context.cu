@@ -103,13 +103,11 @@ extern "C" int hg_ctx_create(int log_n, int device, hg_ctx** out) {
             v = mulmod64(v, pi.c32, p);
         }
     }
-    size_t tw_bytes = (size_t)ctx->nprimes * ctx->N * sizeof(uint32_t);
+    size_t tw_bytes = (size_t)ctx->nprimes * ctx->N * sizeof(uint2);
     if (cudaMalloc(&ctx->d_pinfo, sizeof(PrimeInfo) * ctx->nprimes) != cudaSuccess ||
         cudaMalloc(&ctx->d_modup, modup.size() * sizeof(uint32_t)) != cudaSuccess ||
-        cudaMalloc(&ctx->d_psi, tw_bytes) != cudaSuccess ||
-        cudaMalloc(&ctx->d_psi_sh, tw_bytes) != cudaSuccess ||
-        cudaMalloc(&ctx->d_ipsi, tw_bytes) != cudaSuccess ||
-        cudaMalloc(&ctx->d_ipsi_sh, tw_bytes) != cudaSuccess) {
+        cudaMalloc(&ctx->d_tw_fwd, tw_bytes) != cudaSuccess ||
+        cudaMalloc(&ctx->d_tw_inv, tw_bytes) != cudaSuccess) {
         hg_ctx_destroy(ctx);
         return hg_fail(HG_ENOMEM, "context allocation failed");
     }
@@ -135,10 +133,8 @@ extern "C" int hg_ctx_destroy(hg_ctx* ctx) {
     if (!ctx) return HG_OK;
     cudaFree(ctx->d_pinfo);
     cudaFree(ctx->d_modup);
-    cudaFree(ctx->d_psi);
-    cudaFree(ctx->d_psi_sh);
-    cudaFree(ctx->d_ipsi);
-    cudaFree(ctx->d_ipsi_sh);
+    cudaFree(ctx->d_tw_fwd);
+    cudaFree(ctx->d_tw_inv);
     cudaFree(ctx->d_modup_frag);
     for (auto& kv : ctx->crt) {
         cudaFree(kv.second.d_M);
@@ -242,7 +238,8 @@ int hg_ensure_twiddles(hg_ctx* ctx, int P) {
     const int N = ctx->N, logn = ctx->log_n;
     int j0 = ctx->tw_ready;
     size_t cnt = (size_t)(P - j0) * N;
-    std::vector<uint32_t> psi(cnt), psi_sh(cnt), ipsi(cnt), ipsi_sh(cnt), pw(N);
+    std::vector<uint2> psi(cnt), ipsi(cnt);
+    std::vector<uint32_t> pw(N);
     for (int j = j0; j < P; ++j) {
         uint32_t p = ctx->primes[j];
         uint64_t root = 0;
@@ -258,17 +255,13 @@ int hg_ensure_twiddles(hg_ctx* ctx, int P) {
             uint32_t e = bitrev((uint32_t)k, logn);
             uint32_t w = pw[e];
             uint32_t iw = e == 0 ? 1u : (uint32_t)(p - pw[N - e]);  // psi^-e = -psi^(N-e)
-            psi[base + k] = w;
-            psi_sh[base + k] = shoup_of(w, p);
-            ipsi[base + k] = iw;
-            ipsi_sh[base + k] = shoup_of(iw, p);
+            psi[base + k] = make_uint2(w, shoup_of(w, p));
+            ipsi[base + k] = make_uint2(iw, shoup_of(iw, p));
         }
     }
     size_t off = (size_t)j0 * N;
-    HG_CUDA_TRY(cudaMemcpy(ctx->d_psi + off, psi.data(), cnt * 4, cudaMemcpyHostToDevice));
-    HG_CUDA_TRY(cudaMemcpy(ctx->d_psi_sh + off, psi_sh.data(), cnt * 4, cudaMemcpyHostToDevice));
-    HG_CUDA_TRY(cudaMemcpy(ctx->d_ipsi + off, ipsi.data(), cnt * 4, cudaMemcpyHostToDevice));
-    HG_CUDA_TRY(cudaMemcpy(ctx->d_ipsi_sh + off, ipsi_sh.data(), cnt * 4, cudaMemcpyHostToDevice));
+    HG_CUDA_TRY(cudaMemcpy(ctx->d_tw_fwd + off, psi.data(), cnt * 8, cudaMemcpyHostToDevice));
+    HG_CUDA_TRY(cudaMemcpy(ctx->d_tw_inv + off, ipsi.data(), cnt * 8, cudaMemcpyHostToDevice));
     ctx->tw_ready = P;
     return HG_OK;
 }

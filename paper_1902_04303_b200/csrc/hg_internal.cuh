@@ -59,11 +59,10 @@ struct hg_ctx {
     std::vector<double> prefix_bits;    // prefix_bits[P] = sum_{j<P} log2 p_j
     PrimeInfo* d_pinfo = nullptr;       // [nprimes]
     uint32_t* d_modup = nullptr;        // [nprimes][HG_MODUP_WMAX] : 2^(32w) mod p_j
-    // twiddles, lazily materialised for the first `tw_ready` primes: [nprimes][N]
-    uint32_t* d_psi = nullptr;
-    uint32_t* d_psi_sh = nullptr;
-    uint32_t* d_ipsi = nullptr;
-    uint32_t* d_ipsi_sh = nullptr;
+    // twiddles (w, floor(w 2^32/p)) interleaved, lazily materialised for the first
+    // `tw_ready` primes: [nprimes][N] uint2, forward psi^bitrev and inverse psi^-bitrev
+    uint2* d_tw_fwd = nullptr;
+    uint2* d_tw_inv = nullptr;
     int tw_ready = 0;
     uint32_t* d_modup_frag = nullptr;   // ModUp-on-tensor-cores B fragments (hg_modup_mma.cu)
     int modup_frag_ks = 0;
