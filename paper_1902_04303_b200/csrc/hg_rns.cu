@@ -560,7 +560,7 @@ extern "C" int hg_key_prepare(hg_ctx* ctx, const uint32_t* kb, const uint32_t* k
     key->big_l = big_l;
     key->P = P;
     key->bytes = (size_t)2 * P * N * 4;
-    if (cudaMalloc(&key->d_kb, key->bytes) != cudaSuccess) {
+    if (cudaMallocAsync(&key->d_kb, key->bytes, st) != cudaSuccess) {  // pool: no device sync
         delete key;
         return hg_fail(HG_ENOMEM, "key allocation failed");
     }
@@ -577,7 +577,7 @@ extern "C" int hg_key_prepare(hg_ctx* ctx, const uint32_t* kb, const uint32_t* k
         HG_LAUNCH_CHECK(ctx);
     }
     if (rc) {
-        cudaFree(key->d_kb);
+        cudaFreeAsync(key->d_kb, 0);
         delete key;
         return rc;
     }
@@ -587,7 +587,7 @@ extern "C" int hg_key_prepare(hg_ctx* ctx, const uint32_t* kb, const uint32_t* k
 
 extern "C" int hg_key_destroy(hg_key* key) {
     if (!key) return HG_OK;
-    cudaFree(key->d_kb);
+    cudaFreeAsync(key->d_kb, 0);
     delete key;
     return HG_OK;
 }
@@ -701,7 +701,7 @@ extern "C" int hg_ct_prepare(hg_ctx* ctx, const uint32_t* c0, const uint32_t* c1
     pr->level = level;
     pr->P = P;
     pr->bytes = (size_t)2 * P * N * 4;
-    if (cudaMalloc(&pr->d_res, pr->bytes) != cudaSuccess) {
+    if (cudaMallocAsync(&pr->d_res, pr->bytes, st) != cudaSuccess) {  // pool: no device sync
         delete pr;
         return hg_fail(HG_ENOMEM, "prepared operand allocation failed");
     }
@@ -711,7 +711,7 @@ extern "C" int hg_ct_prepare(hg_ctx* ctx, const uint32_t* c0, const uint32_t* c1
     int rc = launch_modup(ctx, ops, 2, P, pr->d_res, 0, st);
     if (!rc) rc = hg_ntt_launch(ctx, pr->d_res, 2 * P, P, 0, true, st);
     if (rc) {
-        cudaFree(pr->d_res);
+        cudaFreeAsync(pr->d_res, 0);
         delete pr;
         return rc;
     }
@@ -721,7 +721,7 @@ extern "C" int hg_ct_prepare(hg_ctx* ctx, const uint32_t* c0, const uint32_t* c1
 
 extern "C" int hg_ctprep_destroy(hg_ctprep* pr) {
     if (!pr) return HG_OK;
-    cudaFree(pr->d_res);
+    cudaFreeAsync(pr->d_res, 0);
     delete pr;
     return HG_OK;
 }

@@ -28,7 +28,9 @@ def _run(n, k, log_n, seed=0):
     gen.manual_seed(seed + 5)
     config = GwasConfig(n=n, d=4, k=k).resolve(params)
     enc = encrypt_gwas_inputs(ds, config, params, pk, gen)
-    out = compute_gwas_encrypted(hg.HeEngine(params, evk, rot), enc)
+    with hg.track_ops() as ops:
+        out = compute_gwas_encrypted(hg.HeEngine(params, evk, rot), enc)
+    _run.last_ops = ops.snapshot()
     num, den = decrypt_statistics(out.batch_outputs, config, params, sk)
     res = assemble_result(num, den)
     rep = replay_gwas(ds.X, ds.y, ds.S)
@@ -50,6 +52,10 @@ def test_replay_agreement_n64_k256():
 def test_replay_agreement_config0_p17():
     """Config 0 at the parity preset P17: n=245, d=4, 256 SNPs, N=2^17, log_l=1700."""
     num, den, res, rep, eff, se, pv = _run(245, 256, 17)
+    # exact op-count contract of the reference at config-0 shape (SURVEY F10, dry run)
+    assert _run.last_ops == {"ct_mults": 596, "pt_mults": 577, "rotations": 8191,
+                             "conjugations": 1, "keyswitches": 8788, "rescales_ct": 596,
+                             "rescales_pt": 577}
     assert np.max(np.abs(num - rep["numerator"])) < 1e-3
     assert np.max(np.abs(den - rep["denominator"])) < 1e-3
     ok = np.isfinite(eff)

@@ -214,7 +214,7 @@ def make_gwas(n=8, d=4, k=16, log_n=7, seed=0, key_seed=5, fname="gwas_toy.npz")
     st.save(fname)
 
 
-if __name__ == "__main__":
+def main():
     which = sys.argv[1] if len(sys.argv) > 1 else "all"
     os.makedirs(OUT, exist_ok=True)
     if which in ("unit", "all"):
@@ -223,3 +223,34 @@ if __name__ == "__main__":
         make_deep()
     if which in ("gwas", "all"):
         make_gwas()
+    if which in ("hegw", "all"):
+        make_hegw()
+
+
+def make_hegw():
+    """HEGW v1 bytes written by the reference's own serialize module (UNIT params)."""
+    from hegwas import serialize as S
+
+    st = Store()
+    params = hegwas.CkksParams(log_n=8, log_l=350, log_p=45, log_p_small=30, h=16)
+    sk, pk, evk, rot = hegwas.keygen(params, 7)
+    eng = hegwas.HeEngine(params, evk, rot)
+    a = hegwas.encrypt_values(rand_vec(1, params.slot_count), params.log_p, pk, params, random.Random(11))
+    m = eng.mult(a, a)
+    blobs = {
+        "ct_a": S.ciphertext_to_bytes(a),
+        "ct_mult": S.ciphertext_to_bytes(m),
+        "pt_mask": S.plaintext_to_bytes(eng.mask(("slot", 3)), params.log_n),
+        "sk": S.secret_key_to_bytes(sk, params.log_n),
+        "pk": S.public_key_to_bytes(pk, params.log_n),
+        "evk": S.evaluation_key_to_bytes(evk, params.log_n),
+        "rot": S.rotation_keys_to_bytes(rot, params.log_n),
+    }
+    for k, v in blobs.items():
+        st.arr("hegw." + k, np.frombuffer(v, dtype=np.uint8))
+    st.arr("params", params_arr(params))
+    st.save("hegw_unit.npz")
+
+
+if __name__ == "__main__":
+    main()
