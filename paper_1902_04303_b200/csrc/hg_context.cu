@@ -143,6 +143,7 @@ extern "C" int hg_ctx_destroy(hg_ctx* ctx) {
         cudaFree(kv.second.d_cinv_sh);
         cudaFree(kv.second.d_invp);
         cudaFree(kv.second.d_Bfrag);
+        cudaFree(kv.second.d_Bconv);
     }
     delete ctx;
     return HG_OK;
@@ -341,12 +342,17 @@ int hg_get_crt(hg_ctx* ctx, int P, const CrtTable** out) {
         hg_crt_build_fragments(t, P, t.P32, frag, M);
         HG_CUDA_TRY(cudaMalloc(&t.d_Bfrag, frag.size() * 4));
         HG_CUDA_TRY(cudaMemcpy(t.d_Bfrag, frag.data(), frag.size() * 4, cudaMemcpyHostToDevice));
+        std::vector<uint8_t> conv;
+        hg_crt_build_conv(t, P, t.P32, conv, M);
+        HG_CUDA_TRY(cudaMalloc(&t.d_Bconv, conv.size()));
+        HG_CUDA_TRY(cudaMemcpy(t.d_Bconv, conv.data(), conv.size(), cudaMemcpyHostToDevice));
     }
     std::lock_guard<std::mutex> lk(ctx->mu);
     auto ins = ctx->crt.emplace(P, t);
     if (!ins.second) {  // another thread won the race
         cudaFree(t.d_M); cudaFree(t.d_negQ); cudaFree(t.d_cinv); cudaFree(t.d_cinv_sh); cudaFree(t.d_invp);
         cudaFree(t.d_Bfrag);
+        cudaFree(t.d_Bconv);
     }
     *out = &ins.first->second;
     return HG_OK;

@@ -1,0 +1,313 @@
+// hg_crt_umma.cu -- CRT reconstruction on the 5th-gen tensor cores (tcgen05.mma kind::i8,
+// SASS UTCIMMA), accumulators in TMEM.
+//
+// "Digit" layout: with y_j = sum_q yb_{j,q} 2^(8q) and the 32-bit words of Q/p_j split into
+// bytes, column t of the exact product is
+//     col_t = sum_{s=0..6} E_s(t) 2^(8s),   E_s(t) = sum_j sum_q yb_{j,q} * byte_{s-q}(M[j][t]),
+// i.e. one u8 x u8 -> s32 GEMM with rows = coefficients (M = 128 per CTA), K = (prime, byte of y)
+// and columns = (output word t, digit s) -- 8 TMEM columns per output word (s = 7 is zero).
+// Every TMEM lane (= thread) therefore holds all digits of its own coefficient: the epilogue is
+// a per-thread radix-2^8 -> radix-2^32 fold plus the exact carry chain, with no shuffles.
+// A (the y bytes) is computed from the residues straight into shared memory in the UMMA
+// K-major core-matrix layout; B (constant per prime basis) is streamed in 32-prime K chunks.
+#include "hg_internal.cuh"
+
+namespace {
+
+constexpr int kRows = 128;      // coefficients per CTA = UMMA M
+constexpr int kColChunk = 32;   // output words per accumulation pass (N = 256)
+constexpr int kKChunk = 128;    // bytes of K per pipeline stage (32 primes, 4 UMMA k-steps)
+constexpr int kBStage = kColChunk * 8 * kKChunk;   // 32 KB
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46);  // SWIZZLE_NONE, v1
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(bar), "r"(parity));
+    }
+}
+
+struct UOuts {
+    uint32_t* out[4];
+};
+
+// exact column scan for one coefficient (rare fallback when the truncated carry window is
+// ambiguous); y_j read back from the A tile (row n, byte 4j)
+__device__ void umma_rescan_exact(const uint8_t* sa, int kc16, int n, int P, int W,
+                                  const uint32_t* __restrict__ Mtab,
+                                  const uint32_t* __restrict__ negQ, uint32_t v, int shift,
+                                  int out_bits, uint32_t* __restrict__ out, int N, int i) {
+    const int sw = shift >> 5, sb = shift & 31;
+    const int out_w = (out_bits + 31) >> 5;
+    const uint32_t top_mask = (out_bits & 31) ? ((1u << (out_bits & 31)) - 1u) : 0xffffffffu;
+    const int T = sw + out_w + (sb ? 1 : 0);
+    const int round_col = shift > 0 ? ((shift - 1) >> 5) : -1;
+    const uint32_t round_bit = shift > 0 ? (1u << ((shift - 1) & 31)) : 0u;
+    const int g = n >> 3, rr = n & 7;
+    uint64_t carry = 0;
+    uint32_t prev = 0;
+    for (int t = 0; t < T; ++t) {
+        uint64_t x = (uint64_t)v * negQ[t] + (t == round_col ? round_bit : 0u) + (uint32_t)carry;
+        uint64_t top = (carry >> 32) + (x >> 32);
+        uint64_t acc = (uint32_t)x;
+        for (int j = 0; j < P; ++j) {
+            const int c = j >> 2;
+            const uint32_t y = *reinterpret_cast<const uint32_t*>(sa + ((size_t)(g * kc16 + c) * 8 + rr) * 16 + (j & 3) * 4);
+            acc += (uint64_t)y * Mtab[(size_t)j * W + t];
+            top += acc >> 32;
+            acc &= 0xffffffffull;
+        }
+        const uint32_t word = (uint32_t)acc;
+        carry = top;
+        if (t >= sw) {
+            if (sb == 0) {
+                const int u = t - sw;
+                out[(size_t)u * N + i] = (u == out_w - 1) ? (word & top_mask) : word;
+            } else if (t > sw) {
+                const int u = t - sw - 1;
+                const uint32_t o = (prev >> sb) | (word << (32 - sb));
+                out[(size_t)u * N + i] = (u == out_w - 1) ? (o & top_mask) : o;
+            }
+        }
+        prev = word;
+    }
+}
+
+__global__ void __launch_bounds__(kRows) crt_umma_kernel(
+    const uint32_t* __restrict__ res, int P, int P32, int N, const PrimeInfo* __restrict__ pinfo,
+    const uint8_t* __restrict__ Bconv, const uint32_t* __restrict__ Mtab, int W,
+    const uint32_t* __restrict__ negQ, const uint32_t* __restrict__ cinv,
+    const uint32_t* __restrict__ cinv_sh, const double* __restrict__ invp, int shift,
+    int out_bits, int tb0, UOuts outs) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint32_t tmem_base;
+    __shared__ __align__(8) uint64_t mbar[2];
+    const int K = 4 * P32;                 // bytes of K
+    const int kc16 = K / 16;               // 16-byte K chunks per row
+    uint8_t* sa = smem;                    // A: 128 rows x K bytes (core-matrix layout)
+    uint8_t* sb = smem + (size_t)kRows * K;  // B: 2 stages x 32 KB
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int cb = blockIdx.x * kRows;
+    const int oy = blockIdx.y;
+    const uint32_t* r = res + (size_t)oy * P * N;
+    uint32_t* out = oy == 0 ? outs.out[0] : oy == 1 ? outs.out[1] : oy == 2 ? outs.out[2] : outs.out[3];
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base)), "n"(256));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&mbar[0])));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&mbar[1])));
+    }
+
+    // ---- phase 1: thread = coefficient; y_j -> A (K-major core layout), S -> v ----------------
+    double S = 0.0;
+    {
+        const int n = tid, g = n >> 3, rr = n & 7;
+        for (int j0 = 0; j0 < P32; j0 += 16) {
+            uint32_t x[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                const int j = j0 + u;
+                x[u] = j < P ? __ldcs(r + (size_t)j * N + cb + n) : 0u;
+            }
+#pragma unroll
+            for (int c4 = 0; c4 < 4; ++c4) {
+                uint32_t y[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int j = j0 + 4 * c4 + u;
+                    y[u] = 0;
+                    if (j < P) {
+                        const uint32_t p = pinfo[j].p;
+                        y[u] = reduce_2p(mul_shoup_lazy(x[4 * c4 + u], cinv[j], cinv_sh[j], p), p);
+                        S += (double)y[u] * invp[j];
+                    }
+                }
+                const int c = (j0 >> 2) + c4;
+                *reinterpret_cast<uint4*>(sa + ((size_t)(g * kc16 + c) * 8 + rr) * 16) =
+                    make_uint4(y[0], y[1], y[2], y[3]);
+            }
+        }
+    }
+    const uint32_t v = (uint32_t)floor(S + 0.5);
+    asm volatile("fence.proxy.async.shared::cta;\n");
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    const uint32_t tmem = tmem_base;
+
+    // ---- phase 2/3: column chunks: K-pipelined UMMA into TMEM, then the per-thread chain ------
+    const int sw = shift >> 5, sbit = shift & 31;
+    const int out_w = (out_bits + 31) >> 5;
+    const uint32_t top_mask = (out_bits & 31) ? ((1u << (out_bits & 31)) - 1u) : 0xffffffffu;
+    const int T = sw + out_w + (sbit ? 1 : 0);
+    const int round_col = shift > 0 ? ((shift - 1) >> 5) : -1;
+    const uint32_t round_bit = shift > 0 ? (1u << ((shift - 1) & 31)) : 0u;
+    const int nkc = P32 / 32;
+    const uint32_t a_base = smem_u32(sa);
+    const uint32_t b_base = smem_u32(sb);
+    const int i = cb + tid;
+    uint64_t carry = 0;
+    uint32_t prev = 0;
+    bool amb = false;
+    uint32_t phase[2] = {0u, 0u};
+    bool used[2] = {false, false};
+    int stage_ctr = 0;
+    for (int t0 = tb0; t0 < T; t0 += kColChunk) {
+        int ncols = T - t0;
+        if (ncols > kColChunk) ncols = kColChunk;
+        ncols = (ncols + 1) & ~1;                      // N = 8 * ncols, a multiple of 16
+        const uint32_t Nn = 8u * ncols;
+        const uint32_t idesc = (2u << 4) | ((Nn >> 3) << 17) | ((uint32_t)(kRows >> 4) << 24);
+        const int tg0 = t0 >> 3;                       // first 8-column group in the B table
+        for (int kc = 0; kc < nkc; ++kc, ++stage_ctr) {
+            const int s = stage_ctr & 1;
+            if (used[s]) {                             // the MMAs that read this stage are done
+                mbar_wait(smem_u32(&mbar[s]), phase[s]);
+                phase[s] ^= 1u;
+            }
+            // B chunk (kc, column groups tg0 .. tg0 + ncols/8): contiguous 8 KB per group
+            {
+                const int ngroups = (ncols + 7) >> 3;
+                const uint4* src = reinterpret_cast<const uint4*>(Bconv + ((size_t)kc * (W >> 3) + tg0) * 8192);
+                uint4* dst = reinterpret_cast<uint4*>(sb + (size_t)s * kBStage);
+                for (int e = tid; e < ngroups * 512; e += kRows) dst[e] = __ldg(src + e);
+            }
+            asm volatile("fence.proxy.async.shared::cta;\n");
+            __syncthreads();
+            if (tid == 0) {
+                asm volatile("tcgen05.fence::after_thread_sync;\n");
+#pragma unroll
+                for (int k = 0; k < kKChunk / 32; ++k) {
+                    const uint64_t da = umma_desc(a_base + (uint32_t)((kc * (kKChunk / 16) + 2 * k) * 128), 128, kc16 * 128);
+                    const uint64_t db = umma_desc(b_base + (uint32_t)(s * kBStage + 2 * k * 128), 128, 8 * 128);
+                    const uint32_t acc = (kc > 0 || k > 0) ? 1u : 0u;
+                    asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                                 "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n"
+                                 ::"r"(tmem), "l"(da), "l"(db), "r"(idesc), "r"(acc));
+                }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+                             ::"r"(smem_u32(&mbar[s])));
+            }
+            used[s] = true;
+        }
+        // wait for the last stage's commit (covers all earlier MMAs of this chunk)
+        {
+            const int s = (stage_ctr - 1) & 1;
+            mbar_wait(smem_u32(&mbar[s]), phase[s]);
+            phase[s] ^= 1u;
+            used[s] = false;
+            if (used[s ^ 1]) {   // the other stage's commit also completed (issued earlier)
+                mbar_wait(smem_u32(&mbar[s ^ 1]), phase[s ^ 1]);
+                phase[s ^ 1] ^= 1u;
+                used[s ^ 1] = false;
+            }
+        }
+        asm volatile("tcgen05.fence::after_thread_sync;\n");
+        // epilogue: this thread's TMEM lane = its coefficient
+        const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
+        for (int tl = 0; tl < ncols; tl += 2) {
+            uint32_t e[16];
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+                         : "=r"(e[0]), "=r"(e[1]), "=r"(e[2]), "=r"(e[3]), "=r"(e[4]), "=r"(e[5]),
+                           "=r"(e[6]), "=r"(e[7]), "=r"(e[8]), "=r"(e[9]), "=r"(e[10]), "=r"(e[11]),
+                           "=r"(e[12]), "=r"(e[13]), "=r"(e[14]), "=r"(e[15])
+                         : "r"(lane_addr + (uint32_t)(tl * 8)));
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n");
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int t = t0 + tl + h;
+                if (t >= T) break;
+                const uint32_t* E = e + 8 * h;
+                const uint64_t lo = (uint64_t)E[0] + ((uint64_t)E[1] << 8) + ((uint64_t)E[2] << 16) + ((uint64_t)E[3] << 24);
+                const uint64_t hi = (uint64_t)E[4] + ((uint64_t)E[5] << 8) + ((uint64_t)E[6] << 16) + ((uint64_t)E[7] << 24);
+                const uint64_t extra = (uint64_t)v * negQ[t] + (t == round_col ? round_bit : 0u);
+                const uint64_t sum = (lo & 0xffffffffull) + (carry & 0xffffffffull) + (extra & 0xffffffffull);
+                const uint32_t word = (uint32_t)sum;
+                carry = (sum >> 32) + (lo >> 32) + hi + (carry >> 32) + (extra >> 32);
+                if (t < sw) {
+                    if (t == tb0 + 1) amb = word >= 0xFFFFFF00u;
+                    else if (t > tb0 + 1) amb = amb && (word == 0xffffffffu);
+                } else if (sbit == 0) {
+                    const int u = t - sw;
+                    out[(size_t)u * N + i] = (u == out_w - 1) ? (word & top_mask) : word;
+                } else if (t > sw) {
+                    const int u = t - sw - 1;
+                    const uint32_t o = (prev >> sbit) | (word << (32 - sbit));
+                    out[(size_t)u * N + i] = (u == out_w - 1) ? (o & top_mask) : o;
+                }
+                prev = word;
+            }
+        }
+        // all lanes must finish reading TMEM before the next chunk's MMAs overwrite it
+        asm volatile("tcgen05.fence::before_thread_sync;\n");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;\n");
+    }
+    if (tb0 > 0 && amb)
+        umma_rescan_exact(sa, kc16, tid, P, W, Mtab, negQ, v, shift, out_bits, out, N, i);
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(256));
+}
+
+}  // namespace
+
+// B in the digit layout, pre-arranged as the exact shared-memory image the kernel copies:
+// [K chunk kc (32 primes)][8-column group tg][row group t (8 rows: digits s)][16-byte K chunk c]
+// [row s][16 bytes]; byte 4jj+q of row (t,s) = byte (s-q) of M[32kc+4c+jj][t] (0 if out of 0..3).
+int hg_crt_build_conv(const CrtTable& t, int P, int P32, std::vector<uint8_t>& out,
+                      const std::vector<uint32_t>& M) {
+    const int W = t.W, nkc = P32 / 32, ntg = W / 8;
+    out.assign((size_t)nkc * ntg * 8192, 0);
+    for (int kc = 0; kc < nkc; ++kc)
+        for (int tg = 0; tg < ntg; ++tg)
+            for (int tl = 0; tl < 8; ++tl) {
+                const int col = tg * 8 + tl;
+                for (int c = 0; c < 8; ++c)
+                    for (int s = 0; s < 8; ++s)
+                        for (int jj = 0; jj < 4; ++jj)
+                            for (int q = 0; q < 4; ++q) {
+                                const int j = kc * 32 + c * 4 + jj;
+                                const int rbyte = s - q;
+                                uint8_t val = 0;
+                                if (j < P && rbyte >= 0 && rbyte < 4)
+                                    val = (uint8_t)(M[(size_t)j * W + col] >> (8 * rbyte));
+                                const size_t off = ((size_t)kc * ntg + tg) * 8192 +
+                                                   ((size_t)(tl * 8 + c) * 8 + s) * 16 + jj * 4 + q;
+                                out[off] = val;
+                            }
+            }
+    return HG_OK;
+}
+
+size_t hg_crt_umma_smem(int P32) { return (size_t)kRows * 4 * P32 + 2 * (size_t)kBStage; }
+
+int hg_crt_umma_launch(hg_ctx* ctx, const CrtTable* tab, const uint32_t* res, int nouts, int P,
+                       int shift, int out_bits, int tb0, uint32_t* const* outs_in, cudaStream_t st) {
+    const size_t smem = hg_crt_umma_smem(tab->P32);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(crt_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        attr = true;
+    }
+    UOuts o{};
+    for (int k = 0; k < nouts; ++k) o.out[k] = outs_in[k];
+    dim3 grid(ctx->N / kRows, nouts);
+    crt_umma_kernel<<<grid, kRows, smem, st>>>(res, P, tab->P32, ctx->N, ctx->d_pinfo, tab->d_Bconv,
+                                               tab->d_M, tab->W, tab->d_negQ, tab->d_cinv,
+                                               tab->d_cinv_sh, tab->d_invp, shift, out_bits, tb0, o);
+    HG_LAUNCH_CHECK(ctx);
+    return HG_OK;
+}

@@ -48,6 +48,7 @@ struct CrtTable {
     double* d_invp = nullptr;     // [P]: 1/p_j
     int P32 = 0;                  // P rounded up to 32 (mma K dimension)
     uint2* d_Bfrag = nullptr;     // byte-split M in mma B-fragment order (hg_crt_mma.cu)
+    uint8_t* d_Bconv = nullptr;   // digit-layout B as a UMMA smem image (hg_crt_umma.cu)
 };
 
 struct hg_ctx {
@@ -134,6 +135,11 @@ int hg_crt_build_fragments(const CrtTable& t, int P, int P32, std::vector<uint32
                            const std::vector<uint32_t>& M);
 int hg_crt_mma_launch(hg_ctx* ctx, const CrtTable* tab, const uint32_t* res, int nouts, int P,
                       int shift, int out_bits, int tb0, uint32_t* const* outs, cudaStream_t st);
+int hg_crt_build_conv(const CrtTable& t, int P, int P32, std::vector<uint8_t>& out,
+                      const std::vector<uint32_t>& M);
+int hg_crt_umma_launch(hg_ctx* ctx, const CrtTable* tab, const uint32_t* res, int nouts, int P,
+                       int shift, int out_bits, int tb0, uint32_t* const* outs, cudaStream_t st);
+size_t hg_crt_umma_smem(int P32);
 int hg_modup_mma_launch(hg_ctx* ctx, const uint32_t* const* words, const int* bits,
                         const int* is_signed, int nops, int P, uint32_t* out, int64_t kinv,
                         cudaStream_t st);

@@ -427,6 +427,12 @@ int launch_crt(hg_ctx* ctx, const uint32_t* res, int nouts, int P, int shift, in
     const int threads = N < kCrtThreads ? N : kCrtThreads;
     size_t smem = (size_t)tab->P4 * threads * 4;
     dim3 grid(N / threads, nouts);
+    if (N >= 128 && !getenv("HG_NO_UMMA") && !getenv("HG_NO_MMA") &&
+        hg_crt_umma_smem(tab->P32) <= 220 * 1024) {
+        // tcgen05 path (UTCIMMA, accumulators in TMEM)
+        HgTimed tm(ctx, st, HG_K_CRT, (double)nouts * N * (double)P * (T - tb0));
+        return hg_crt_umma_launch(ctx, tab, res, nouts, P, shift, out_bits, tb0, outs.out, st);
+    }
     if (N >= 64 && !getenv("HG_NO_MMA")) {
         // tensor-core path: work counted as 32x32-bit MACs, like the integer-pipe kernel
         HgTimed tm(ctx, st, HG_K_CRT, (double)nouts * N * (double)P * (T - tb0));
