@@ -83,7 +83,7 @@ __device__ void umma_rescan_exact(const uint8_t* sa, int kc16, int n, int P, int
     }
 }
 
-__global__ void __launch_bounds__(kRows) crt_umma_kernel(
+__global__ void __launch_bounds__(2 * kRows) crt_umma_kernel(
     const uint32_t* __restrict__ res, int P, int P32, int N, const PrimeInfo* __restrict__ pinfo,
     const uint8_t* __restrict__ Bconv, const uint32_t* __restrict__ Mtab, int W,
     const uint32_t* __restrict__ negQ, const uint32_t* __restrict__ cinv,
@@ -106,21 +106,52 @@ __global__ void __launch_bounds__(kRows) crt_umma_kernel(
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base)), "n"(256));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
     }
+    __shared__ __align__(8) uint64_t mbar_b[2];   // B stage landed (bulk copy tx count)
+    __shared__ __align__(8) uint64_t mbar_ld;     // residue chunk landed
+    __shared__ __align__(8) uint64_t mbar_done;   // all MMAs of a column chunk retired
     if (tid == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&mbar[0])));
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&mbar[1])));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&mbar_b[0])));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&mbar_b[1])));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&mbar_ld)));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&mbar_done)));
+        asm volatile("fence.mbarrier_init.release.cluster;\n");
     }
+    __syncthreads();
 
-    // ---- phase 1: thread = coefficient; y_j -> A (K-major core layout), S -> v ----------------
-    double S = 0.0;
+    // ---- phase 1: residues of 128 primes at a time land in the (still idle) B stages through
+    // bulk copies (one 512-byte row per prime); two threads per coefficient (alternating
+    // 16-prime groups) turn them into y_j -> A (K-major core layout) and S = sum y_j / p_j -> v --
+    __shared__ double ssum[2 * kRows];
     {
-        const int n = tid, g = n >> 3, rr = n & 7;
-        for (int j0 = 0; j0 < P32; j0 += 16) {
+        double S = 0.0;
+        const int n = tid & (kRows - 1), half = tid >> 7, g = n >> 3, rr = n & 7;
+        const uint32_t* stage = reinterpret_cast<const uint32_t*>(sb);
+        uint32_t ld_phase = 0;
+        for (int jc = 0; jc < P32; jc += 128) {
+            const int cnt = P - jc < 128 ? P - jc : 128;
+            if (cnt > 0) {
+                if (tid == 0) {
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n"
+                                 ::"r"(smem_u32(&mbar_ld)), "r"(cnt * kRows * 4));
+                    for (int jj = 0; jj < cnt; ++jj)
+                        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                                     ::"r"(smem_u32(sb) + jj * kRows * 4),
+                                     "l"(r + (size_t)(jc + jj) * N + cb), "n"(kRows * 4),
+                                     "r"(smem_u32(&mbar_ld))
+                                     : "memory");
+                }
+                mbar_wait(smem_u32(&mbar_ld), ld_phase);
+                ld_phase ^= 1u;
+            }
+            const int jend = jc + 128 < P32 ? jc + 128 : P32;
+        for (int j0 = jc + 16 * half; j0 < jend; j0 += 32) {
             uint32_t x[16];
 #pragma unroll
             for (int u = 0; u < 16; ++u) {
                 const int j = j0 + u;
-                x[u] = j < P ? __ldcs(r + (size_t)j * N + cb + n) : 0u;
+                x[u] = j < P ? stage[(j - jc) * kRows + n] : 0u;
             }
 #pragma unroll
             for (int c4 = 0; c4 < 4; ++c4) {
@@ -140,12 +171,19 @@ __global__ void __launch_bounds__(kRows) crt_umma_kernel(
                     make_uint4(y[0], y[1], y[2], y[3]);
             }
         }
+            // the staging rows are rewritten by the async proxy next: order our reads first
+            asm volatile("fence.proxy.async.shared::cta;\n");
+            __syncthreads();
+        }
+        ssum[tid] = S;
     }
-    const uint32_t v = (uint32_t)floor(S + 0.5);
     asm volatile("fence.proxy.async.shared::cta;\n");
     asm volatile("tcgen05.fence::before_thread_sync;\n");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n");
+    const int nn = tid & (kRows - 1);
+    const uint32_t v = (uint32_t)floor(ssum[nn] + ssum[kRows + nn] + 0.5);
+    const bool epi = tid < kRows;   // warps 0-3 own TMEM lanes 0-127
     const uint32_t tmem = tmem_base;
 
     // ---- phase 2/3: column chunks: K-pipelined UMMA into TMEM, then the per-thread chain ------
@@ -158,11 +196,13 @@ __global__ void __launch_bounds__(kRows) crt_umma_kernel(
     const int nkc = P32 / 32;
     const uint32_t a_base = smem_u32(sa);
     const uint32_t b_base = smem_u32(sb);
-    const int i = cb + tid;
+    const int i = cb + nn;
     uint64_t carry = 0;
     uint32_t prev = 0;
     bool amb = false;
-    uint32_t phase[2] = {0u, 0u};
+    uint32_t phase[2] = {0u, 0u};     // MMA-commit barriers (tid 0's bookkeeping)
+    uint32_t bphase[2] = {0u, 0u};    // B-landed barriers (tid 0)
+    uint32_t done_phase = 0u;         // chunk-done barrier (everyone)
     bool used[2] = {false, false};
     int stage_ctr = 0;
     for (int t0 = tb0; t0 < T; t0 += kColChunk) {
@@ -172,22 +212,30 @@ __global__ void __launch_bounds__(kRows) crt_umma_kernel(
         const uint32_t Nn = 8u * ncols;
         const uint32_t idesc = (2u << 4) | ((Nn >> 3) << 17) | ((uint32_t)(kRows >> 4) << 24);
         const int tg0 = t0 >> 3;                       // first 8-column group in the B table
-        for (int kc = 0; kc < nkc; ++kc, ++stage_ctr) {
-            const int s = stage_ctr & 1;
-            if (used[s]) {                             // the MMAs that read this stage are done
-                mbar_wait(smem_u32(&mbar[s]), phase[s]);
-                phase[s] ^= 1u;
-            }
-            // B chunk (kc, column groups tg0 .. tg0 + ncols/8): contiguous 8 KB per group
-            {
-                const int ngroups = (ncols + 7) >> 3;
-                const uint4* src = reinterpret_cast<const uint4*>(Bconv + ((size_t)kc * (W >> 3) + tg0) * 8192);
-                uint4* dst = reinterpret_cast<uint4*>(sb + (size_t)s * kBStage);
-                for (int e = tid; e < ngroups * 512; e += kRows) dst[e] = __ldg(src + e);
-            }
-            asm volatile("fence.proxy.async.shared::cta;\n");
-            __syncthreads();
-            if (tid == 0) {
+        // one thread drives the pipeline: bulk-copy B stage kc+1 while the MMAs of stage kc run
+        if (tid == 0) {
+            const int ngroups = (ncols + 7) >> 3;
+            auto issue_b = [&](int kc) {
+                const int s = (stage_ctr + kc) & 1;
+                if (used[s]) {                         // the MMAs that read this stage retired
+                    mbar_wait(smem_u32(&mbar[s]), phase[s]);
+                    phase[s] ^= 1u;
+                    used[s] = false;
+                }
+                const uint32_t bytes = (uint32_t)ngroups * 8192u;
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n"
+                             ::"r"(smem_u32(&mbar_b[s])), "r"(bytes));
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                             ::"r"(b_base + (uint32_t)(s * kBStage)),
+                             "l"(Bconv + ((size_t)kc * (W >> 3) + tg0) * 8192), "r"(bytes),
+                             "r"(smem_u32(&mbar_b[s]))
+                             : "memory");
+            };
+            issue_b(0);
+            for (int kc = 0; kc < nkc; ++kc) {
+                const int s = (stage_ctr + kc) & 1;
+                mbar_wait(smem_u32(&mbar_b[s]), bphase[s]);
+                bphase[s] ^= 1u;
                 asm volatile("tcgen05.fence::after_thread_sync;\n");
 #pragma unroll
                 for (int k = 0; k < kKChunk / 32; ++k) {
@@ -200,25 +248,20 @@ __global__ void __launch_bounds__(kRows) crt_umma_kernel(
                 }
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
                              ::"r"(smem_u32(&mbar[s])));
+                used[s] = true;
+                if (kc + 1 < nkc) issue_b(kc + 1);
             }
-            used[s] = true;
+            // one more commit tracking every MMA issued so far: the chunk is complete when it fires
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+                         ::"r"(smem_u32(&mbar_done)));
         }
-        // wait for the last stage's commit (covers all earlier MMAs of this chunk)
-        {
-            const int s = (stage_ctr - 1) & 1;
-            mbar_wait(smem_u32(&mbar[s]), phase[s]);
-            phase[s] ^= 1u;
-            used[s] = false;
-            if (used[s ^ 1]) {   // the other stage's commit also completed (issued earlier)
-                mbar_wait(smem_u32(&mbar[s ^ 1]), phase[s ^ 1]);
-                phase[s ^ 1] ^= 1u;
-                used[s ^ 1] = false;
-            }
-        }
+        stage_ctr += nkc;
+        mbar_wait(smem_u32(&mbar_done), done_phase);
+        done_phase ^= 1u;
         asm volatile("tcgen05.fence::after_thread_sync;\n");
         // epilogue: this thread's TMEM lane = its coefficient
-        const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
-        for (int tl = 0; tl < ncols; tl += 2) {
+        const uint32_t lane_addr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+        for (int tl = 0; epi && tl < ncols; tl += 2) {   // warp-uniform: warps 4-7 skip
             uint32_t e[16];
             asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
                          : "=r"(e[0]), "=r"(e[1]), "=r"(e[2]), "=r"(e[3]), "=r"(e[4]), "=r"(e[5]),
@@ -256,8 +299,8 @@ __global__ void __launch_bounds__(kRows) crt_umma_kernel(
         __syncthreads();
         asm volatile("tcgen05.fence::after_thread_sync;\n");
     }
-    if (tb0 > 0 && amb)
-        umma_rescan_exact(sa, kc16, tid, P, W, Mtab, negQ, v, shift, out_bits, out, N, i);
+    if (epi && tb0 > 0 && amb)
+        umma_rescan_exact(sa, kc16, nn, P, W, Mtab, negQ, v, shift, out_bits, out, N, i);
     __syncthreads();
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(256));
 }
@@ -299,13 +342,15 @@ int hg_crt_umma_launch(hg_ctx* ctx, const CrtTable* tab, const uint32_t* res, in
     const size_t smem = hg_crt_umma_smem(tab->P32);
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(crt_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        // 227 KB per block includes the kernel's static shared variables
+        HG_CUDA_TRY(cudaFuncSetAttribute(crt_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         220 * 1024));
         attr = true;
     }
     UOuts o{};
     for (int k = 0; k < nouts; ++k) o.out[k] = outs_in[k];
     dim3 grid(ctx->N / kRows, nouts);
-    crt_umma_kernel<<<grid, kRows, smem, st>>>(res, P, tab->P32, ctx->N, ctx->d_pinfo, tab->d_Bconv,
+    crt_umma_kernel<<<grid, 2 * kRows, smem, st>>>(res, P, tab->P32, ctx->N, ctx->d_pinfo, tab->d_Bconv,
                                                tab->d_M, tab->W, tab->d_negQ, tab->d_cinv,
                                                tab->d_cinv_sh, tab->d_invp, shift, out_bits, tb0, o);
     HG_LAUNCH_CHECK(ctx);
