@@ -136,6 +136,7 @@ extern "C" int hg_ctx_destroy(hg_ctx* ctx) {
     cudaFree(ctx->d_tw_fwd);
     cudaFree(ctx->d_tw_inv);
     cudaFree(ctx->d_modup_frag);
+    cudaFree(ctx->d_modup_umma);
     for (auto& kv : ctx->crt) {
         cudaFree(kv.second.d_M);
         cudaFree(kv.second.d_negQ);

@@ -66,6 +66,7 @@ struct hg_ctx {
     uint2* d_tw_inv = nullptr;
     int tw_ready = 0;
     uint32_t* d_modup_frag = nullptr;   // ModUp-on-tensor-cores B fragments (hg_modup_mma.cu)
+    uint8_t* d_modup_umma = nullptr;    // ModUp tcgen05 B smem images (hg_modup_umma.cu)
     int modup_frag_ks = 0;
     std::map<int, CrtTable> crt;
     std::mutex mu;
@@ -140,6 +141,9 @@ int hg_crt_build_conv(const CrtTable& t, int P, int P32, std::vector<uint8_t>& o
 int hg_crt_umma_launch(hg_ctx* ctx, const CrtTable* tab, const uint32_t* res, int nouts, int P,
                        int shift, int out_bits, int tb0, uint32_t* const* outs, cudaStream_t st);
 size_t hg_crt_umma_smem(int P32);
+int hg_modup_umma_launch(hg_ctx* ctx, const uint32_t* const* words, const int* bits,
+                         const int* is_signed, int nops, int P, uint32_t* out, int64_t kinv,
+                         cudaStream_t st);
 int hg_modup_mma_launch(hg_ctx* ctx, const uint32_t* const* words, const int* bits,
                         const int* is_signed, int nops, int P, uint32_t* out, int64_t kinv,
                         cudaStream_t st);

@@ -386,6 +386,12 @@ int launch_modup(hg_ctx* ctx, const OperandSet& ops, int nops, int P, uint32_t* 
     dim3 grid(N / threads, nops);
     double macs = 0.0;
     for (int k = 0; k < nops; ++k) macs += (double)words_for_bits(ops.bits[k]) * P * N;
+    if (!getenv("HG_NO_UMMA") && !getenv("HG_NO_MMA")) {
+        HgTimed tm(ctx, st, HG_K_MODUP, macs);
+        int h = hg_modup_umma_launch(ctx, ops.words, ops.bits, ops.is_signed, nops, P, out, kinv, st);
+        if (h < 0) return -h;
+        if (h == 1) return HG_OK;
+    }
     if (!getenv("HG_NO_MMA")) {
         HgTimed tm(ctx, st, HG_K_MODUP, macs);
         int h = hg_modup_mma_launch(ctx, ops.words, ops.bits, ops.is_signed, nops, P, out, kinv, st);
