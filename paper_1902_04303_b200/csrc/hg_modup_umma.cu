@@ -46,6 +46,7 @@ __global__ void __launch_bounds__(256) modup_umma_kernel(
     __shared__ uint32_t tmem_base;
     __shared__ __align__(8) uint64_t mbar_b[2], mbar_mma[2];
     __shared__ uint32_t flags[kRows];   // bit0 sign, bit1 negate, bit2 any-nonzero
+    __shared__ uint32_t spw[HG_MAX_PRIMES];
     const int op = blockIdx.y;
     const uint32_t* in = op == 0 ? ops.words[0] : op == 1 ? ops.words[1] : op == 2 ? ops.words[2] : ops.words[3];
     const int bits = op == 0 ? ops.bits[0] : op == 1 ? ops.bits[1] : op == 2 ? ops.bits[2] : ops.bits[3];
@@ -84,31 +85,37 @@ __global__ void __launch_bounds__(256) modup_umma_kernel(
         const uint32_t top_mask = (bits & 31) ? ((1u << (bits & 31)) - 1u) : 0xffffffffu;
         const int g = n >> 3, rr = n & 7;
         uint32_t any = 0, sign = 0;
-        for (int c = half; c < kc16; c += 2) {       // 4 words per 16-byte chunk
-            uint32_t w4[4];
+        // all of this half's loads are issued before any is consumed (32 in flight per thread)
+        uint32_t wv[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+            const int w = 4 * (half + 2 * (e >> 2)) + (e & 3);
+            wv[e] = w < W ? __ldg(in + (size_t)w * N + src) : 0u;
+        }
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc) {
+            const int c = half + 2 * cc;              // 16-byte chunk = words 4c .. 4c+3
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 const int w = 4 * c + e;
-                uint32_t v = 0;
-                if (w < W) {
-                    v = __ldg(in + (size_t)w * N + src);
-                    if (w == W - 1) {
-                        v &= top_mask;
-                        sign = is_signed ? (v >> ((bits - 1) & 31)) & 1u : 0u;
-                    }
+                if (w == W - 1) {
+                    wv[4 * cc + e] &= top_mask;
+                    sign = is_signed ? (wv[4 * cc + e] >> ((bits - 1) & 31)) & 1u : 0u;
                 }
-                any |= v;
-                w4[e] = v;
+                any |= wv[4 * cc + e];
             }
             if (4 * c < W8)
                 *reinterpret_cast<uint4*>(sa + ((size_t)(g * kc16 + c) * 8 + rr) * 16) =
-                    make_uint4(w4[0], w4[1], w4[2], w4[3]);
+                    make_uint4(wv[4 * cc], wv[4 * cc + 1], wv[4 * cc + 2], wv[4 * cc + 3]);
         }
         // both halves contribute flags
         if (half == 0) flags[n] = 0;
         __syncthreads();
         atomicOr(&flags[n], (sign ? 1u : 0u) | (neg ? 2u : 0u) | (any ? 4u : 0u));
     }
+    // 2^bits mod p_j for the sign / negation corrections, once per CTA
+    for (int j = tid; j < P; j += blockDim.x)
+        spw[j] = reduce_u64((uint64_t)modup_tab[(size_t)j * HG_MODUP_WMAX + (bits >> 5)] << (bits & 31), pinfo[j]);
     asm volatile("fence.proxy.async.shared::cta;\n");
     asm volatile("tcgen05.fence::before_thread_sync;\n");
     __syncthreads();
@@ -185,8 +192,7 @@ __global__ void __launch_bounds__(256) modup_umma_kernel(
                                    ((uint64_t)d[4 * e + 2] << 16) + ((uint64_t)d[4 * e + 3] << 24);
                 uint32_t r = reduce_u64(v, pi);
                 if (sgn || ng) {
-                    const uint32_t pw = reduce_u64((uint64_t)modup_tab[(size_t)j * HG_MODUP_WMAX + (bits >> 5)]
-                                                       << (bits & 31), pi);
+                    const uint32_t pw = spw[j];
                     if (sgn) r = r >= pw ? r - pw : r + pi.p - pw;
                     if (ng) {
                         if (is_signed) r = r ? pi.p - r : 0;
@@ -244,7 +250,9 @@ int hg_modup_umma_launch(hg_ctx* ctx, const uint32_t* const* words, const int* b
                          cudaStream_t st) {
     int maxw = 0;
     for (int k = 0; k < nops; ++k) maxw = std::max(maxw, (bits[k] + 31) >> 5);
-    if (ctx->N < kRows || maxw > kWMax) return 0;
+    // narrow operands (compact plaintexts, low levels) stay on the mma.sync path: the full-K
+    // B images (64 KB per 64 primes) would dominate their cost
+    if (ctx->N < kRows || maxw > kWMax || maxw < 24) return 0;
     int rc = hg_modup_build_umma(ctx);
     if (rc) return -rc;
     static bool attr = false;
