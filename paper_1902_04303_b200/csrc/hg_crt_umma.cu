@@ -305,7 +305,357 @@ __global__ void __launch_bounds__(2 * kRows) crt_umma_kernel(
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(256));
 }
 
+// ==========================================================================================
+// Persistent, warp-specialised variant (the production path).  One CTA per SM walks tiles of
+// 128 coefficients x one output polynomial; the whole column window (<= 64 words, N <= 512)
+// accumulates in one TMEM pass, so A (the y bytes) is consumed once per K chunk and streamed
+// through a small ring instead of being held whole.  Roles, linked by mbarrier rings:
+//   warp 0      residue producer: cp.async.bulk of 32 prime rows (16 KB) per K chunk
+//   warp 1      MMA issuer (lane 0): 4 k-steps x (1-2) tcgen05.mma per K chunk, commits free
+//               the A / B stages; the tile's last commit hands TMEM to the epilogue
+//   warp 2      B producer: the digit-layout B image of the K chunk (<= 64 KB) per stage
+//   warps 3-6   converters: residues -> y_j = x_j (Q/p_j)^{-1} -> A stage; S = sum y_j/p_j
+//   warps 7-10  epilogue: TMEM lane = coefficient: digit fold, carry chain, window emission
+// While the epilogue drains tile t, the producers and converters already fill the rings for
+// tile t+1 (TMEM is single-buffered: a 64-word window needs all 512 columns).
+constexpr int kPipeWarps = 11;
+constexpr int kRR = 3, kRA = 2, kRB = 2;
+constexpr int kResStage = 32 * kRows * 4;        // 16 KB: 32 prime rows of 128 residues
+constexpr int kAStage = kRows * kKChunk;         // 16 KB
+constexpr int kBStageMax = 64 * 8 * kKChunk;     // 64 KB: up to 64 words x 8 digits
+constexpr int kPipeMaxCols = 64;
+constexpr size_t kPipeSmem = (size_t)kRR * kResStage + (size_t)kRA * kAStage + (size_t)kRB * kBStageMax;
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar) : "memory");
+}
+
+// exact column scan for one coefficient with y_j recomputed from the residues in HBM (rare)
+__device__ void pipe_rescan_exact(const uint32_t* __restrict__ r, int P, int N, int W,
+                                  const PrimeInfo* __restrict__ pinfo,
+                                  const uint32_t* __restrict__ cinv,
+                                  const uint32_t* __restrict__ cinv_sh,
+                                  const uint32_t* __restrict__ Mtab,
+                                  const uint32_t* __restrict__ negQ, uint32_t v, int shift,
+                                  int out_bits, uint32_t* __restrict__ out, int i) {
+    const int sw = shift >> 5, sb = shift & 31;
+    const int out_w = (out_bits + 31) >> 5;
+    const uint32_t top_mask = (out_bits & 31) ? ((1u << (out_bits & 31)) - 1u) : 0xffffffffu;
+    const int T = sw + out_w + (sb ? 1 : 0);
+    const int round_col = shift > 0 ? ((shift - 1) >> 5) : -1;
+    const uint32_t round_bit = shift > 0 ? (1u << ((shift - 1) & 31)) : 0u;
+    uint64_t carry = 0;
+    uint32_t prev = 0;
+    for (int t = 0; t < T; ++t) {
+        uint64_t x = (uint64_t)v * negQ[t] + (t == round_col ? round_bit : 0u) + (uint32_t)carry;
+        uint64_t top = (carry >> 32) + (x >> 32);
+        uint64_t acc = (uint32_t)x;
+        for (int j = 0; j < P; ++j) {
+            const uint32_t p = pinfo[j].p;
+            const uint32_t y = reduce_2p(mul_shoup_lazy(r[(size_t)j * N + i], cinv[j], cinv_sh[j], p), p);
+            acc += (uint64_t)y * Mtab[(size_t)j * W + t];
+            top += acc >> 32;
+            acc &= 0xffffffffull;
+        }
+        const uint32_t word = (uint32_t)acc;
+        carry = top;
+        if (t >= sw) {
+            if (sb == 0) {
+                const int u = t - sw;
+                out[(size_t)u * N + i] = (u == out_w - 1) ? (word & top_mask) : word;
+            } else if (t > sw) {
+                const int u = t - sw - 1;
+                const uint32_t o = (prev >> sb) | (word << (32 - sb));
+                out[(size_t)u * N + i] = (u == out_w - 1) ? (o & top_mask) : o;
+            }
+        }
+        prev = word;
+    }
+}
+
+__global__ void __launch_bounds__(kPipeWarps * 32, 1) crt_umma_pipe_kernel(
+    const uint32_t* __restrict__ res, int P, int P32, int N, int nouts,
+    const PrimeInfo* __restrict__ pinfo, const uint8_t* __restrict__ Bconv,
+    const uint32_t* __restrict__ Mtab, int W, const uint32_t* __restrict__ negQ,
+    const uint32_t* __restrict__ cinv, const uint32_t* __restrict__ cinv_sh,
+    const double* __restrict__ invp, int shift, int out_bits, int tb0, UOuts outs) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t* s_res = smem;
+    uint8_t* s_a = smem + kRR * kResStage;
+    uint8_t* s_b = s_a + kRA * kAStage;
+    __shared__ __align__(8) uint64_t bar_res_full[kRR], bar_res_empty[kRR];
+    __shared__ __align__(8) uint64_t bar_a_full[kRA], bar_a_empty[kRA];
+    __shared__ __align__(8) uint64_t bar_b_full[kRB], bar_b_empty[kRB];
+    __shared__ __align__(8) uint64_t bar_tm_full, bar_tm_empty;
+    __shared__ __align__(8) uint64_t bar_v_full[2], bar_v_empty[2];
+    __shared__ uint32_t tmem_base;
+    __shared__ uint32_t s_v[2][kRows];
+    __shared__ uint32_t s_p[HG_MAX_PRIMES], s_ci[HG_MAX_PRIMES], s_cs[HG_MAX_PRIMES];
+    __shared__ double s_ip[HG_MAX_PRIMES];
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    for (int j = tid; j < P32; j += blockDim.x) {
+        const bool ok = j < P;
+        s_p[j] = ok ? pinfo[j].p : 1u;
+        s_ci[j] = ok ? cinv[j] : 0u;
+        s_cs[j] = ok ? cinv_sh[j] : 0u;
+        s_ip[j] = ok ? invp[j] : 0.0;
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base)), "n"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    if (tid == 0) {
+        auto init = [](uint64_t* b, int cnt) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(cnt));
+        };
+        for (int s = 0; s < kRR; ++s) { init(&bar_res_full[s], 1); init(&bar_res_empty[s], 4); }
+        for (int s = 0; s < kRA; ++s) { init(&bar_a_full[s], 4); init(&bar_a_empty[s], 1); }
+        for (int s = 0; s < kRB; ++s) { init(&bar_b_full[s], 1); init(&bar_b_empty[s], 1); }
+        init(&bar_tm_full, 1);
+        init(&bar_tm_empty, 4);
+        for (int s = 0; s < 2; ++s) { init(&bar_v_full[s], 4); init(&bar_v_empty[s], 4); }
+        asm volatile("fence.mbarrier_init.release.cluster;\n");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    const uint32_t tmem = tmem_base;
+
+    const int tpo = N / kRows;
+    const int ntiles = nouts * tpo;
+    const int nkc = P32 / 32;
+    const int sw = shift >> 5, sbit = shift & 31;
+    const int out_w = (out_bits + 31) >> 5;
+    const int T = sw + out_w + (sbit ? 1 : 0);
+    const int ncols = ((T - tb0) + 1) & ~1;            // host guarantees <= kPipeMaxCols
+    const uint32_t bbytes = (uint32_t)((ncols + 7) >> 3) * 8192u;
+
+    if (warp == 0) {
+        // ---------------- residue producer ----------------
+        int it = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            const int oy = tile / tpo, cb = (tile - oy * tpo) * kRows;
+            const uint32_t* r = res + (size_t)oy * P * N + cb;
+            for (int kc = 0; kc < nkc; ++kc, ++it) {
+                const int s = it % kRR;
+                mbar_wait(smem_u32(&bar_res_empty[s]), ((it / kRR) & 1) ^ 1);
+                const int cnt = P - kc * 32 < 32 ? P - kc * 32 : 32;
+                if (lane == 0) mbar_expect_tx(smem_u32(&bar_res_full[s]), (uint32_t)cnt * kRows * 4);
+                __syncwarp();
+                if (lane < cnt)
+                    bulk_g2s(smem_u32(s_res + s * kResStage + lane * kRows * 4),
+                             r + (size_t)(kc * 32 + lane) * N, kRows * 4, smem_u32(&bar_res_full[s]));
+            }
+        }
+    } else if (warp == 2) {
+        // ---------------- B producer ----------------
+        if (lane == 0) {
+            int it = 0;
+            const uint8_t* bsrc = Bconv + (size_t)(tb0 >> 3) * 8192;
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
+                for (int kc = 0; kc < nkc; ++kc, ++it) {
+                    const int s = it % kRB;
+                    mbar_wait(smem_u32(&bar_b_empty[s]), ((it / kRB) & 1) ^ 1);
+                    mbar_expect_tx(smem_u32(&bar_b_full[s]), bbytes);
+                    bulk_g2s(smem_u32(s_b + s * kBStageMax), bsrc + (size_t)kc * (W >> 3) * 8192, bbytes,
+                             smem_u32(&bar_b_full[s]));
+                }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer ----------------
+        if (lane == 0) {
+            const uint32_t Nn = 8u * (uint32_t)ncols;
+            const int nh = Nn > 256 ? 2 : 1;
+            uint32_t idesc[2];
+            for (int h = 0; h < 2; ++h) {
+                const uint32_t nh_cols = h == 0 ? (Nn < 256 ? Nn : 256u) : (Nn > 256 ? Nn - 256 : 16u);
+                idesc[h] = (2u << 4) | ((nh_cols >> 3) << 17) | ((uint32_t)(kRows >> 4) << 24);
+            }
+            const uint32_t a_base = smem_u32(s_a), b_base = smem_u32(s_b);
+            int ia = 0, ib = 0, tt = 0;
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tt) {
+                mbar_wait(smem_u32(&bar_tm_empty), (tt & 1) ^ 1);
+                asm volatile("tcgen05.fence::after_thread_sync;\n");
+                for (int kc = 0; kc < nkc; ++kc, ++ia, ++ib) {
+                    const int sa_ = ia % kRA, sb_ = ib % kRB;
+                    mbar_wait(smem_u32(&bar_a_full[sa_]), (ia / kRA) & 1);
+                    mbar_wait(smem_u32(&bar_b_full[sb_]), (ib / kRB) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;\n");
+#pragma unroll
+                    for (int k = 0; k < kKChunk / 32; ++k) {
+                        const uint64_t da = umma_desc(a_base + (uint32_t)(sa_ * kAStage + 2 * k * 128), 128, 1024);
+                        const uint32_t acc = (kc > 0 || k > 0) ? 1u : 0u;
+                        for (int h = 0; h < nh; ++h) {
+                            const uint64_t db = umma_desc(b_base + (uint32_t)(sb_ * kBStageMax + h * 32768 + 2 * k * 128), 128, 1024);
+                            asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                                         "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n"
+                                         ::"r"(tmem + (uint32_t)(h * 256)), "l"(da), "l"(db), "r"(idesc[h]), "r"(acc));
+                        }
+                    }
+                    umma_commit(smem_u32(&bar_a_empty[sa_]));
+                    umma_commit(smem_u32(&bar_b_empty[sb_]));
+                }
+                umma_commit(smem_u32(&bar_tm_full));
+            }
+        }
+    } else if (warp <= 6) {
+        // ---------------- converters ----------------
+        const int n = (warp - 3) * 32 + lane;
+        const int g = n >> 3, rr = n & 7;
+        int ir = 0, ia = 0, tt = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tt) {
+            double S = 0.0;
+            for (int kc = 0; kc < nkc; ++kc, ++ir, ++ia) {
+                const int s = ir % kRR, sa_ = ia % kRA;
+                mbar_wait(smem_u32(&bar_res_full[s]), (ir / kRR) & 1);
+                mbar_wait(smem_u32(&bar_a_empty[sa_]), ((ia / kRA) & 1) ^ 1);
+                const uint32_t* stg = reinterpret_cast<const uint32_t*>(s_res + s * kResStage);
+                uint8_t* dst = s_a + sa_ * kAStage + (g * 8) * 128 + rr * 16;
+                const int j0 = kc * 32;
+                uint32_t x[32];
+#pragma unroll
+                for (int u = 0; u < 32; ++u) x[u] = stg[u * kRows + n];
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    uint32_t y[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int j = j0 + 4 * c + u;
+                        const uint32_t p = s_p[j];
+                        // padding primes: x is stale but cinv = 0 gives y = 0
+                        y[u] = reduce_2p(mul_shoup_lazy(x[4 * c + u], s_ci[j], s_cs[j], p), p);
+                        S += (double)y[u] * s_ip[j];
+                    }
+                    *reinterpret_cast<uint4*>(dst + c * 128) = make_uint4(y[0], y[1], y[2], y[3]);
+                }
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(smem_u32(&bar_res_empty[s]));
+                    mbar_arrive(smem_u32(&bar_a_full[sa_]));
+                }
+            }
+            const int vb = tt & 1;
+            mbar_wait(smem_u32(&bar_v_empty[vb]), ((tt >> 1) & 1) ^ 1);
+            s_v[vb][n] = (uint32_t)floor(S + 0.5);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&bar_v_full[vb]));
+        }
+    } else {
+        // ---------------- epilogue ----------------
+        const int q = warp & 3;
+        const int n = q * 32 + lane;
+        const uint32_t top_mask = (out_bits & 31) ? ((1u << (out_bits & 31)) - 1u) : 0xffffffffu;
+        const int round_col = shift > 0 ? ((shift - 1) >> 5) : -1;
+        const uint32_t round_bit = shift > 0 ? (1u << ((shift - 1) & 31)) : 0u;
+        const uint32_t lane_addr = tmem + ((uint32_t)(q * 32) << 16);
+        int tt = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tt) {
+            const int oy = tile / tpo, cb = (tile - oy * tpo) * kRows;
+            uint32_t* out = oy == 0 ? outs.out[0] : oy == 1 ? outs.out[1] : oy == 2 ? outs.out[2] : outs.out[3];
+            const int i = cb + n;
+            const int vb = tt & 1;
+            mbar_wait(smem_u32(&bar_v_full[vb]), (tt >> 1) & 1);
+            const uint32_t v = s_v[vb][n];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&bar_v_empty[vb]));
+            mbar_wait(smem_u32(&bar_tm_full), tt & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;\n");
+            uint64_t carry = 0;
+            uint32_t prev = 0;
+            bool amb = false;
+            for (int tl = 0; tl < ncols; tl += 4) {
+                uint32_t e[32];
+                asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                             "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+                             : "=r"(e[0]), "=r"(e[1]), "=r"(e[2]), "=r"(e[3]), "=r"(e[4]), "=r"(e[5]),
+                               "=r"(e[6]), "=r"(e[7]), "=r"(e[8]), "=r"(e[9]), "=r"(e[10]), "=r"(e[11]),
+                               "=r"(e[12]), "=r"(e[13]), "=r"(e[14]), "=r"(e[15]), "=r"(e[16]), "=r"(e[17]),
+                               "=r"(e[18]), "=r"(e[19]), "=r"(e[20]), "=r"(e[21]), "=r"(e[22]), "=r"(e[23]),
+                               "=r"(e[24]), "=r"(e[25]), "=r"(e[26]), "=r"(e[27]), "=r"(e[28]), "=r"(e[29]),
+                               "=r"(e[30]), "=r"(e[31])
+                             : "r"(lane_addr + (uint32_t)(tl * 8)));
+                asm volatile("tcgen05.wait::ld.sync.aligned;\n");
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    const int t = tb0 + tl + h;
+                    if (t >= T) break;
+                    const uint32_t* E = e + 8 * h;
+                    const uint64_t lo = (uint64_t)E[0] + ((uint64_t)E[1] << 8) + ((uint64_t)E[2] << 16) + ((uint64_t)E[3] << 24);
+                    const uint64_t hi = (uint64_t)E[4] + ((uint64_t)E[5] << 8) + ((uint64_t)E[6] << 16) + ((uint64_t)E[7] << 24);
+                    const uint64_t extra = (uint64_t)v * negQ[t] + (t == round_col ? round_bit : 0u);
+                    const uint64_t sum = (lo & 0xffffffffull) + (carry & 0xffffffffull) + (extra & 0xffffffffull);
+                    const uint32_t word = (uint32_t)sum;
+                    carry = (sum >> 32) + (lo >> 32) + hi + (carry >> 32) + (extra >> 32);
+                    if (t < sw) {
+                        if (t == tb0 + 1) amb = word >= 0xFFFFFF00u;
+                        else if (t > tb0 + 1) amb = amb && (word == 0xffffffffu);
+                    } else if (sbit == 0) {
+                        const int u = t - sw;
+                        out[(size_t)u * N + i] = (u == out_w - 1) ? (word & top_mask) : word;
+                    } else if (t > sw) {
+                        const int u = t - sw - 1;
+                        const uint32_t o = (prev >> sbit) | (word << (32 - sbit));
+                        out[(size_t)u * N + i] = (u == out_w - 1) ? (o & top_mask) : o;
+                    }
+                    prev = word;
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;\n");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&bar_tm_empty));
+            if (tb0 > 0 && amb)
+                pipe_rescan_exact(res + (size_t)oy * P * N, P, N, W, pinfo, cinv, cinv_sh, Mtab, negQ, v,
+                                  shift, out_bits, out, i);
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(512));
+}
+
 }  // namespace
+
+// true when the pipelined kernel covers this window
+bool hg_crt_umma_pipe_ok(const CrtTable* tab, int N, int shift, int out_bits, int tb0) {
+    const int sw = shift >> 5, sbit = shift & 31;
+    const int T = sw + (out_bits + 31) / 32 + (sbit ? 1 : 0);
+    const int ncols = ((T - tb0) + 1) & ~1;
+    return N % kRows == 0 && ncols >= 2 && ncols <= kPipeMaxCols &&
+           tb0 + 8 * ((ncols + 7) >> 3) <= tab->W && (tb0 & 7) == 0;
+}
+
+int hg_crt_umma_pipe_launch(hg_ctx* ctx, const CrtTable* tab, const uint32_t* res, int nouts, int P,
+                            int shift, int out_bits, int tb0, uint32_t* const* outs_in,
+                            cudaStream_t st) {
+    static int nsm = 0;
+    if (!nsm) {
+        HG_CUDA_TRY(cudaFuncSetAttribute(crt_umma_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kPipeSmem));
+        HG_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device));
+    }
+    UOuts o{};
+    for (int k = 0; k < nouts; ++k) o.out[k] = outs_in[k];
+    const int ntiles = nouts * (ctx->N / kRows);
+    const int grid = ntiles < nsm ? ntiles : nsm;
+    crt_umma_pipe_kernel<<<grid, kPipeWarps * 32, kPipeSmem, st>>>(
+        res, P, tab->P32, ctx->N, nouts, ctx->d_pinfo, tab->d_Bconv, tab->d_M, tab->W, tab->d_negQ,
+        tab->d_cinv, tab->d_cinv_sh, tab->d_invp, shift, out_bits, tb0, o);
+    HG_LAUNCH_CHECK(ctx);
+    return HG_OK;
+}
 
 // B in the digit layout, pre-arranged as the exact shared-memory image the kernel copies:
 // [K chunk kc (32 primes)][8-column group tg][row group t (8 rows: digits s)][16-byte K chunk c]

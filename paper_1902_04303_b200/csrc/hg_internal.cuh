@@ -141,6 +141,10 @@ int hg_crt_build_conv(const CrtTable& t, int P, int P32, std::vector<uint8_t>& o
 int hg_crt_umma_launch(hg_ctx* ctx, const CrtTable* tab, const uint32_t* res, int nouts, int P,
                        int shift, int out_bits, int tb0, uint32_t* const* outs, cudaStream_t st);
 size_t hg_crt_umma_smem(int P32);
+bool hg_crt_umma_pipe_ok(const CrtTable* tab, int N, int shift, int out_bits, int tb0);
+int hg_crt_umma_pipe_launch(hg_ctx* ctx, const CrtTable* tab, const uint32_t* res, int nouts, int P,
+                            int shift, int out_bits, int tb0, uint32_t* const* outs,
+                            cudaStream_t st);
 int hg_modup_umma_launch(hg_ctx* ctx, const uint32_t* const* words, const int* bits,
                          const int* is_signed, int nops, int P, uint32_t* out, int64_t kinv,
                          cudaStream_t st);

@@ -433,6 +433,12 @@ int launch_crt(hg_ctx* ctx, const uint32_t* res, int nouts, int P, int shift, in
     const int threads = N < kCrtThreads ? N : kCrtThreads;
     size_t smem = (size_t)tab->P4 * threads * 4;
     dim3 grid(N / threads, nouts);
+    if (N >= 128 && !getenv("HG_NO_UMMA") && !getenv("HG_NO_MMA") && !getenv("HG_NO_PIPE") &&
+        hg_crt_umma_pipe_ok(tab, N, shift, out_bits, tb0)) {
+        // persistent warp-specialised tcgen05 path
+        HgTimed tm(ctx, st, HG_K_CRT, (double)nouts * N * (double)P * (T - tb0));
+        return hg_crt_umma_pipe_launch(ctx, tab, res, nouts, P, shift, out_bits, tb0, outs.out, st);
+    }
     if (N >= 128 && !getenv("HG_NO_UMMA") && !getenv("HG_NO_MMA") &&
         hg_crt_umma_smem(tab->P32) <= 220 * 1024) {
         // tcgen05 path (UTCIMMA, accumulators in TMEM)
