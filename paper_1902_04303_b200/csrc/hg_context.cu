@@ -145,6 +145,7 @@ extern "C" int hg_ctx_destroy(hg_ctx* ctx) {
         cudaFree(kv.second.d_invp);
         cudaFree(kv.second.d_Bfrag);
         cudaFree(kv.second.d_Bconv);
+        cudaFree(kv.second.d_Bpipe);
     }
     delete ctx;
     return HG_OK;
@@ -268,6 +269,34 @@ int hg_ensure_twiddles(hg_ctx* ctx, int P) {
     return HG_OK;
 }
 
+// ---- TMA tensor maps ------------------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+int hg_tmap_2d_u32(CUtensorMap* tm, const void* base, uint64_t inner, uint64_t outer,
+                   uint32_t box_inner, uint32_t box_outer) {
+    static EncodeTiledFn encode = nullptr;
+    if (!encode) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn)
+            return hg_fail(HG_ECUDA, "cuTensorMapEncodeTiled entry point unavailable");
+        encode = (EncodeTiledFn)fn;
+    }
+    const cuuint64_t dims[2] = {inner, outer};
+    const cuuint64_t strides[1] = {inner * 4};
+    const cuuint32_t box[2] = {box_inner, box_outer};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void*>(base), dims, strides,
+                        box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return hg_fail(HG_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    return HG_OK;
+}
+
 // ---- CRT tables ---------------------------------------------------------------------------
 // multiply a little-endian word array (truncated to W words) by a 32-bit value in place
 static void mul_small_trunc(std::vector<uint32_t>& a, uint32_t m) {
@@ -347,6 +376,14 @@ int hg_get_crt(hg_ctx* ctx, int P, const CrtTable** out) {
         hg_crt_build_conv(t, P, t.P32, conv, M);
         HG_CUDA_TRY(cudaMalloc(&t.d_Bconv, conv.size()));
         HG_CUDA_TRY(cudaMemcpy(t.d_Bconv, conv.data(), conv.size(), cudaMemcpyHostToDevice));
+        // pipelined kernel: one more K row (slot P) carries -Q, so v * (-Q) comes out of the GEMM
+        t.P32p = (P + 1 + 31) & ~31;
+        std::vector<uint32_t> Mp((size_t)W * t.P32p, 0u);
+        std::copy(M.begin(), M.begin() + (size_t)W * P, Mp.begin());
+        std::copy(negQ.begin(), negQ.end(), Mp.begin() + (size_t)W * P);
+        hg_crt_build_conv(t, P + 1, t.P32p, conv, Mp);
+        HG_CUDA_TRY(cudaMalloc(&t.d_Bpipe, conv.size()));
+        HG_CUDA_TRY(cudaMemcpy(t.d_Bpipe, conv.data(), conv.size(), cudaMemcpyHostToDevice));
     }
     std::lock_guard<std::mutex> lk(ctx->mu);
     auto ins = ctx->crt.emplace(P, t);
@@ -354,6 +391,7 @@ int hg_get_crt(hg_ctx* ctx, int P, const CrtTable** out) {
         cudaFree(t.d_M); cudaFree(t.d_negQ); cudaFree(t.d_cinv); cudaFree(t.d_cinv_sh); cudaFree(t.d_invp);
         cudaFree(t.d_Bfrag);
         cudaFree(t.d_Bconv);
+        cudaFree(t.d_Bpipe);
     }
     *out = &ins.first->second;
     return HG_OK;

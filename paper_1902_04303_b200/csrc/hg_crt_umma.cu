@@ -306,25 +306,27 @@ __global__ void __launch_bounds__(2 * kRows) crt_umma_kernel(
 }
 
 // ==========================================================================================
-// Persistent, warp-specialised variant (the production path).  One CTA per SM walks tiles of
-// 128 coefficients x one output polynomial; the whole column window (<= 64 words, N <= 512)
-// accumulates in one TMEM pass, so A (the y bytes) is consumed once per K chunk and streamed
-// through a small ring instead of being held whole.  Roles, linked by mbarrier rings:
+// Persistent, warp-specialised variant (the production path).  One CTA per SM walks jobs =
+// (tile of 128 coefficients of one output polynomial, block of <= 32 output words): N <= 256 per
+// job, so TMEM holds two job accumulators and the epilogue of job i overlaps the MMAs of job
+// i+1.  The y bytes (A) are streamed per K chunk through a ring (recomputed for each column
+// block of a tile: the residues come back from L2).  The reduction term v * (-Q) is one more K
+// row (slot P: A = v, B = the digits of -Q mod 2^(32W)), so the epilogue only folds digits and
+// runs the carry chain.  Roles, linked by mbarrier rings:
 //   warp 0      residue producer: cp.async.bulk of 32 prime rows (16 KB) per K chunk
-//   warp 1      MMA issuer (lane 0): 4 k-steps x (1-2) tcgen05.mma per K chunk, commits free
-//               the A / B stages; the tile's last commit hands TMEM to the epilogue
-//   warp 2      B producer: the digit-layout B image of the K chunk (<= 64 KB) per stage
-//   warps 3-6   converters: residues -> y_j = x_j (Q/p_j)^{-1} -> A stage; S = sum y_j/p_j
-//   warps 7-10  epilogue: TMEM lane = coefficient: digit fold, carry chain, window emission
-// While the epilogue drains tile t, the producers and converters already fill the rings for
-// tile t+1 (TMEM is single-buffered: a 64-word window needs all 512 columns).
-constexpr int kPipeWarps = 11;
-constexpr int kRR = 3, kRA = 2, kRB = 2;
+//   warp 1      MMA issuer (lane 0): 4 k-steps of 128 x N x 32 per K chunk; commits free the
+//               A / B stages, the job's last commit hands its TMEM buffer to the epilogue
+//   warp 2      B producer: the job's digit-layout B slice of the K chunk (<= 32 KB) per stage
+//   warps 3-10  converters: residues -> y_j = x_j (Q/p_j)^{-1} -> A stage; v = round(sum y_j/p_j)
+//   warps 11-18 epilogue, two groups of 4 taking alternate jobs: TMEM lane = coefficient:
+//               digit fold, carry chain (handed between the groups), window emission
+constexpr int kConvWarp0 = 3, kEpiWarp0 = 11, kPipeWarps = 19;
+constexpr int kRR = 3, kRA = 4, kRB = 3;
+constexpr int kJobCols = 32;                     // output words per job (N = 256)
 constexpr int kResStage = 32 * kRows * 4;        // 16 KB: 32 prime rows of 128 residues
 constexpr int kAStage = kRows * kKChunk;         // 16 KB
-constexpr int kBStageMax = 64 * 8 * kKChunk;     // 64 KB: up to 64 words x 8 digits
-constexpr int kPipeMaxCols = 64;
-constexpr size_t kPipeSmem = (size_t)kRR * kResStage + (size_t)kRA * kAStage + (size_t)kRB * kBStageMax;
+constexpr int kBStagePipe = kJobCols * 8 * kKChunk;   // 32 KB
+constexpr size_t kPipeSmem = (size_t)kRR * kResStage + (size_t)kRA * kAStage + (size_t)kRB * kBStagePipe;
 
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
@@ -341,14 +343,21 @@ __device__ __forceinline__ void umma_commit(uint32_t bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar) : "memory");
 }
 
-// exact column scan for one coefficient with y_j recomputed from the residues in HBM (rare)
+// exact column scan for one coefficient with y_j and v recomputed from the residues (rare)
 __device__ void pipe_rescan_exact(const uint32_t* __restrict__ r, int P, int N, int W,
                                   const PrimeInfo* __restrict__ pinfo,
                                   const uint32_t* __restrict__ cinv,
                                   const uint32_t* __restrict__ cinv_sh,
+                                  const double* __restrict__ invp,
                                   const uint32_t* __restrict__ Mtab,
-                                  const uint32_t* __restrict__ negQ, uint32_t v, int shift,
-                                  int out_bits, uint32_t* __restrict__ out, int i) {
+                                  const uint32_t* __restrict__ negQ, int shift, int out_bits,
+                                  uint32_t* __restrict__ out, int i) {
+    double S = 0.0;
+    for (int j = 0; j < P; ++j) {
+        const uint32_t p = pinfo[j].p;
+        S += (double)reduce_2p(mul_shoup_lazy(r[(size_t)j * N + i], cinv[j], cinv_sh[j], p), p) * invp[j];
+    }
+    const uint32_t v = (uint32_t)floor(S + 0.5);
     const int sw = shift >> 5, sb = shift & 31;
     const int out_w = (out_bits + 31) >> 5;
     const uint32_t top_mask = (out_bits & 31) ? ((1u << (out_bits & 31)) - 1u) : 0xffffffffu;
@@ -385,8 +394,8 @@ __device__ void pipe_rescan_exact(const uint32_t* __restrict__ r, int P, int N, 
 }
 
 __global__ void __launch_bounds__(kPipeWarps * 32, 1) crt_umma_pipe_kernel(
-    const uint32_t* __restrict__ res, int P, int P32, int N, int nouts,
-    const PrimeInfo* __restrict__ pinfo, const uint8_t* __restrict__ Bconv,
+    const __grid_constant__ CUtensorMap res_map, const uint32_t* __restrict__ res, int P, int P32p, int N, int nouts,
+    const PrimeInfo* __restrict__ pinfo, const uint8_t* __restrict__ Bpipe,
     const uint32_t* __restrict__ Mtab, int W, const uint32_t* __restrict__ negQ,
     const uint32_t* __restrict__ cinv, const uint32_t* __restrict__ cinv_sh,
     const double* __restrict__ invp, int shift, int out_bits, int tb0, UOuts outs) {
@@ -397,20 +406,18 @@ __global__ void __launch_bounds__(kPipeWarps * 32, 1) crt_umma_pipe_kernel(
     __shared__ __align__(8) uint64_t bar_res_full[kRR], bar_res_empty[kRR];
     __shared__ __align__(8) uint64_t bar_a_full[kRA], bar_a_empty[kRA];
     __shared__ __align__(8) uint64_t bar_b_full[kRB], bar_b_empty[kRB];
-    __shared__ __align__(8) uint64_t bar_tm_full, bar_tm_empty;
-    __shared__ __align__(8) uint64_t bar_v_full[2], bar_v_empty[2];
+    __shared__ __align__(8) uint64_t bar_tm_full[2], bar_tm_empty[2];
+    __shared__ __align__(8) uint64_t bar_hand_full[2], bar_hand_empty[2];
+    __shared__ uint4 s_hand[2][kRows];             // carry lo/hi, previous word, ambiguity
     __shared__ uint32_t tmem_base;
-    __shared__ uint32_t s_v[2][kRows];
-    __shared__ uint32_t s_p[HG_MAX_PRIMES], s_ci[HG_MAX_PRIMES], s_cs[HG_MAX_PRIMES];
-    __shared__ double s_ip[HG_MAX_PRIMES];
+    __shared__ uint4 s_pc[HG_MAX_PRIMES + 32];     // p, cinv, cinv_sh, floor(2^53/p) (1,0,0,0 padding)
+    __shared__ uint64_t s_acc[2][kRows];
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    for (int j = tid; j < P32; j += blockDim.x) {
+    for (int j = tid; j < P32p; j += blockDim.x) {
         const bool ok = j < P;
-        s_p[j] = ok ? pinfo[j].p : 1u;
-        s_ci[j] = ok ? cinv[j] : 0u;
-        s_cs[j] = ok ? cinv_sh[j] : 0u;
-        s_ip[j] = ok ? invp[j] : 0.0;
+        const uint32_t p = ok ? pinfo[j].p : 1u;
+        s_pc[j] = ok ? make_uint4(p, cinv[j], cinv_sh[j], (uint32_t)((1ull << 53) / p)) : make_uint4(1u, 0u, 0u, 0u);
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base)), "n"(512));
@@ -420,12 +427,11 @@ __global__ void __launch_bounds__(kPipeWarps * 32, 1) crt_umma_pipe_kernel(
         auto init = [](uint64_t* b, int cnt) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(cnt));
         };
-        for (int s = 0; s < kRR; ++s) { init(&bar_res_full[s], 1); init(&bar_res_empty[s], 4); }
-        for (int s = 0; s < kRA; ++s) { init(&bar_a_full[s], 4); init(&bar_a_empty[s], 1); }
+        for (int s = 0; s < kRR; ++s) { init(&bar_res_full[s], 1); init(&bar_res_empty[s], 8); }
+        for (int s = 0; s < kRA; ++s) { init(&bar_a_full[s], 8); init(&bar_a_empty[s], 1); }
         for (int s = 0; s < kRB; ++s) { init(&bar_b_full[s], 1); init(&bar_b_empty[s], 1); }
-        init(&bar_tm_full, 1);
-        init(&bar_tm_empty, 4);
-        for (int s = 0; s < 2; ++s) { init(&bar_v_full[s], 4); init(&bar_v_empty[s], 4); }
+        for (int s = 0; s < 2; ++s) { init(&bar_tm_full[s], 1); init(&bar_tm_empty[s], 4); }
+        for (int s = 0; s < 2; ++s) { init(&bar_hand_full[s], 4); init(&bar_hand_empty[s], 4); }
         asm volatile("fence.mbarrier_init.release.cluster;\n");
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n");
@@ -434,59 +440,69 @@ __global__ void __launch_bounds__(kPipeWarps * 32, 1) crt_umma_pipe_kernel(
     const uint32_t tmem = tmem_base;
 
     const int tpo = N / kRows;
-    const int ntiles = nouts * tpo;
-    const int nkc = P32 / 32;
     const int sw = shift >> 5, sbit = shift & 31;
     const int out_w = (out_bits + 31) >> 5;
     const int T = sw + out_w + (sbit ? 1 : 0);
-    const int ncols = ((T - tb0) + 1) & ~1;            // host guarantees <= kPipeMaxCols
-    const uint32_t bbytes = (uint32_t)((ncols + 7) >> 3) * 8192u;
+    const int jpt = (T - tb0 + kJobCols - 1) / kJobCols;   // jobs (column blocks) per tile
+    const int ntiles = nouts * tpo;
+    const int nkc = P32p / 32;
+    // columns of job block h: [tb0 + 32h, min(T, tb0 + 32h + 32)), padded to an even count
+    auto job_cols = [&](int h) {
+        const int c0 = tb0 + h * kJobCols;
+        const int c = (T - c0 < kJobCols ? T - c0 : kJobCols);
+        return (c + 1) & ~1;
+    };
 
     if (warp == 0) {
         // ---------------- residue producer ----------------
-        int it = 0;
-        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-            const int oy = tile / tpo, cb = (tile - oy * tpo) * kRows;
-            const uint32_t* r = res + (size_t)oy * P * N + cb;
-            for (int kc = 0; kc < nkc; ++kc, ++it) {
-                const int s = it % kRR;
-                mbar_wait(smem_u32(&bar_res_empty[s]), ((it / kRR) & 1) ^ 1);
-                const int cnt = P - kc * 32 < 32 ? P - kc * 32 : 32;
-                if (lane == 0) mbar_expect_tx(smem_u32(&bar_res_full[s]), (uint32_t)cnt * kRows * 4);
-                __syncwarp();
-                if (lane < cnt)
-                    bulk_g2s(smem_u32(s_res + s * kResStage + lane * kRows * 4),
-                             r + (size_t)(kc * 32 + lane) * N, kRows * 4, smem_u32(&bar_res_full[s]));
-            }
+        // one 2-D TMA box (128 coefficients x 32 prime rows) per K chunk; rows past P belong to
+        // the next output (or are zero-filled past the end) and meet cinv = 0 in the converters
+        if (lane == 0) {
+            int it = 0;
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
+                for (int h = 0; h < jpt; ++h) {
+                    const int oy = tile / tpo, cb = (tile - oy * tpo) * kRows;
+                    for (int kc = 0; kc < nkc; ++kc, ++it) {
+                        const int s = it % kRR;
+                        mbar_wait(smem_u32(&bar_res_empty[s]), ((it / kRR) & 1) ^ 1);
+                        mbar_expect_tx(smem_u32(&bar_res_full[s]), (uint32_t)kResStage);
+                        asm volatile(
+                            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                            " [%0], [%1, {%2, %3}], [%4];\n"
+                            ::"r"(smem_u32(s_res + s * kResStage)), "l"(reinterpret_cast<uint64_t>(&res_map)),
+                            "r"(cb), "r"(oy * P + kc * 32), "r"(smem_u32(&bar_res_full[s]))
+                            : "memory");
+                    }
+                }
         }
     } else if (warp == 2) {
         // ---------------- B producer ----------------
         if (lane == 0) {
             int it = 0;
-            const uint8_t* bsrc = Bconv + (size_t)(tb0 >> 3) * 8192;
             for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
+              for (int h = 0; h < jpt; ++h) {
+                const uint32_t bytes = (uint32_t)((job_cols(h) + 7) >> 3) * 8192u;
+                const uint8_t* bsrc = Bpipe + (size_t)((tb0 >> 3) + h * (kJobCols / 8)) * 8192;
                 for (int kc = 0; kc < nkc; ++kc, ++it) {
                     const int s = it % kRB;
                     mbar_wait(smem_u32(&bar_b_empty[s]), ((it / kRB) & 1) ^ 1);
-                    mbar_expect_tx(smem_u32(&bar_b_full[s]), bbytes);
-                    bulk_g2s(smem_u32(s_b + s * kBStageMax), bsrc + (size_t)kc * (W >> 3) * 8192, bbytes,
+                    mbar_expect_tx(smem_u32(&bar_b_full[s]), bytes);
+                    bulk_g2s(smem_u32(s_b + s * kBStagePipe), bsrc + (size_t)kc * (W >> 3) * 8192, bytes,
                              smem_u32(&bar_b_full[s]));
                 }
+            }
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer ----------------
         if (lane == 0) {
-            const uint32_t Nn = 8u * (uint32_t)ncols;
-            const int nh = Nn > 256 ? 2 : 1;
-            uint32_t idesc[2];
-            for (int h = 0; h < 2; ++h) {
-                const uint32_t nh_cols = h == 0 ? (Nn < 256 ? Nn : 256u) : (Nn > 256 ? Nn - 256 : 16u);
-                idesc[h] = (2u << 4) | ((nh_cols >> 3) << 17) | ((uint32_t)(kRows >> 4) << 24);
-            }
             const uint32_t a_base = smem_u32(s_a), b_base = smem_u32(s_b);
-            int ia = 0, ib = 0, tt = 0;
-            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tt) {
-                mbar_wait(smem_u32(&bar_tm_empty), (tt & 1) ^ 1);
+            int ia = 0, ib = 0, ij = 0;
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
+              for (int h = 0; h < jpt; ++h, ++ij) {
+                const uint32_t Nn = 8u * (uint32_t)job_cols(h);
+                const uint32_t idesc = (2u << 4) | ((Nn >> 3) << 17) | ((uint32_t)(kRows >> 4) << 24);
+                const int tb = ij & 1;
+                mbar_wait(smem_u32(&bar_tm_empty[tb]), ((ij >> 1) & 1) ^ 1);
                 asm volatile("tcgen05.fence::after_thread_sync;\n");
                 for (int kc = 0; kc < nkc; ++kc, ++ia, ++ib) {
                     const int sa_ = ia % kRA, sb_ = ib % kRB;
@@ -496,62 +512,69 @@ __global__ void __launch_bounds__(kPipeWarps * 32, 1) crt_umma_pipe_kernel(
 #pragma unroll
                     for (int k = 0; k < kKChunk / 32; ++k) {
                         const uint64_t da = umma_desc(a_base + (uint32_t)(sa_ * kAStage + 2 * k * 128), 128, 1024);
+                        const uint64_t db = umma_desc(b_base + (uint32_t)(sb_ * kBStagePipe + 2 * k * 128), 128, 1024);
                         const uint32_t acc = (kc > 0 || k > 0) ? 1u : 0u;
-                        for (int h = 0; h < nh; ++h) {
-                            const uint64_t db = umma_desc(b_base + (uint32_t)(sb_ * kBStageMax + h * 32768 + 2 * k * 128), 128, 1024);
-                            asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-                                         "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n"
-                                         ::"r"(tmem + (uint32_t)(h * 256)), "l"(da), "l"(db), "r"(idesc[h]), "r"(acc));
-                        }
+                        asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                                     "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n"
+                                     ::"r"(tmem + (uint32_t)(tb * 256)), "l"(da), "l"(db), "r"(idesc), "r"(acc));
                     }
                     umma_commit(smem_u32(&bar_a_empty[sa_]));
                     umma_commit(smem_u32(&bar_b_empty[sb_]));
                 }
-                umma_commit(smem_u32(&bar_tm_full));
+                umma_commit(smem_u32(&bar_tm_full[tb]));
             }
         }
-    } else if (warp <= 6) {
+    } else if (warp < kEpiWarp0) {
         // ---------------- converters ----------------
-        const int n = (warp - 3) * 32 + lane;
+        // warp pair (c, c + 4) owns coefficients 32c .. 32c+31; each takes 16 of a chunk's 32 primes
+        const int cw = warp - kConvWarp0, q = cw & 3, half = cw >> 2;
+        const int n = q * 32 + lane;
         const int g = n >> 3, rr = n & 7;
-        int ir = 0, ia = 0, tt = 0;
-        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tt) {
-            double S = 0.0;
+        int ir = 0, ia = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
+          for (int h = 0; h < jpt; ++h) {
+            // v = round(sum y_j / p_j) in fixed point: y_j * floor(2^53 / p_j) summed exactly
+            // (error < P * 2^30 * 2^-53 << 1/8, the CRT margin)
+            uint64_t acc = 0;
             for (int kc = 0; kc < nkc; ++kc, ++ir, ++ia) {
                 const int s = ir % kRR, sa_ = ia % kRA;
                 mbar_wait(smem_u32(&bar_res_full[s]), (ir / kRR) & 1);
-                mbar_wait(smem_u32(&bar_a_empty[sa_]), ((ia / kRA) & 1) ^ 1);
-                const uint32_t* stg = reinterpret_cast<const uint32_t*>(s_res + s * kResStage);
-                uint8_t* dst = s_a + sa_ * kAStage + (g * 8) * 128 + rr * 16;
-                const int j0 = kc * 32;
-                uint32_t x[32];
+                const uint32_t* stg = reinterpret_cast<const uint32_t*>(s_res + s * kResStage) + half * 16 * kRows;
+                const int j0 = kc * 32 + half * 16;
+                uint32_t y[16];
 #pragma unroll
-                for (int u = 0; u < 32; ++u) x[u] = stg[u * kRows + n];
+                for (int u = 0; u < 16; ++u) y[u] = stg[u * kRows + n];
+                // the residue stage is free as soon as it sits in registers
+                __syncwarp();
+                if (lane == 0) mbar_arrive(smem_u32(&bar_res_empty[s]));
 #pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    uint32_t y[4];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int j = j0 + 4 * c + u;
-                        const uint32_t p = s_p[j];
-                        // padding primes: x is stale but cinv = 0 gives y = 0
-                        y[u] = reduce_2p(mul_shoup_lazy(x[4 * c + u], s_ci[j], s_cs[j], p), p);
-                        S += (double)y[u] * s_ip[j];
-                    }
-                    *reinterpret_cast<uint4*>(dst + c * 128) = make_uint4(y[0], y[1], y[2], y[3]);
+                for (int u = 0; u < 16; ++u) {
+                    // padding primes: x is stale but cinv = 0 gives y = 0
+                    const uint4 pc = s_pc[j0 + u];
+                    y[u] = reduce_2p(mul_shoup_lazy(y[u], pc.y, pc.z, pc.x), pc.x);
+                    acc += (uint64_t)y[u] * pc.w;
                 }
+                if (kc == nkc - 1) {
+                    // slot P of the last chunk carries v (its B row holds -Q): combine the halves
+                    s_acc[half][n] = acc;
+                    asm volatile("bar.sync 1, %0;\n" ::"n"(8 * 32) : "memory");
+                    const uint64_t tot = s_acc[0][n] + s_acc[1][n];
+                    asm volatile("bar.sync 1, %0;\n" ::"n"(8 * 32) : "memory");
+                    const uint32_t v = (uint32_t)((tot + (1ull << 52)) >> 53);
+#pragma unroll
+                    for (int u = 0; u < 16; ++u)
+                        if (j0 + u == P) y[u] = v;
+                }
+                mbar_wait(smem_u32(&bar_a_empty[sa_]), ((ia / kRA) & 1) ^ 1);
+                uint8_t* dst = s_a + sa_ * kAStage + (g * 8 + 4 * half) * 128 + rr * 16;
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    *reinterpret_cast<uint4*>(dst + c * 128) =
+                        make_uint4(y[4 * c], y[4 * c + 1], y[4 * c + 2], y[4 * c + 3]);
                 asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
                 __syncwarp();
-                if (lane == 0) {
-                    mbar_arrive(smem_u32(&bar_res_empty[s]));
-                    mbar_arrive(smem_u32(&bar_a_full[sa_]));
-                }
+                if (lane == 0) mbar_arrive(smem_u32(&bar_a_full[sa_]));
             }
-            const int vb = tt & 1;
-            mbar_wait(smem_u32(&bar_v_empty[vb]), ((tt >> 1) & 1) ^ 1);
-            s_v[vb][n] = (uint32_t)floor(S + 0.5);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(smem_u32(&bar_v_full[vb]));
         }
     } else {
         // ---------------- epilogue ----------------
@@ -560,22 +583,41 @@ __global__ void __launch_bounds__(kPipeWarps * 32, 1) crt_umma_pipe_kernel(
         const uint32_t top_mask = (out_bits & 31) ? ((1u << (out_bits & 31)) - 1u) : 0xffffffffu;
         const int round_col = shift > 0 ? ((shift - 1) >> 5) : -1;
         const uint32_t round_bit = shift > 0 ? (1u << ((shift - 1) & 31)) : 0u;
-        const uint32_t lane_addr = tmem + ((uint32_t)(q * 32) << 16);
-        int tt = 0;
-        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tt) {
+        // two groups take alternate jobs (job parity = TMEM buffer); within a tile the carry
+        // state moves from the group that finished column block h to the one taking h+1
+        const int grp = (warp - kEpiWarp0) >> 2;
+        uint64_t carry = 0;
+        uint32_t prev = 0;
+        bool amb = false;
+        int nwr = 0, nrd = 0;   // handoffs written to slot grp / read from slot 1 - grp
+        int ij = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
+          for (int h = 0; h < jpt; ++h, ++ij) {
+            if ((ij & 1) != grp) continue;
             const int oy = tile / tpo, cb = (tile - oy * tpo) * kRows;
             uint32_t* out = oy == 0 ? outs.out[0] : oy == 1 ? outs.out[1] : oy == 2 ? outs.out[2] : outs.out[3];
             const int i = cb + n;
-            const int vb = tt & 1;
-            mbar_wait(smem_u32(&bar_v_full[vb]), (tt >> 1) & 1);
-            const uint32_t v = s_v[vb][n];
-            __syncwarp();
-            if (lane == 0) mbar_arrive(smem_u32(&bar_v_empty[vb]));
-            mbar_wait(smem_u32(&bar_tm_full), tt & 1);
+            if (h == 0) {
+                carry = 0;
+                prev = 0;
+                amb = false;
+            } else {
+                const int sl = 1 - grp;
+                mbar_wait(smem_u32(&bar_hand_full[sl]), nrd & 1);
+                const uint4 hv = s_hand[sl][n];
+                __syncwarp();
+                if (lane == 0) mbar_arrive(smem_u32(&bar_hand_empty[sl]));
+                ++nrd;
+                carry = ((uint64_t)hv.y << 32) | hv.x;
+                prev = hv.z;
+                amb = hv.w != 0;
+            }
+            const int tb = ij & 1;
+            const int c0 = tb0 + h * kJobCols;
+            const int ncols = job_cols(h);
+            mbar_wait(smem_u32(&bar_tm_full[tb]), (ij >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;\n");
-            uint64_t carry = 0;
-            uint32_t prev = 0;
-            bool amb = false;
+            const uint32_t lane_addr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(tb * 256);
             for (int tl = 0; tl < ncols; tl += 4) {
                 uint32_t e[32];
                 asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
@@ -589,16 +631,16 @@ __global__ void __launch_bounds__(kPipeWarps * 32, 1) crt_umma_pipe_kernel(
                              : "r"(lane_addr + (uint32_t)(tl * 8)));
                 asm volatile("tcgen05.wait::ld.sync.aligned;\n");
 #pragma unroll
-                for (int h = 0; h < 4; ++h) {
-                    const int t = tb0 + tl + h;
+                for (int hh = 0; hh < 4; ++hh) {
+                    const int t = c0 + tl + hh;
                     if (t >= T) break;
-                    const uint32_t* E = e + 8 * h;
+                    const uint32_t* E = e + 8 * hh;
+                    // column value = lo + hi * 2^32 (digit 7 is identically zero)
                     const uint64_t lo = (uint64_t)E[0] + ((uint64_t)E[1] << 8) + ((uint64_t)E[2] << 16) + ((uint64_t)E[3] << 24);
-                    const uint64_t hi = (uint64_t)E[4] + ((uint64_t)E[5] << 8) + ((uint64_t)E[6] << 16) + ((uint64_t)E[7] << 24);
-                    const uint64_t extra = (uint64_t)v * negQ[t] + (t == round_col ? round_bit : 0u);
-                    const uint64_t sum = (lo & 0xffffffffull) + (carry & 0xffffffffull) + (extra & 0xffffffffull);
+                    const uint64_t hi = (uint64_t)E[4] + ((uint64_t)E[5] << 8) + ((uint64_t)E[6] << 16);
+                    const uint64_t sum = (lo & 0xffffffffull) + (carry & 0xffffffffull) + (t == round_col ? round_bit : 0u);
                     const uint32_t word = (uint32_t)sum;
-                    carry = (sum >> 32) + (lo >> 32) + hi + (carry >> 32) + (extra >> 32);
+                    carry = (sum >> 32) + (lo >> 32) + hi + (carry >> 32);
                     if (t < sw) {
                         if (t == tb0 + 1) amb = word >= 0xFFFFFF00u;
                         else if (t > tb0 + 1) amb = amb && (word == 0xffffffffu);
@@ -615,10 +657,17 @@ __global__ void __launch_bounds__(kPipeWarps * 32, 1) crt_umma_pipe_kernel(
             }
             asm volatile("tcgen05.fence::before_thread_sync;\n");
             __syncwarp();
-            if (lane == 0) mbar_arrive(smem_u32(&bar_tm_empty));
-            if (tb0 > 0 && amb)
-                pipe_rescan_exact(res + (size_t)oy * P * N, P, N, W, pinfo, cinv, cinv_sh, Mtab, negQ, v,
-                                  shift, out_bits, out, i);
+            if (lane == 0) mbar_arrive(smem_u32(&bar_tm_empty[tb]));
+            if (h < jpt - 1) {
+                mbar_wait(smem_u32(&bar_hand_empty[grp]), (nwr & 1) ^ 1);
+                s_hand[grp][n] = make_uint4((uint32_t)carry, (uint32_t)(carry >> 32), prev, amb ? 1u : 0u);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(smem_u32(&bar_hand_full[grp]));
+                ++nwr;
+            }
+            if (h == jpt - 1 && tb0 > 0 && amb)
+                pipe_rescan_exact(res + (size_t)oy * P * N, P, N, W, pinfo, cinv, cinv_sh, invp, Mtab,
+                                  negQ, shift, out_bits, out, i);
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n");
@@ -633,8 +682,8 @@ bool hg_crt_umma_pipe_ok(const CrtTable* tab, int N, int shift, int out_bits, in
     const int sw = shift >> 5, sbit = shift & 31;
     const int T = sw + (out_bits + 31) / 32 + (sbit ? 1 : 0);
     const int ncols = ((T - tb0) + 1) & ~1;
-    return N % kRows == 0 && ncols >= 2 && ncols <= kPipeMaxCols &&
-           tb0 + 8 * ((ncols + 7) >> 3) <= tab->W && (tb0 & 7) == 0;
+    return tab->d_Bpipe && N % kRows == 0 && ncols >= 2 && (tb0 & 7) == 0 &&
+           tb0 + 8 * ((ncols + 7) >> 3) <= tab->W && tab->P32p + 32 <= HG_MAX_PRIMES + 32;
 }
 
 int hg_crt_umma_pipe_launch(hg_ctx* ctx, const CrtTable* tab, const uint32_t* res, int nouts, int P,
@@ -650,8 +699,10 @@ int hg_crt_umma_pipe_launch(hg_ctx* ctx, const CrtTable* tab, const uint32_t* re
     for (int k = 0; k < nouts; ++k) o.out[k] = outs_in[k];
     const int ntiles = nouts * (ctx->N / kRows);
     const int grid = ntiles < nsm ? ntiles : nsm;
+    CUtensorMap res_map;
+    if (int rc = hg_tmap_2d_u32(&res_map, res, (uint64_t)ctx->N, (uint64_t)nouts * P, kRows, 32)) return rc;
     crt_umma_pipe_kernel<<<grid, kPipeWarps * 32, kPipeSmem, st>>>(
-        res, P, tab->P32, ctx->N, nouts, ctx->d_pinfo, tab->d_Bconv, tab->d_M, tab->W, tab->d_negQ,
+        res_map, res, P, tab->P32p, ctx->N, nouts, ctx->d_pinfo, tab->d_Bpipe, tab->d_M, tab->W, tab->d_negQ,
         tab->d_cinv, tab->d_cinv_sh, tab->d_invp, shift, out_bits, tb0, o);
     HG_LAUNCH_CHECK(ctx);
     return HG_OK;

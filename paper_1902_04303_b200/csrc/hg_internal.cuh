@@ -9,6 +9,7 @@
 // divide_round of ckks._keyswitch / rescale fused into the reconstruction.
 #pragma once
 
+#include <cuda.h>   // CUtensorMap (encoded through the runtime's driver entry point)
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <algorithm>
@@ -49,6 +50,8 @@ struct CrtTable {
     int P32 = 0;                  // P rounded up to 32 (mma K dimension)
     uint2* d_Bfrag = nullptr;     // byte-split M in mma B-fragment order (hg_crt_mma.cu)
     uint8_t* d_Bconv = nullptr;   // digit-layout B as a UMMA smem image (hg_crt_umma.cu)
+    int P32p = 0;                 // (P + 1) rounded up to 32: K of the pipelined kernel
+    uint8_t* d_Bpipe = nullptr;   // as d_Bconv with row P = -Q mod 2^(32W)
 };
 
 struct hg_ctx {
@@ -129,6 +132,9 @@ int hg_fail(int code, const std::string& msg);
 static inline int words_for_bits(int bits) { return (bits + 31) >> 5; }
 
 // ---- host-side helpers (hg_context.cu) ----------------------------------------------
+// 2-D uint32 tensor map (row pitch = inner * 4 bytes) for cp.async.bulk.tensor boxes
+int hg_tmap_2d_u32(CUtensorMap* tm, const void* base, uint64_t inner, uint64_t outer,
+                   uint32_t box_inner, uint32_t box_outer);
 int hg_ensure_twiddles(hg_ctx* ctx, int P);
 int hg_get_crt(hg_ctx* ctx, int P, const CrtTable** out);
 int hg_primes_for_bits(const hg_ctx* ctx, double bits);   // -1 if too wide

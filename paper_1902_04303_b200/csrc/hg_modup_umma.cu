@@ -14,7 +14,7 @@
 //   warp 1      MMA issuer: W8/8 k-steps of 128x256x32 per chunk into one of 2 TMEM stages
 //   warps 2-5   A loaders: gather the words of 128 coefficients (automorphism permutation),
 //               write the K-major core layout, record sign / negation flags
-//   warps 6-13  epilogue: two warps per TMEM lane quarter split a chunk's 64 primes
+//   warps 6-21  epilogue: four warps per TMEM lane quarter split a chunk's 64 primes
 // TMEM is double-buffered per prime chunk, so the epilogue of chunk c overlaps the MMAs of c+1
 // and the A / B rings keep the loads of the next tile in flight.
 #include "hg_internal.cuh"
@@ -26,8 +26,10 @@ constexpr int kPrimesChunk = 64;  // primes per accumulation (N = 256)
 constexpr int kWMax = 64;         // widest operand handled here (words)
 constexpr int kBChunkBytes = 256 * 4 * kWMax;   // 64 KB: 256 rows x 256 K bytes
 constexpr int kAStage = kRows * 4 * kWMax;      // 32 KB
-constexpr int kWarps = 14;
+constexpr int kEpiGroups = 4;    // epilogue warps per TMEM lane quarter
 constexpr int kEpiWarp0 = 6;
+constexpr int kWarps = kEpiWarp0 + 4 * kEpiGroups;
+constexpr int kEpiPrimes = kPrimesChunk / kEpiGroups;   // primes per epilogue warp and chunk
 constexpr size_t kSmem = 2 * (size_t)kBChunkBytes + 2 * (size_t)kAStage;   // 192 KB
 
 struct MOps {
@@ -102,9 +104,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1) modup_umma_kernel(
             init(&bar_a_full[s], 4);
             init(&bar_a_empty[s], 1);
             init(&bar_tm_full[s], 1);
-            init(&bar_tm_empty[s], 8);
+            init(&bar_tm_empty[s], 4 * kEpiGroups);
             init(&bar_fl_full[s], 4);
-            init(&bar_fl_empty[s], 8);
+            init(&bar_fl_empty[s], 4 * kEpiGroups);
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n");
     }
@@ -224,7 +226,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) modup_umma_kernel(
         }
     } else {
         // ---------------- epilogue ----------------
-        const int q = warp & 3, h = (warp - kEpiWarp0) >> 2;
+        const int q = warp & 3, h = (warp - kEpiWarp0) >> 2;   // lane quarter, prime group
         const int n = q * 32 + lane;
         int ia = 0, ic = 0;
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++ia) {
@@ -241,11 +243,11 @@ __global__ void __launch_bounds__(kWarps * 32, 1) modup_umma_kernel(
                 const int ts = ic & 1;
                 mbar_wait(smem_u32(&bar_tm_full[ts]), (ic >> 1) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;\n");
-                const int jbase = ch * kPrimesChunk + h * (kPrimesChunk / 2);
+                const int jbase = ch * kPrimesChunk + h * kEpiPrimes;
                 const uint32_t lane_addr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ts * 256) +
-                                           (uint32_t)(h * (kPrimesChunk / 2) * 4);
+                                           (uint32_t)(h * kEpiPrimes * 4);
 #pragma unroll 1
-                for (int jj = 0; jj < kPrimesChunk / 2 && jbase + jj < P; jj += 8) {
+                for (int jj = 0; jj < kEpiPrimes && jbase + jj < P; jj += 8) {
                     uint32_t d[32];
                     asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
                                  "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
