@@ -198,6 +198,7 @@ int64_t inv_mod_pow2(int64_t k, int64_t n2) {
 int hg_ew_add(hg_ctx* ctx, uint32_t* out, const uint32_t* a, const uint32_t* b, int bits,
               bool subtract, cudaStream_t st) {
     int W = words_for_bits(bits);
+    HgTimed tm(ctx, st, HG_K_ELEMENTWISE, (double)ctx->N);
     if (subtract)
         add_kernel<true><<<grid_for(ctx->N), kThreads, 0, st>>>(out, a, b, W, bits, ctx->N);
     else
@@ -208,6 +209,7 @@ int hg_ew_add(hg_ctx* ctx, uint32_t* out, const uint32_t* a, const uint32_t* b, 
 
 int hg_ew_divide_round(hg_ctx* ctx, uint32_t* out, int out_bits, const uint32_t* a, int in_bits,
                        int shift, cudaStream_t st) {
+    HgTimed tm(ctx, st, HG_K_ELEMENTWISE, (double)ctx->N);
     divide_round_kernel<<<grid_for(ctx->N), kThreads, 0, st>>>(out, out_bits, a, in_bits, shift,
                                                                ctx->N);
     HG_LAUNCH_CHECK(ctx);
@@ -219,6 +221,7 @@ int hg_ew_automorphism(hg_ctx* ctx, uint32_t* out, const uint32_t* a, int bits, 
     int64_t n2 = 2ll * ctx->N;
     int64_t kk = ((k % n2) + n2) % n2;
     if ((kk & 1) == 0) return hg_fail(HG_EINVAL, "automorphism exponent must be odd");
+    HgTimed tm(ctx, st, HG_K_ELEMENTWISE, (double)ctx->N);
     automorphism_kernel<<<grid_for(ctx->N), kThreads, 0, st>>>(out, a, words_for_bits(bits), bits,
                                                                ctx->N, inv_mod_pow2(kk, n2));
     HG_LAUNCH_CHECK(ctx);
@@ -246,6 +249,7 @@ extern "C" int hg_poly_sub(hg_ctx* ctx, uint32_t* out, const uint32_t* a, const 
 extern "C" int hg_poly_neg(hg_ctx* ctx, uint32_t* out, const uint32_t* a, int bits,
                            void* stream) {
     HG_CHECK_ARGS(ctx && out && a && bits >= 1, "hg_poly_neg: bad arguments");
+    HgTimed tm(ctx, (cudaStream_t)stream, HG_K_ELEMENTWISE, (double)ctx->N);
     neg_kernel<<<grid_for(ctx->N), kThreads, 0, (cudaStream_t)stream>>>(out, a, words_for_bits(bits),
                                                                         bits, ctx->N);
     HG_LAUNCH_CHECK(ctx);
@@ -262,6 +266,7 @@ extern "C" int hg_poly_scalar_mul(hg_ctx* ctx, uint32_t* out, const uint32_t* a,
     for (int j = 0; j < kw; ++j) ks.k[j] = k_words_host[j];
     // an out-of-place product: `out` must not alias `a` (columns read lower words)
     HG_CHECK_ARGS(out != a || kw == 1, "hg_poly_scalar_mul: in-place needs a one-word scalar");
+    HgTimed tm(ctx, (cudaStream_t)stream, HG_K_ELEMENTWISE, (double)ctx->N);
     scalar_mul_kernel<<<grid_for(ctx->N), kThreads, 0, (cudaStream_t)stream>>>(out, a, W, bits,
                                                                                ctx->N, ks, kw);
     HG_LAUNCH_CHECK(ctx);
@@ -272,6 +277,7 @@ extern "C" int hg_poly_reduce_to(hg_ctx* ctx, uint32_t* out, int out_bits, const
                                  int in_bits, void* stream) {
     HG_CHECK_ARGS(ctx && out && a && out_bits >= 1 && out_bits <= in_bits,
                   "hg_poly_reduce_to: bad arguments");
+    HgTimed tm(ctx, (cudaStream_t)stream, HG_K_ELEMENTWISE, (double)ctx->N);
     resize_kernel<false><<<grid_for(ctx->N), kThreads, 0, (cudaStream_t)stream>>>(out, out_bits, a,
                                                                                   in_bits, ctx->N);
     HG_LAUNCH_CHECK(ctx);
@@ -282,6 +288,7 @@ extern "C" int hg_poly_lift_centered(hg_ctx* ctx, uint32_t* out, int out_bits, c
                                      int in_bits, void* stream) {
     HG_CHECK_ARGS(ctx && out && a && in_bits >= 1 && out_bits >= in_bits,
                   "hg_poly_lift_centered: bad arguments");
+    HgTimed tm(ctx, (cudaStream_t)stream, HG_K_ELEMENTWISE, (double)ctx->N);
     resize_kernel<true><<<grid_for(ctx->N), kThreads, 0, (cudaStream_t)stream>>>(out, out_bits, a,
                                                                                  in_bits, ctx->N);
     HG_LAUNCH_CHECK(ctx);

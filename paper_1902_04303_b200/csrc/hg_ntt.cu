@@ -125,13 +125,27 @@ __device__ __forceinline__ void round8(uint32_t (&x)[8], int G, int base,
     for (int kk = 0; kk < R; ++kk) {
         const int k = FWD ? kk : R - 1 - kk;
         const int d = 1 << (R - 1 - k);
+        // the 8 >> (R-k) twiddles of this stage are contiguous and aligned to their count:
+        // 16-byte loads
         const uint2* tg = twp + (G << (LS0 + k)) + (base >> (B + R - k));
+        constexpr int kMaxTw = 4;
+        uint2 w[kMaxTw];
+        const int nt = 8 >> (R - k);
+        if (nt == 1) {
+            w[0] = __ldg(tg);
+        } else {
+#pragma unroll
+            for (int v = 0; v < nt / 2; ++v) {
+                const uint4 q = __ldg(reinterpret_cast<const uint4*>(tg) + v);
+                w[2 * v] = make_uint2(q.x, q.y);
+                w[2 * v + 1] = make_uint2(q.z, q.w);
+            }
+        }
 #pragma unroll
         for (int m = 0; m < 8; ++m) {
             if (m & d) continue;
-            const uint2 w = __ldg(tg + (m >> (R - k)));
-            if (FWD) fwd_bfly(x[m], x[m + d], w, p);
-            else inv_bfly(x[m], x[m + d], w, p);
+            if (FWD) fwd_bfly(x[m], x[m + d], w[m >> (R - k)], p);
+            else inv_bfly(x[m], x[m + d], w[m >> (R - k)], p);
         }
     }
 }
@@ -149,22 +163,45 @@ __device__ __forceinline__ void lo_round(uint32_t (&x)[8], uint32_t* __restrict_
     constexpr int R = (K2 - LS0) < 3 ? (K2 - LS0) : 3;
     constexpr int B = K2 - LS0 - R;
     const int base = ((t >> B) << (B + 3)) | (t & ((1 << B) - 1));
+    // B == 0: the thread's 8 words are contiguous (and the swizzle keeps 4-word groups)
     if (ROUND == 0) {
+        if (B == 0) {
+            const uint4 a = *reinterpret_cast<const uint4*>(rowp + base);
+            const uint4 b = *reinterpret_cast<const uint4*>(rowp + base + 4);
+            x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+        } else {
 #pragma unroll
-        for (int m = 0; m < 8; ++m) x[m] = rowp[base + (m << B)];
+            for (int m = 0; m < 8; ++m) x[m] = rowp[base + (m << B)];
+        }
     } else {
         const uint32_t* s = sm[(ROUND - 1) & 1];
+        if (B == 0) {
+            const uint4 a = *reinterpret_cast<const uint4*>(s + swz(base));
+            const uint4 b = *reinterpret_cast<const uint4*>(s + swz(base + 4));
+            x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+        } else {
 #pragma unroll
-        for (int m = 0; m < 8; ++m) x[m] = s[swz(base + (m << B))];
+            for (int m = 0; m < 8; ++m) x[m] = s[swz(base + (m << B))];
+        }
     }
     round8<FWD, R, B, LS0>(x, G, base, twp, p);
     if (ROUND == NR - 1) {
+        if (B == 0) {
+            *reinterpret_cast<uint4*>(rowp + base) = make_uint4(x[0], x[1], x[2], x[3]);
+            *reinterpret_cast<uint4*>(rowp + base + 4) = make_uint4(x[4], x[5], x[6], x[7]);
+        } else {
 #pragma unroll
-        for (int m = 0; m < 8; ++m) rowp[base + (m << B)] = x[m];
+            for (int m = 0; m < 8; ++m) rowp[base + (m << B)] = x[m];
+        }
     } else {
         uint32_t* s = sm[ROUND & 1];
+        if (B == 0) {
+            *reinterpret_cast<uint4*>(s + swz(base)) = make_uint4(x[0], x[1], x[2], x[3]);
+            *reinterpret_cast<uint4*>(s + swz(base + 4)) = make_uint4(x[4], x[5], x[6], x[7]);
+        } else {
 #pragma unroll
-        for (int m = 0; m < 8; ++m) s[swz(base + (m << B))] = x[m];
+            for (int m = 0; m < 8; ++m) s[swz(base + (m << B))] = x[m];
+        }
         __syncthreads();
     }
 }
@@ -175,7 +212,7 @@ __global__ void __launch_bounds__(256) ntt_lo8_kernel(uint32_t* __restrict__ dat
                                                       int P, int B, int prime_offset,
                                                       const PrimeInfo* __restrict__ pinfo,
                                                       const uint2* __restrict__ tw) {
-    __shared__ uint32_t sm[2][kTile + 64];
+    __shared__ __align__(16) uint32_t sm[2][kTile + 64];
     const int N = 1 << log_n;
     const int k1 = log_n - K2;
     const int jp = blockIdx.y / B, bb = blockIdx.y - jp * B;
