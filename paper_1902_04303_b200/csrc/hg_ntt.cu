@@ -22,7 +22,7 @@ constexpr int kTile = 2048;  // words per shared-memory tile
 
 __device__ __forceinline__ void fwd_bfly(uint32_t& x, uint32_t& y, uint2 w, uint32_t p) {
     const uint32_t p2 = p << 1;
-    const uint32_t a = x >= p2 ? x - p2 : x;
+    const uint32_t a = min(x, x - p2);   // [0, 4p) -> [0, 2p)
     const uint32_t t = mul_shoup_lazy(y, w.x, w.y, p);
     x = a + t;
     y = a - t + p2;
@@ -30,7 +30,7 @@ __device__ __forceinline__ void fwd_bfly(uint32_t& x, uint32_t& y, uint2 w, uint
 __device__ __forceinline__ void inv_bfly(uint32_t& x, uint32_t& y, uint2 w, uint32_t p) {
     const uint32_t p2 = p << 1;
     uint32_t s = x + y;
-    s = s >= p2 ? s - p2 : s;
+    s = min(s, s - p2);
     const uint32_t d = x - y + p2;
     x = s;
     y = mul_shoup_lazy(d, w.x, w.y, p);
@@ -117,9 +117,11 @@ __global__ void __launch_bounds__(256) ntt_hi_kernel(uint32_t* __restrict__ data
 // local position base + m*2^B (base has zero bits [B, B+3)); the stage distances are
 // 2^(B+R-1) ... 2^B.  For local stage LS0 + k the butterfly group of the pair starting at
 // element m is G*2^(LS0+k) + (base >> (B+R-k)) + (m >> (R-k)), twiddle psi_rev[group]
-// (G = 2^k1 + chunk index for the contiguous pass, 1 for the strided pass).
-template <bool FWD, int R, int B, int LS0>
-__device__ __forceinline__ void round8(uint32_t (&x)[8], int G, int base,
+// (G = 2^k1 + chunk index for the contiguous pass, 1 for the strided pass).  A block carries
+// RB rows of the same prime (batch rows of one [B][P][N] launch): the twiddles of a stage are
+// loaded once and applied to every row, and the rows' butterflies interleave.
+template <bool FWD, int R, int B, int LS0, int RB>
+__device__ __forceinline__ void round8(uint32_t (&x)[RB][8], int G, int base,
                                        const uint2* __restrict__ twp, uint32_t p) {
 #pragma unroll
     for (int kk = 0; kk < R; ++kk) {
@@ -128,8 +130,7 @@ __device__ __forceinline__ void round8(uint32_t (&x)[8], int G, int base,
         // the 8 >> (R-k) twiddles of this stage are contiguous and aligned to their count:
         // 16-byte loads
         const uint2* tg = twp + (G << (LS0 + k)) + (base >> (B + R - k));
-        constexpr int kMaxTw = 4;
-        uint2 w[kMaxTw];
+        uint2 w[4];
         const int nt = 8 >> (R - k);
         if (nt == 1) {
             w[0] = __ldg(tg);
@@ -144,8 +145,11 @@ __device__ __forceinline__ void round8(uint32_t (&x)[8], int G, int base,
 #pragma unroll
         for (int m = 0; m < 8; ++m) {
             if (m & d) continue;
-            if (FWD) fwd_bfly(x[m], x[m + d], w[m >> (R - k)], p);
-            else inv_bfly(x[m], x[m + d], w[m >> (R - k)], p);
+#pragma unroll
+            for (int r = 0; r < RB; ++r) {
+                if (FWD) fwd_bfly(x[r][m], x[r][m + d], w[m >> (R - k)], p);
+                else inv_bfly(x[r][m], x[r][m + d], w[m >> (R - k)], p);
+            }
         }
     }
 }
@@ -153,9 +157,54 @@ __device__ __forceinline__ void round8(uint32_t (&x)[8], int G, int base,
 // bank-conflict swizzle (a bijection on [0, 2048)): bits 2-4 ^= bits 5-7
 __device__ __forceinline__ int swz(int i) { return i ^ (((i >> 5) & 7) << 2); }
 
-template <bool FWD, int K2, int ROUND>
-__device__ __forceinline__ void lo_round(uint32_t (&x)[8], uint32_t* __restrict__ rowp,
-                                         uint32_t (*sm)[kTile + 64], int G, int t,
+template <int B>
+__device__ __forceinline__ void load8(uint32_t (&x)[8], const uint32_t* src, int base) {
+    if (B == 0) {   // contiguous (the smem swizzle keeps 4-word groups): 16-byte accesses
+        const uint4 a = *reinterpret_cast<const uint4*>(src + base);
+        const uint4 b = *reinterpret_cast<const uint4*>(src + base + 4);
+        x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+    } else {
+#pragma unroll
+        for (int m = 0; m < 8; ++m) x[m] = src[base + (m << B)];
+    }
+}
+template <int B>
+__device__ __forceinline__ void store8(const uint32_t (&x)[8], uint32_t* dst, int base) {
+    if (B == 0) {
+        *reinterpret_cast<uint4*>(dst + base) = make_uint4(x[0], x[1], x[2], x[3]);
+        *reinterpret_cast<uint4*>(dst + base + 4) = make_uint4(x[4], x[5], x[6], x[7]);
+    } else {
+#pragma unroll
+        for (int m = 0; m < 8; ++m) dst[base + (m << B)] = x[m];
+    }
+}
+template <int B>
+__device__ __forceinline__ void sload8(uint32_t (&x)[8], const uint32_t* s, int base) {
+    if (B == 0) {
+        const uint4 a = *reinterpret_cast<const uint4*>(s + swz(base));
+        const uint4 b = *reinterpret_cast<const uint4*>(s + swz(base + 4));
+        x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+    } else {
+#pragma unroll
+        for (int m = 0; m < 8; ++m) x[m] = s[swz(base + (m << B))];
+    }
+}
+template <int B>
+__device__ __forceinline__ void sstore8(const uint32_t (&x)[8], uint32_t* s, int base) {
+    if (B == 0) {
+        *reinterpret_cast<uint4*>(s + swz(base)) = make_uint4(x[0], x[1], x[2], x[3]);
+        *reinterpret_cast<uint4*>(s + swz(base + 4)) = make_uint4(x[4], x[5], x[6], x[7]);
+    } else {
+#pragma unroll
+        for (int m = 0; m < 8; ++m) s[swz(base + (m << B))] = x[m];
+    }
+}
+
+constexpr int kSmRow = kTile;   // the swizzle stays inside the row: no padding
+
+template <bool FWD, int K2, int ROUND, int RB>
+__device__ __forceinline__ void lo_round(uint32_t (&x)[RB][8], uint32_t* __restrict__ rowp,
+                                         size_t rstride, uint32_t* __restrict__ sm, int G, int t,
                                          const uint2* __restrict__ twp, uint32_t p) {
     constexpr int NR = (K2 + 2) / 3;
     constexpr int R_IDX = FWD ? ROUND : NR - 1 - ROUND;   // which stage triple
@@ -163,97 +212,78 @@ __device__ __forceinline__ void lo_round(uint32_t (&x)[8], uint32_t* __restrict_
     constexpr int R = (K2 - LS0) < 3 ? (K2 - LS0) : 3;
     constexpr int B = K2 - LS0 - R;
     const int base = ((t >> B) << (B + 3)) | (t & ((1 << B) - 1));
-    // B == 0: the thread's 8 words are contiguous (and the swizzle keeps 4-word groups)
-    if (ROUND == 0) {
-        if (B == 0) {
-            const uint4 a = *reinterpret_cast<const uint4*>(rowp + base);
-            const uint4 b = *reinterpret_cast<const uint4*>(rowp + base + 4);
-            x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
-        } else {
 #pragma unroll
-            for (int m = 0; m < 8; ++m) x[m] = rowp[base + (m << B)];
-        }
-    } else {
-        const uint32_t* s = sm[(ROUND - 1) & 1];
-        if (B == 0) {
-            const uint4 a = *reinterpret_cast<const uint4*>(s + swz(base));
-            const uint4 b = *reinterpret_cast<const uint4*>(s + swz(base + 4));
-            x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
-        } else {
-#pragma unroll
-            for (int m = 0; m < 8; ++m) x[m] = s[swz(base + (m << B))];
-        }
+    for (int r = 0; r < RB; ++r) {
+        if (ROUND == 0) load8<B>(x[r], rowp + r * rstride, base);
+        else sload8<B>(x[r], sm + (((ROUND - 1) & 1) * RB + r) * kSmRow, base);
     }
-    round8<FWD, R, B, LS0>(x, G, base, twp, p);
+    round8<FWD, R, B, LS0, RB>(x, G, base, twp, p);
     if (ROUND == NR - 1) {
-        if (B == 0) {
-            *reinterpret_cast<uint4*>(rowp + base) = make_uint4(x[0], x[1], x[2], x[3]);
-            *reinterpret_cast<uint4*>(rowp + base + 4) = make_uint4(x[4], x[5], x[6], x[7]);
-        } else {
 #pragma unroll
-            for (int m = 0; m < 8; ++m) rowp[base + (m << B)] = x[m];
-        }
+        for (int r = 0; r < RB; ++r) store8<B>(x[r], rowp + r * rstride, base);
     } else {
-        uint32_t* s = sm[ROUND & 1];
-        if (B == 0) {
-            *reinterpret_cast<uint4*>(s + swz(base)) = make_uint4(x[0], x[1], x[2], x[3]);
-            *reinterpret_cast<uint4*>(s + swz(base + 4)) = make_uint4(x[4], x[5], x[6], x[7]);
-        } else {
 #pragma unroll
-            for (int m = 0; m < 8; ++m) s[swz(base + (m << B))] = x[m];
-        }
+        for (int r = 0; r < RB; ++r) sstore8<B>(x[r], sm + ((ROUND & 1) * RB + r) * kSmRow, base);
         __syncthreads();
     }
 }
 
 // Contiguous stages: chunk of 2^K2 words, K2/3 rounds; block = 2^K2 / 8 threads.
-template <bool FWD, int K2>
+// grid = (N >> K2 chunks, batch-row groups of RB, primes): prime-major scheduling keeps the
+// prime's twiddles in L2 while its batch rows pass.
+template <bool FWD, int K2, int RB>
 __global__ void __launch_bounds__(256) ntt_lo8_kernel(uint32_t* __restrict__ data, int log_n,
-                                                      int P, int B, int prime_offset,
+                                                      int P, int bb0, int prime_offset,
                                                       const PrimeInfo* __restrict__ pinfo,
                                                       const uint2* __restrict__ tw) {
-    __shared__ __align__(16) uint32_t sm[2][kTile + 64];
+    __shared__ __align__(16) uint32_t sm[2 * RB * kSmRow];
     const int N = 1 << log_n;
     const int k1 = log_n - K2;
-    const int jp = blockIdx.y / B, bb = blockIdx.y - jp * B;
+    const int jp = blockIdx.z, bb = bb0 + blockIdx.y * RB;
     const int prime = prime_offset + jp;
     const uint32_t p = pinfo[prime].p;
     const uint2* twp = tw + (size_t)prime * N;
+    const size_t rstride = (size_t)P * N;
     uint32_t* rowp = data + ((size_t)bb * P + jp) * N + ((size_t)blockIdx.x << K2);
     const int G = (1 << k1) + blockIdx.x;
     const int t = threadIdx.x;
-    uint32_t x[8];
+    uint32_t x[RB][8];
     constexpr int NR = (K2 + 2) / 3;
-    lo_round<FWD, K2, 0>(x, rowp, sm, G, t, twp, p);
-    if (NR > 1) lo_round<FWD, K2, (NR > 1 ? 1 : 0)>(x, rowp, sm, G, t, twp, p);
-    if (NR > 2) lo_round<FWD, K2, (NR > 2 ? 2 : 0)>(x, rowp, sm, G, t, twp, p);
-    if (NR > 3) lo_round<FWD, K2, (NR > 3 ? 3 : 0)>(x, rowp, sm, G, t, twp, p);
+    lo_round<FWD, K2, 0, RB>(x, rowp, rstride, sm, G, t, twp, p);
+    if (NR > 1) lo_round<FWD, K2, (NR > 1 ? 1 : 0), RB>(x, rowp, rstride, sm, G, t, twp, p);
+    if (NR > 2) lo_round<FWD, K2, (NR > 2 ? 2 : 0), RB>(x, rowp, rstride, sm, G, t, twp, p);
+    if (NR > 3) lo_round<FWD, K2, (NR > 3 ? 3 : 0), RB>(x, rowp, rstride, sm, G, t, twp, p);
 }
 
 // Strided stages [0, K1), K1 in {3, 6}: tile of 2^K1 rows (stride 2^k2) x (2048 >> K1)
 // columns; thread = (column c, row group g) holding 8 rows.  K1 = 3 needs no shared memory.
-template <bool FWD, int K1>
+template <bool FWD, int K1, int RB>
 __global__ void __launch_bounds__(256) ntt_hi8_kernel(uint32_t* __restrict__ data, int log_n,
-                                                      int P, int B, int prime_offset,
+                                                      int P, int bb0, int prime_offset,
                                                       const PrimeInfo* __restrict__ pinfo,
                                                       const uint2* __restrict__ tw) {
-    __shared__ uint32_t sm[K1 > 3 ? kTile : 1];
+    __shared__ uint32_t sm[K1 > 3 ? RB * kTile : 1];
     constexpr int TC = kTile >> K1;
     const int N = 1 << log_n;
     const int k2 = log_n - K1;
-    const int jp = blockIdx.y / B, bb = blockIdx.y - jp * B;
+    const int jp = blockIdx.z, bb = bb0 + blockIdx.y * RB;
     const int prime = prime_offset + jp;
     const uint32_t p = pinfo[prime].p;
     const uint2* twp = tw + (size_t)prime * N;
+    const size_t rstride = (size_t)P * N;
     const int c = threadIdx.x % TC, g = threadIdx.x / TC;
     uint32_t* colp = data + ((size_t)bb * P + jp) * N + blockIdx.x * TC + c;
-    uint32_t x[8];
+    uint32_t x[RB][8];
     if (K1 == 3) {
 #pragma unroll
-        for (int m = 0; m < 8; ++m) x[m] = colp[(size_t)m << k2];
-        round8<FWD, 3, 0, 0>(x, 1, 0, twp, p);
+        for (int r = 0; r < RB; ++r)
 #pragma unroll
-        for (int m = 0; m < 8; ++m) colp[(size_t)m << k2] = x[m];
+            for (int m = 0; m < 8; ++m) x[r][m] = colp[r * rstride + ((size_t)m << k2)];
+        round8<FWD, 3, 0, 0, RB>(x, 1, 0, twp, p);
+#pragma unroll
+        for (int r = 0; r < RB; ++r)
+#pragma unroll
+            for (int m = 0; m < 8; ++m) colp[r * rstride + ((size_t)m << k2)] = x[r][m];
     } else {
         // forward: stages 0-2 on rows g + 8m, then 3-5 on rows 8g + m; inverse reversed
         constexpr int BA = FWD ? 3 : 0;   // first round's row stride exponent
@@ -261,32 +291,78 @@ __global__ void __launch_bounds__(256) ntt_hi8_kernel(uint32_t* __restrict__ dat
         const int ra = BA ? g : 8 * g;
         const int rb = BB ? g : 8 * g;
 #pragma unroll
-        for (int m = 0; m < 8; ++m) x[m] = colp[(size_t)(ra + (m << BA)) << k2];
-        round8<FWD, 3, BA, (FWD ? 0 : 3)>(x, 1, ra, twp, p);
+        for (int r = 0; r < RB; ++r)
 #pragma unroll
-        for (int m = 0; m < 8; ++m) sm[(ra + (m << BA)) * TC + c] = x[m];
+            for (int m = 0; m < 8; ++m) x[r][m] = colp[r * rstride + ((size_t)(ra + (m << BA)) << k2)];
+        round8<FWD, 3, BA, (FWD ? 0 : 3), RB>(x, 1, ra, twp, p);
+#pragma unroll
+        for (int r = 0; r < RB; ++r)
+#pragma unroll
+            for (int m = 0; m < 8; ++m) sm[r * kTile + (ra + (m << BA)) * TC + c] = x[r][m];
         __syncthreads();
 #pragma unroll
-        for (int m = 0; m < 8; ++m) x[m] = sm[(rb + (m << BB)) * TC + c];
-        round8<FWD, 3, BB, (FWD ? 3 : 0)>(x, 1, rb, twp, p);
+        for (int r = 0; r < RB; ++r)
 #pragma unroll
-        for (int m = 0; m < 8; ++m) colp[(size_t)(rb + (m << BB)) << k2] = x[m];
+            for (int m = 0; m < 8; ++m) x[r][m] = sm[r * kTile + (rb + (m << BB)) * TC + c];
+        round8<FWD, 3, BB, (FWD ? 3 : 0), RB>(x, 1, rb, twp, p);
+#pragma unroll
+        for (int r = 0; r < RB; ++r)
+#pragma unroll
+            for (int m = 0; m < 8; ++m) colp[r * rstride + ((size_t)(rb + (m << BB)) << k2)] = x[r][m];
     }
 }
 
-template <bool FWD>
-int launch_lo8(int k2, dim3 grid, cudaStream_t st, uint32_t* data, int log_n, int P, int B,
+template <bool FWD, int RB>
+int launch_lo8(int k2, dim3 grid, cudaStream_t st, uint32_t* data, int log_n, int P, int bb0,
                int off, const PrimeInfo* pinfo, const uint2* tw) {
     const int threads = (1 << k2) / 8;
     switch (k2) {
-#define HG_LO(K)                                                                              \
-    case K:                                                                                   \
-        ntt_lo8_kernel<FWD, K><<<grid, threads, 0, st>>>(data, log_n, P, B, off, pinfo, tw); \
+#define HG_LO(K)                                                                                     \
+    case K:                                                                                          \
+        ntt_lo8_kernel<FWD, K, RB><<<grid, threads, 0, st>>>(data, log_n, P, bb0, off, pinfo, tw); \
         return 0;
         HG_LO(3) HG_LO(4) HG_LO(5) HG_LO(6) HG_LO(7) HG_LO(8) HG_LO(9) HG_LO(10) HG_LO(11)
 #undef HG_LO
     }
     return -1;
+}
+
+template <bool FWD, int RB>
+int launch_hi8(int k1, dim3 grid, cudaStream_t st, uint32_t* data, int log_n, int P, int bb0,
+               int off, const PrimeInfo* pinfo, const uint2* tw) {
+    if (k1 == 3) ntt_hi8_kernel<FWD, 3, RB><<<grid, 256, 0, st>>>(data, log_n, P, bb0, off, pinfo, tw);
+    else if (k1 == 6) ntt_hi8_kernel<FWD, 6, RB><<<grid, 256, 0, st>>>(data, log_n, P, bb0, off, pinfo, tw);
+    return 0;
+}
+
+// one pass over all rows: groups of 2 batch rows per block (3 for an odd count), 1 if B == 1
+template <bool FWD>
+int ntt_pass(hg_ctx* ctx, bool hi, int k1, int k2, uint32_t* data, int B, int P, int off,
+             const uint2* tw, cudaStream_t st) {
+    const int log_n = ctx->log_n, N = ctx->N;
+    const int gx = hi ? N / kTile : N >> k2;
+    auto run = [&](int rb, int groups, int bb0) {
+        const dim3 g(gx, groups, P);
+        if (rb == 1) {
+            if (hi) launch_hi8<FWD, 1>(k1, g, st, data, log_n, P, bb0, off, ctx->d_pinfo, tw);
+            else launch_lo8<FWD, 1>(k2, g, st, data, log_n, P, bb0, off, ctx->d_pinfo, tw);
+        } else if (rb == 2) {
+            if (hi) launch_hi8<FWD, 2>(k1, g, st, data, log_n, P, bb0, off, ctx->d_pinfo, tw);
+            else launch_lo8<FWD, 2>(k2, g, st, data, log_n, P, bb0, off, ctx->d_pinfo, tw);
+        } else {
+            if (hi) launch_hi8<FWD, 3>(k1, g, st, data, log_n, P, bb0, off, ctx->d_pinfo, tw);
+            else launch_lo8<FWD, 3>(k2, g, st, data, log_n, P, bb0, off, ctx->d_pinfo, tw);
+        }
+        HG_LAUNCH_CHECK(ctx);
+        return HG_OK;
+    };
+    int rc;
+    if (B == 1) return run(1, 1, 0);
+    const int odd = B & 1;                  // an odd count ends with one 3-row group
+    const int pairs = (B - 3 * odd) / 2;
+    if (pairs > 0 && (rc = run(2, pairs, 0))) return rc;
+    if (odd && (rc = run(3, 1, 2 * pairs))) return rc;
+    return HG_OK;
 }
 
 }  // namespace
@@ -300,24 +376,16 @@ int hg_ntt_launch(hg_ctx* ctx, uint32_t* data, int rows, int P, int prime_offset
     const int log_n = ctx->log_n, N = ctx->N;
     const uint2* tw = forward ? ctx->d_tw_fwd : ctx->d_tw_inv;
     HgTimed tm(ctx, stream, HG_K_NTT, (double)rows * (N / 2) * log_n);
-    if (log_n >= 3 && rows % P == 0) {
+    if (log_n >= 3 && rows % P == 0 && P <= 65535) {
         const int k1 = log_n <= 11 ? 0 : (log_n <= 14 ? 3 : 6);
         const int k2 = log_n - k1;
         const int B = rows / P;
-        dim3 glo(N >> k2, rows);
-        dim3 ghi(N / kTile, rows);
         if (forward) {
-            if (k1 == 3) ntt_hi8_kernel<true, 3><<<ghi, 256, 0, stream>>>(data, log_n, P, B, prime_offset, ctx->d_pinfo, tw);
-            if (k1 == 6) ntt_hi8_kernel<true, 6><<<ghi, 256, 0, stream>>>(data, log_n, P, B, prime_offset, ctx->d_pinfo, tw);
-            if (k1) HG_LAUNCH_CHECK(ctx);
-            launch_lo8<true>(k2, glo, stream, data, log_n, P, B, prime_offset, ctx->d_pinfo, tw);
-            HG_LAUNCH_CHECK(ctx);
+            if (k1 && (rc = ntt_pass<true>(ctx, true, k1, k2, data, B, P, prime_offset, tw, stream))) return rc;
+            if ((rc = ntt_pass<true>(ctx, false, k1, k2, data, B, P, prime_offset, tw, stream))) return rc;
         } else {
-            launch_lo8<false>(k2, glo, stream, data, log_n, P, B, prime_offset, ctx->d_pinfo, tw);
-            HG_LAUNCH_CHECK(ctx);
-            if (k1 == 3) ntt_hi8_kernel<false, 3><<<ghi, 256, 0, stream>>>(data, log_n, P, B, prime_offset, ctx->d_pinfo, tw);
-            if (k1 == 6) ntt_hi8_kernel<false, 6><<<ghi, 256, 0, stream>>>(data, log_n, P, B, prime_offset, ctx->d_pinfo, tw);
-            if (k1) HG_LAUNCH_CHECK(ctx);
+            if ((rc = ntt_pass<false>(ctx, false, k1, k2, data, B, P, prime_offset, tw, stream))) return rc;
+            if (k1 && (rc = ntt_pass<false>(ctx, true, k1, k2, data, B, P, prime_offset, tw, stream))) return rc;
         }
         return HG_OK;
     }
