@@ -152,7 +152,9 @@ long long hg_launch_count(const hg_ctx* ctx);
  * 4 = elementwise) on the launching stream.  hg_kernel_stats synchronises the recorded
  * events and returns, for one class, the summed device milliseconds, the number of
  * launches and the algorithmic work (MACs for CRT/ModUp, butterflies for NTT, bytes
- * for pointwise/elementwise).  Enabling resets the counters.                        */
+ * for pointwise/elementwise).  Enabling resets the counters.  `enabled`: 0 = off,
+ * 1 = every class, otherwise (mask << 1) with bit k of mask selecting class k (so a
+ * timed region can bracket only the class whose roofline it reports).                */
 int hg_set_kernel_timing(hg_ctx* ctx, int enabled);
 int hg_kernel_stats(hg_ctx* ctx, int kind, double* ms, long long* launches, double* work);
 

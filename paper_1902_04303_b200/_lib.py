@@ -145,8 +145,15 @@ class Context:
     def launches(self) -> int:
         return int(self.lib.hg_launch_count(self.handle))
 
-    def set_kernel_timing(self, enabled: bool):
-        check(self.lib.hg_set_kernel_timing(self.handle, 1 if enabled else 0))
+    def set_kernel_timing(self, enabled: bool, kinds=None):
+        """Bracket launches with CUDA events: every class, or only `kinds` (names)."""
+        if not enabled:
+            code = 0
+        elif kinds is None:
+            code = 1
+        else:
+            code = sum(1 << KERNEL_KINDS[k] for k in kinds) << 1
+        check(self.lib.hg_set_kernel_timing(self.handle, code))
 
     def kernel_stats(self, kind: str) -> dict:
         """{'ms', 'launches', 'work'} of the events recorded since timing was enabled."""

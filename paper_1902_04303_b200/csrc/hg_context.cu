@@ -163,8 +163,8 @@ extern "C" int hg_ctx_primes(const hg_ctx* ctx, uint32_t* out) {
 extern "C" long long hg_launch_count(const hg_ctx* ctx) { return ctx ? ctx->launches.load() : 0; }
 
 // ---- live kernel timing ----------------------------------------------------------------------
-int hg_timer_begin(hg_ctx* ctx, cudaStream_t st) {
-    if (!ctx->timing) return -1;
+int hg_timer_begin(hg_ctx* ctx, cudaStream_t st, int kind) {
+    if (!(ctx->timing & (1 << kind))) return -1;
     std::lock_guard<std::mutex> lk(ctx->mu);
     hg_ctx::Timer t;
     if (!ctx->spare.empty()) {
@@ -195,7 +195,7 @@ extern "C" int hg_set_kernel_timing(hg_ctx* ctx, int enabled) {
     std::lock_guard<std::mutex> lk(ctx->mu);
     for (auto& t : ctx->timers) ctx->spare.push_back(t);
     ctx->timers.clear();
-    ctx->timing = enabled != 0;
+    ctx->timing = enabled == 1 ? 0x1f : (enabled < 0 ? 0 : enabled >> 1);
     return HG_OK;
 }
 

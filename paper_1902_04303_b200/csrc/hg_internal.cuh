@@ -80,7 +80,7 @@ struct hg_ctx {
         int kind = 0;
         double work = 0.0;
     };
-    bool timing = false;
+    int timing = 0;                // bitmask of timed kernel classes (1 << kind)
     std::vector<Timer> timers;     // recorded this window
     std::vector<Timer> spare;      // event pairs available for reuse
 };
@@ -88,7 +88,7 @@ struct hg_ctx {
 enum { HG_K_CRT = 0, HG_K_MODUP = 1, HG_K_NTT = 2, HG_K_POINTWISE = 3, HG_K_ELEMENTWISE = 4 };
 
 // Bracket a launch with events when timing is enabled (returns -1 otherwise).
-int hg_timer_begin(hg_ctx* ctx, cudaStream_t st);
+int hg_timer_begin(hg_ctx* ctx, cudaStream_t st, int kind);
 void hg_timer_end(hg_ctx* ctx, int idx, cudaStream_t st, int kind, double work);
 struct HgTimed {
     hg_ctx* ctx;
@@ -97,7 +97,7 @@ struct HgTimed {
     double work;
     int idx;
     HgTimed(hg_ctx* c, cudaStream_t s, int k, double w) : ctx(c), st(s), kind(k), work(w) {
-        idx = hg_timer_begin(c, s);
+        idx = hg_timer_begin(c, s, k);
     }
     ~HgTimed() { hg_timer_end(ctx, idx, st, kind, work); }
 };

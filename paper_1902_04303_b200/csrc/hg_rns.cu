@@ -520,7 +520,7 @@ extern "C" int hg_poly_mul(hg_ctx* ctx, uint32_t* out, int out_bits, hg_operand 
     if (rc) return rc;
     rc = hg_ntt_launch(ctx, buf.u32(), 2 * P, P, 0, true, st);
     if (rc) return rc;
-    const int tpw = hg_timer_begin(ctx, st);
+    const int tpw = hg_timer_begin(ctx, st, HG_K_POINTWISE);
     pw_mul_kernel<<<pw_grid(N, P), 256, 0, st>>>(buf.u32(), buf.u32() + (size_t)P * N, P, N,
                                                  ctx->d_pinfo);
     hg_timer_end(ctx, tpw, st, HG_K_POINTWISE, (double)N * P);
@@ -554,7 +554,7 @@ extern "C" int hg_poly_tensor(hg_ctx* ctx, uint32_t* d0, uint32_t* d1, uint32_t*
     if (rc) return rc;
     rc = hg_ntt_launch(ctx, buf.u32(), 4 * P, P, 0, true, st);
     if (rc) return rc;
-    const int tpw = hg_timer_begin(ctx, st);
+    const int tpw = hg_timer_begin(ctx, st, HG_K_POINTWISE);
     pw_tensor_kernel<<<pw_grid(N, P), 256, 0, st>>>(buf.u32(), P, N, ctx->d_pinfo);
     hg_timer_end(ctx, tpw, st, HG_K_POINTWISE, (double)N * P);
     HG_LAUNCH_CHECK(ctx);
@@ -646,7 +646,7 @@ extern "C" int hg_keyswitch(hg_ctx* ctx, const hg_key* key, const uint32_t* x,
     if (rc) return rc;
     rc = hg_ntt_launch(ctx, buf.u32(), P, P, 0, true, st);
     if (rc) return rc;
-    const int tpw = hg_timer_begin(ctx, st);
+    const int tpw = hg_timer_begin(ctx, st, HG_K_POINTWISE);
     pw_key2_kernel<<<pw_grid(N, P), 256, 0, st>>>(buf.u32(), key->d_kb, key->d_ka, P, N,
                                                   ctx->d_pinfo);
     hg_timer_end(ctx, tpw, st, HG_K_POINTWISE, (double)N * P);
@@ -772,7 +772,7 @@ extern "C" int hg_ct_mult_prepared(hg_ctx* ctx, const hg_key* evk, const hg_ctpr
     if (rc) return rc;
     rc = hg_ntt_launch(ctx, res.u32(), 2 * P, P, 0, true, st);
     if (rc) return rc;
-    const int tpw = hg_timer_begin(ctx, st);
+    const int tpw = hg_timer_begin(ctx, st, HG_K_POINTWISE);
     pw_tensor_prep_kernel<<<pw_grid(N, P), 256, 0, st>>>(a->d_res, a->d_res + (size_t)P * N,
                                                          res.u32(), P, N, ctx->d_pinfo);
     hg_timer_end(ctx, tpw, st, HG_K_POINTWISE, (double)N * P);
