@@ -202,7 +202,7 @@ __device__ __forceinline__ void sstore8(const uint32_t (&x)[8], uint32_t* s, int
 
 constexpr int kSmRow = kTile;   // the swizzle stays inside the row: no padding
 
-template <bool FWD, int K2, int ROUND, int RB>
+template <bool FWD, int K2, int ROUND, int RB, bool PRELOADED = false>
 __device__ __forceinline__ void lo_round(uint32_t (&x)[RB][8], uint32_t* __restrict__ rowp,
                                          size_t rstride, uint32_t* __restrict__ sm, int G, int t,
                                          const uint2* __restrict__ twp, uint32_t p) {
@@ -214,8 +214,11 @@ __device__ __forceinline__ void lo_round(uint32_t (&x)[RB][8], uint32_t* __restr
     const int base = ((t >> B) << (B + 3)) | (t & ((1 << B) - 1));
 #pragma unroll
     for (int r = 0; r < RB; ++r) {
-        if (ROUND == 0) load8<B>(x[r], rowp + r * rstride, base);
-        else sload8<B>(x[r], sm + (((ROUND - 1) & 1) * RB + r) * kSmRow, base);
+        if (ROUND == 0) {
+            if (!PRELOADED) load8<B>(x[r], rowp + r * rstride, base);
+        } else {
+            sload8<B>(x[r], sm + (((ROUND - 1) & 1) * RB + r) * kSmRow, base);
+        }
     }
     round8<FWD, R, B, LS0, RB>(x, G, base, twp, p);
     if (ROUND == NR - 1) {
@@ -310,6 +313,86 @@ __global__ void __launch_bounds__(256) ntt_hi8_kernel(uint32_t* __restrict__ dat
 #pragma unroll
             for (int m = 0; m < 8; ++m) colp[r * rstride + ((size_t)(rb + (m << BB)) << k2)] = x[r][m];
     }
+}
+
+// Inverse contiguous pass with the NTT-domain product fused into its first round (which is
+// unit-stride: each thread's 8 words are contiguous).  The products are Montgomery products of
+// lazily reduced inputs, left in [0, 2p) (the inverse butterflies accept < 2p; the CRT reduces).
+//   PRE 1 (key switch):  out rows (x*kb, x*ka)           in0 = x [0,4p), in1 = kb, in2 = ka [0,p)
+//   PRE 2 (tensor):      out rows (a0b0, a0b1+a1b0, a1b1) in0..in3 = a0, a1, b0, b1 [0,4p)
+//   PRE 3 (product):     out row  a*b                    in0, in1 [0,4p)
+// Inputs and outputs are [rows][P][N]; a block reads its chunk of every input row before its
+// last round writes, so the outputs may alias the inputs chunk-for-chunk (in-place use).
+template <int PRE>
+struct PreRows { static constexpr int value = PRE == 1 ? 2 : (PRE == 2 ? 3 : 1); };
+
+template <int K2, int PRE>
+__global__ void __launch_bounds__(256) intt_lo8_fused_kernel(
+    uint32_t* out, const uint32_t* in0, const uint32_t* in1, const uint32_t* in2,
+    const uint32_t* in3, int log_n, int P, const PrimeInfo* __restrict__ pinfo,
+    const uint2* __restrict__ tw) {
+    constexpr int RB = PreRows<PRE>::value;
+    __shared__ __align__(16) uint32_t sm[2 * RB * kSmRow];
+    const int N = 1 << log_n;
+    const int k1 = log_n - K2;
+    const int jp = blockIdx.z;
+    const PrimeInfo pi = pinfo[jp];
+    const uint32_t p = pi.p, p2 = p << 1;
+    const uint2* twp = tw + (size_t)jp * N;
+    const size_t rstride = (size_t)P * N;
+    const size_t roff = (size_t)jp * N + ((size_t)blockIdx.x << K2);
+    const int G = (1 << k1) + blockIdx.x;
+    const int t = threadIdx.x;
+    const int base = t << 3;     // round 0 of the inverse pass has B = 0
+    uint32_t x[RB][8];
+    {
+        uint32_t u0[8], u1[8], u2[8], u3[8];
+        load8<0>(u0, in0 + roff, base);
+        load8<0>(u1, in1 + roff, base);
+        if (PRE != 3) load8<0>(u2, in2 + roff, base);
+        if (PRE == 2) load8<0>(u3, in3 + roff, base);
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+            const uint32_t a = min(u0[m], u0[m] - p2);
+            if (PRE == 1) {
+                x[0][m] = mont_mul(a, u1[m], p, pi.pinv_neg);
+                x[RB - 1][m] = mont_mul(a, u2[m], p, pi.pinv_neg);
+            } else if (PRE == 2) {
+                const uint32_t a1 = min(u1[m], u1[m] - p2);
+                const uint32_t b0 = min(u2[m], u2[m] - p2);
+                const uint32_t b1 = min(u3[m], u3[m] - p2);
+                x[0][m] = mont_mul(a, b0, p, pi.pinv_neg);
+                const uint32_t d1 = mont_mul(a, b1, p, pi.pinv_neg) + mont_mul(a1, b0, p, pi.pinv_neg);
+                x[RB > 1 ? 1 : 0][m] = min(d1, d1 - p2);
+                x[RB - 1][m] = mont_mul(a1, b1, p, pi.pinv_neg);
+            } else {
+                x[0][m] = mont_mul(a, min(u1[m], u1[m] - p2), p, pi.pinv_neg);
+            }
+        }
+    }
+    uint32_t* rowp = out + roff;
+    constexpr int NR = (K2 + 2) / 3;
+    lo_round<false, K2, 0, RB, true>(x, rowp, rstride, sm, G, t, twp, p);
+    if (NR > 1) lo_round<false, K2, (NR > 1 ? 1 : 0), RB>(x, rowp, rstride, sm, G, t, twp, p);
+    if (NR > 2) lo_round<false, K2, (NR > 2 ? 2 : 0), RB>(x, rowp, rstride, sm, G, t, twp, p);
+    if (NR > 3) lo_round<false, K2, (NR > 3 ? 3 : 0), RB>(x, rowp, rstride, sm, G, t, twp, p);
+}
+
+template <int PRE>
+int launch_fused_lo8(int k2, dim3 grid, cudaStream_t st, uint32_t* out, const uint32_t* i0,
+                     const uint32_t* i1, const uint32_t* i2, const uint32_t* i3, int log_n, int P,
+                     const PrimeInfo* pinfo, const uint2* tw) {
+    const int threads = (1 << k2) / 8;
+    switch (k2) {
+#define HG_LOF(K)                                                                               \
+    case K:                                                                                     \
+        intt_lo8_fused_kernel<K, PRE><<<grid, threads, 0, st>>>(out, i0, i1, i2, i3, log_n, P,  \
+                                                                pinfo, tw);                     \
+        return 0;
+        HG_LOF(3) HG_LOF(4) HG_LOF(5) HG_LOF(6) HG_LOF(7) HG_LOF(8) HG_LOF(9) HG_LOF(10) HG_LOF(11)
+#undef HG_LOF
+    }
+    return -1;
 }
 
 template <bool FWD, int RB>
@@ -413,6 +496,28 @@ int hg_ntt_launch(hg_ctx* ctx, uint32_t* data, int rows, int P, int prime_offset
             HG_LAUNCH_CHECK(ctx);
         }
     }
+    return HG_OK;
+}
+
+// Inverse NTT with the pointwise product fused in (see intt_lo8_fused_kernel): `out` receives
+// RB = 2 / 3 / 1 rows [RB][P][N] for pre = 1 / 2 / 3.  Returns -1 if the shape is not covered
+// (the caller then runs the separate pointwise kernel + hg_ntt_launch).
+int hg_intt_fused(hg_ctx* ctx, int pre, uint32_t* out, const uint32_t* i0, const uint32_t* i1,
+                  const uint32_t* i2, const uint32_t* i3, int P, cudaStream_t st) {
+    const int log_n = ctx->log_n, N = ctx->N;
+    if (log_n < 3 || P > 65535) return -1;
+    int rc = hg_ensure_twiddles(ctx, P);
+    if (rc) return rc;
+    const int k1 = log_n <= 11 ? 0 : (log_n <= 14 ? 3 : 6);
+    const int k2 = log_n - k1;
+    const int rb = pre == 1 ? 2 : (pre == 2 ? 3 : 1);
+    HgTimed tm(ctx, st, HG_K_NTT, (double)rb * P * (N / 2) * log_n);
+    const dim3 g(N >> k2, 1, P);
+    if (pre == 1) launch_fused_lo8<1>(k2, g, st, out, i0, i1, i2, i3, log_n, P, ctx->d_pinfo, ctx->d_tw_inv);
+    else if (pre == 2) launch_fused_lo8<2>(k2, g, st, out, i0, i1, i2, i3, log_n, P, ctx->d_pinfo, ctx->d_tw_inv);
+    else launch_fused_lo8<3>(k2, g, st, out, i0, i1, i2, i3, log_n, P, ctx->d_pinfo, ctx->d_tw_inv);
+    HG_LAUNCH_CHECK(ctx);
+    if (k1) return ntt_pass<false>(ctx, true, k1, k2, out, rb, P, 0, ctx->d_tw_inv, st);
     return HG_OK;
 }
 

@@ -19,6 +19,13 @@ int hg_ew_divide_round(hg_ctx* ctx, uint32_t* out, int out_bits, const uint32_t*
                        int in_bits, int shift, cudaStream_t stream);
 int hg_ew_automorphism(hg_ctx* ctx, uint32_t* out, const uint32_t* a, int bits, int64_t k,
                        cudaStream_t stream);
+int hg_intt_fused(hg_ctx* ctx, int pre, uint32_t* out, const uint32_t* i0, const uint32_t* i1,
+                  const uint32_t* i2, const uint32_t* i3, int P, cudaStream_t st);
+// pointwise product fused into the inverse NTT unless HG_NO_FUSE is set (A/B checks)
+static bool fuse_pointwise() {
+    static const bool on = getenv("HG_NO_FUSE") == nullptr;
+    return on;
+}
 
 namespace {
 
@@ -520,13 +527,19 @@ extern "C" int hg_poly_mul(hg_ctx* ctx, uint32_t* out, int out_bits, hg_operand 
     if (rc) return rc;
     rc = hg_ntt_launch(ctx, buf.u32(), 2 * P, P, 0, true, st);
     if (rc) return rc;
-    const int tpw = hg_timer_begin(ctx, st, HG_K_POINTWISE);
-    pw_mul_kernel<<<pw_grid(N, P), 256, 0, st>>>(buf.u32(), buf.u32() + (size_t)P * N, P, N,
-                                                 ctx->d_pinfo);
-    hg_timer_end(ctx, tpw, st, HG_K_POINTWISE, (double)N * P);
-    HG_LAUNCH_CHECK(ctx);
-    rc = hg_ntt_launch(ctx, buf.u32(), P, P, 0, false, st);
-    if (rc) return rc;
+    rc = fuse_pointwise() ? hg_intt_fused(ctx, 3, buf.u32(), buf.u32(), buf.u32() + (size_t)P * N,
+                                          nullptr, nullptr, P, st)
+                          : -1;
+    if (rc > 0) return rc;
+    if (rc < 0) {
+        const int tpw = hg_timer_begin(ctx, st, HG_K_POINTWISE);
+        pw_mul_kernel<<<pw_grid(N, P), 256, 0, st>>>(buf.u32(), buf.u32() + (size_t)P * N, P, N,
+                                                     ctx->d_pinfo);
+        hg_timer_end(ctx, tpw, st, HG_K_POINTWISE, (double)N * P);
+        HG_LAUNCH_CHECK(ctx);
+        rc = hg_ntt_launch(ctx, buf.u32(), P, P, 0, false, st);
+        if (rc) return rc;
+    }
     OutSet outs{};
     outs.out[0] = out;
     return launch_crt(ctx, buf.u32(), 1, P, 0, out_bits, outs, st);
@@ -554,12 +567,20 @@ extern "C" int hg_poly_tensor(hg_ctx* ctx, uint32_t* d0, uint32_t* d1, uint32_t*
     if (rc) return rc;
     rc = hg_ntt_launch(ctx, buf.u32(), 4 * P, P, 0, true, st);
     if (rc) return rc;
-    const int tpw = hg_timer_begin(ctx, st, HG_K_POINTWISE);
-    pw_tensor_kernel<<<pw_grid(N, P), 256, 0, st>>>(buf.u32(), P, N, ctx->d_pinfo);
-    hg_timer_end(ctx, tpw, st, HG_K_POINTWISE, (double)N * P);
-    HG_LAUNCH_CHECK(ctx);
-    rc = hg_ntt_launch(ctx, buf.u32(), 3 * P, P, 0, false, st);
-    if (rc) return rc;
+    {
+        const size_t sp = (size_t)P * N;
+        uint32_t* b = buf.u32();
+        rc = fuse_pointwise() ? hg_intt_fused(ctx, 2, b, b, b + sp, b + 2 * sp, b + 3 * sp, P, st) : -1;
+    }
+    if (rc > 0) return rc;
+    if (rc < 0) {
+        const int tpw = hg_timer_begin(ctx, st, HG_K_POINTWISE);
+        pw_tensor_kernel<<<pw_grid(N, P), 256, 0, st>>>(buf.u32(), P, N, ctx->d_pinfo);
+        hg_timer_end(ctx, tpw, st, HG_K_POINTWISE, (double)N * P);
+        HG_LAUNCH_CHECK(ctx);
+        rc = hg_ntt_launch(ctx, buf.u32(), 3 * P, P, 0, false, st);
+        if (rc) return rc;
+    }
     OutSet outs{};
     outs.out[0] = d0; outs.out[1] = d1; outs.out[2] = d2;
     return launch_crt(ctx, buf.u32(), 3, P, 0, out_bits, outs, st);
@@ -646,14 +667,18 @@ extern "C" int hg_keyswitch(hg_ctx* ctx, const hg_key* key, const uint32_t* x,
     if (rc) return rc;
     rc = hg_ntt_launch(ctx, buf.u32(), P, P, 0, true, st);
     if (rc) return rc;
-    const int tpw = hg_timer_begin(ctx, st, HG_K_POINTWISE);
-    pw_key2_kernel<<<pw_grid(N, P), 256, 0, st>>>(buf.u32(), key->d_kb, key->d_ka, P, N,
-                                                  ctx->d_pinfo);
-    hg_timer_end(ctx, tpw, st, HG_K_POINTWISE, (double)N * P);
-    HG_LAUNCH_CHECK(ctx);
     uint32_t* t = buf.u32() + (size_t)P * N;
-    rc = hg_ntt_launch(ctx, t, 2 * P, P, 0, false, st);
-    if (rc) return rc;
+    rc = fuse_pointwise() ? hg_intt_fused(ctx, 1, t, buf.u32(), key->d_kb, key->d_ka, nullptr, P, st) : -1;
+    if (rc > 0) return rc;
+    if (rc < 0) {
+        const int tpw = hg_timer_begin(ctx, st, HG_K_POINTWISE);
+        pw_key2_kernel<<<pw_grid(N, P), 256, 0, st>>>(buf.u32(), key->d_kb, key->d_ka, P, N,
+                                                      ctx->d_pinfo);
+        hg_timer_end(ctx, tpw, st, HG_K_POINTWISE, (double)N * P);
+        HG_LAUNCH_CHECK(ctx);
+        rc = hg_ntt_launch(ctx, t, 2 * P, P, 0, false, st);
+        if (rc) return rc;
+    }
     OutSet outs{};
     outs.out[0] = out0; outs.out[1] = out1;
     return launch_crt(ctx, t, 2, P, key->big_l, key->level, outs, st);
@@ -772,13 +797,19 @@ extern "C" int hg_ct_mult_prepared(hg_ctx* ctx, const hg_key* evk, const hg_ctpr
     if (rc) return rc;
     rc = hg_ntt_launch(ctx, res.u32(), 2 * P, P, 0, true, st);
     if (rc) return rc;
-    const int tpw = hg_timer_begin(ctx, st, HG_K_POINTWISE);
-    pw_tensor_prep_kernel<<<pw_grid(N, P), 256, 0, st>>>(a->d_res, a->d_res + (size_t)P * N,
-                                                         res.u32(), P, N, ctx->d_pinfo);
-    hg_timer_end(ctx, tpw, st, HG_K_POINTWISE, (double)N * P);
-    HG_LAUNCH_CHECK(ctx);
-    rc = hg_ntt_launch(ctx, res.u32(), 3 * P, P, 0, false, st);
-    if (rc) return rc;
+    rc = fuse_pointwise() ? hg_intt_fused(ctx, 2, res.u32(), a->d_res, a->d_res + (size_t)P * N,
+                                          res.u32(), res.u32() + (size_t)P * N, P, st)
+                          : -1;
+    if (rc > 0) return rc;
+    if (rc < 0) {
+        const int tpw = hg_timer_begin(ctx, st, HG_K_POINTWISE);
+        pw_tensor_prep_kernel<<<pw_grid(N, P), 256, 0, st>>>(a->d_res, a->d_res + (size_t)P * N,
+                                                             res.u32(), P, N, ctx->d_pinfo);
+        hg_timer_end(ctx, tpw, st, HG_K_POINTWISE, (double)N * P);
+        HG_LAUNCH_CHECK(ctx);
+        rc = hg_ntt_launch(ctx, res.u32(), 3 * P, P, 0, false, st);
+        if (rc) return rc;
+    }
     uint32_t* d0 = buf.u32();
     uint32_t* d1 = d0 + (size_t)W * N;
     uint32_t* d2 = d1 + (size_t)W * N;
