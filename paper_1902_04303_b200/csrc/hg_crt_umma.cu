@@ -320,13 +320,25 @@ __global__ void __launch_bounds__(2 * kRows) crt_umma_kernel(
 //   warps 3-10  converters: residues -> y_j = x_j (Q/p_j)^{-1} -> A stage; v = round(sum y_j/p_j)
 //   warps 11-18 epilogue, two groups of 4 taking alternate jobs: TMEM lane = coefficient:
 //               digit fold, carry chain (handed between the groups), window emission
-constexpr int kConvWarp0 = 3, kEpiWarp0 = 11, kPipeWarps = 19;
-constexpr int kRR = 3, kRA = 4, kRB = 3;
+//   warp 19     (fused finish only) addend producer: the job's 32 addend words of its 128
+//               coefficients as one 2-D TMA box into a 2-stage ring
+constexpr int kConvWarp0 = 3, kEpiWarp0 = 11, kAddWarp = 19;
+template <bool FUSED> struct PipeCfg {
+    static constexpr int kWarps = FUSED ? 20 : 19;
+    static constexpr int kRA = FUSED ? 2 : 4;
+    static constexpr int kRB = 3;
+};
+constexpr int kRR = 3;
 constexpr int kJobCols = 32;                     // output words per job (N = 256)
 constexpr int kResStage = 32 * kRows * 4;        // 16 KB: 32 prime rows of 128 residues
 constexpr int kAStage = kRows * kKChunk;         // 16 KB
 constexpr int kBStagePipe = kJobCols * 8 * kKChunk;   // 32 KB
-constexpr size_t kPipeSmem = (size_t)kRR * kResStage + (size_t)kRA * kAStage + (size_t)kRB * kBStagePipe;
+constexpr int kAddStage = kJobCols * kRows * 4;  // 16 KB: 32 addend words of 128 coefficients
+template <bool FUSED>
+constexpr size_t pipe_smem() {
+    return (size_t)kRR * kResStage + (size_t)PipeCfg<FUSED>::kRA * kAStage + (size_t)PipeCfg<FUSED>::kRB * kBStagePipe +
+           (FUSED ? 2 * (size_t)kAddStage : 0);
+}
 
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
@@ -343,6 +355,78 @@ __device__ __forceinline__ void umma_commit(uint32_t bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar) : "memory");
 }
 
+// Output stage of the pipelined kernel.  Plain: word u of the CRT window goes to out[u].
+// Fused finish (CrtFinish): the window value e (out_bits = l bits) is streamed through
+//     s = (e + addend + 2^(post-1)) mod 2^l,   out = bits [post, l) of s
+// -- the add of ckks.mult / _apply_automorphism followed by the rescale's divide_round
+// (ckks.py:166-184, 247-253, 310-313) -- with the addend optionally read through the ring
+// automorphism (out[i] = +/- add[i * kinv mod 2N], the negation as ~a + 1).
+struct Emitter {
+    uint32_t* out;
+    const uint32_t* add;
+    int N, i, src, out_w, post, rw, rb, out2_w, rw2;
+    uint32_t top_l, top2, rbit2, c2, prev2;
+    bool plain, negate;
+    __device__ __forceinline__ void init(uint32_t* o, int n, int ii, int out_bits, const CrtFinish& f,
+                                         const uint32_t* addp) {
+        out = o;
+        N = n;
+        i = ii;
+        out_w = (out_bits + 31) >> 5;
+        top_l = (out_bits & 31) ? ((1u << (out_bits & 31)) - 1u) : 0xffffffffu;
+        add = addp;
+        post = f.post;
+        plain = addp == nullptr && post == 0;
+        src = ii;
+        bool neg = false;
+        if (addp && f.kinv != 0) {
+            int64_t j = ((int64_t)ii * f.kinv) & (2ll * n - 1);
+            neg = j >= n;
+            src = (int)(neg ? j - n : j);
+        }
+        c2 = neg ? 1u : 0u;   // -a = ~a + 1
+        prev2 = 0u;
+        negate = neg;
+        rw = post >> 5;
+        rb = post & 31;
+        const int bits2 = out_bits - post;
+        out2_w = (bits2 + 31) >> 5;
+        top2 = (bits2 & 31) ? ((1u << (bits2 & 31)) - 1u) : 0xffffffffu;
+        rw2 = post > 0 ? (post - 1) >> 5 : -1;
+        rbit2 = post > 0 ? 1u << ((post - 1) & 31) : 0u;
+    }
+    // addend word u (0 when there is none); callers prefetch it off the carry chain
+    __device__ __forceinline__ uint32_t load_add(int u) const {
+        return (add && u >= 0 && u < out_w) ? __ldg(add + (size_t)u * N + src) : 0u;
+    }
+    __device__ __forceinline__ void put(int u, uint32_t e, uint32_t a) {
+        if (u == out_w - 1) e &= top_l;
+        if (plain) {
+            out[(size_t)u * N + i] = e;
+            return;
+        }
+        if (negate) a = ~a;
+        const uint64_t sum = (uint64_t)e + a + c2 + (u == rw2 ? rbit2 : 0u);
+        uint32_t w = (uint32_t)sum;
+        c2 = (uint32_t)(sum >> 32);
+        if (u == out_w - 1) w &= top_l;
+        if (rb == 0) {
+            const int v = u - rw;
+            if (v >= 0 && v < out2_w) out[(size_t)v * N + i] = v == out2_w - 1 ? (w & top2) : w;
+        } else {
+            const int v = u - rw - 1;
+            if (v >= 0 && v < out2_w)
+                out[(size_t)v * N + i] = ((prev2 >> rb) | (w << (32 - rb))) & (v == out2_w - 1 ? top2 : 0xffffffffu);
+            prev2 = w;
+        }
+    }
+    __device__ __forceinline__ void flush() {
+        if (plain || rb == 0) return;
+        const int v = out_w - 1 - rw;
+        if (v >= 0 && v < out2_w) out[(size_t)v * N + i] = (prev2 >> rb) & (v == out2_w - 1 ? top2 : 0xffffffffu);
+    }
+};
+
 // exact column scan for one coefficient with y_j and v recomputed from the residues (rare)
 __device__ void pipe_rescan_exact(const uint32_t* __restrict__ r, int P, int N, int W,
                                   const PrimeInfo* __restrict__ pinfo,
@@ -351,7 +435,8 @@ __device__ void pipe_rescan_exact(const uint32_t* __restrict__ r, int P, int N, 
                                   const double* __restrict__ invp,
                                   const uint32_t* __restrict__ Mtab,
                                   const uint32_t* __restrict__ negQ, int shift, int out_bits,
-                                  uint32_t* __restrict__ out, int i) {
+                                  Emitter em) {
+    const int i = em.i;
     double S = 0.0;
     for (int j = 0; j < P; ++j) {
         const uint32_t p = pinfo[j].p;
@@ -380,35 +465,38 @@ __device__ void pipe_rescan_exact(const uint32_t* __restrict__ r, int P, int N, 
         const uint32_t word = (uint32_t)acc;
         carry = top;
         if (t >= sw) {
-            if (sb == 0) {
-                const int u = t - sw;
-                out[(size_t)u * N + i] = (u == out_w - 1) ? (word & top_mask) : word;
-            } else if (t > sw) {
-                const int u = t - sw - 1;
-                const uint32_t o = (prev >> sb) | (word << (32 - sb));
-                out[(size_t)u * N + i] = (u == out_w - 1) ? (o & top_mask) : o;
-            }
+            if (sb == 0) em.put(t - sw, word, em.load_add(t - sw));
+            else if (t > sw) em.put(t - sw - 1, (prev >> sb) | (word << (32 - sb)), em.load_add(t - sw - 1));
         }
         prev = word;
     }
+    em.flush();
+    (void)top_mask;
 }
 
-__global__ void __launch_bounds__(kPipeWarps * 32, 1) crt_umma_pipe_kernel(
-    const __grid_constant__ CUtensorMap res_map, const uint32_t* __restrict__ res, int P, int P32p, int N, int nouts,
+template <bool FUSED>
+__global__ void __launch_bounds__(PipeCfg<FUSED>::kWarps * 32, 1) crt_umma_pipe_kernel(
+    const __grid_constant__ CUtensorMap res_map, const __grid_constant__ CUtensorMap add_map,
+    const uint32_t* __restrict__ res, int P, int P32p, int N, int nouts,
     const PrimeInfo* __restrict__ pinfo, const uint8_t* __restrict__ Bpipe,
     const uint32_t* __restrict__ Mtab, int W, const uint32_t* __restrict__ negQ,
     const uint32_t* __restrict__ cinv, const uint32_t* __restrict__ cinv_sh,
-    const double* __restrict__ invp, int shift, int out_bits, int tb0, UOuts outs) {
+    const double* __restrict__ invp, int shift, int out_bits, int tb0, UOuts outs, CrtFinish fin) {
+    constexpr int kRA = PipeCfg<FUSED>::kRA;
+    constexpr int kRB = PipeCfg<FUSED>::kRB;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* s_res = smem;
     uint8_t* s_a = smem + kRR * kResStage;
     uint8_t* s_b = s_a + kRA * kAStage;
+    const uint32_t* s_add = reinterpret_cast<const uint32_t*>(s_b + kRB * kBStagePipe);
+    __shared__ __align__(8) uint64_t bar_add_full[2], bar_add_empty[2];
     __shared__ __align__(8) uint64_t bar_res_full[kRR], bar_res_empty[kRR];
     __shared__ __align__(8) uint64_t bar_a_full[kRA], bar_a_empty[kRA];
     __shared__ __align__(8) uint64_t bar_b_full[kRB], bar_b_empty[kRB];
     __shared__ __align__(8) uint64_t bar_tm_full[2], bar_tm_empty[2];
     __shared__ __align__(8) uint64_t bar_hand_full[2], bar_hand_empty[2];
     __shared__ uint4 s_hand[2][kRows];             // carry lo/hi, previous word, ambiguity
+    __shared__ uint2 s_hand2[2][kRows];            // emitter state: carry, previous word
     __shared__ uint32_t tmem_base;
     __shared__ uint4 s_pc[HG_MAX_PRIMES + 32];     // p, cinv, cinv_sh, floor(2^53/p) (1,0,0,0 padding)
     __shared__ uint64_t s_acc[2][kRows];
@@ -432,6 +520,7 @@ __global__ void __launch_bounds__(kPipeWarps * 32, 1) crt_umma_pipe_kernel(
         for (int s = 0; s < kRB; ++s) { init(&bar_b_full[s], 1); init(&bar_b_empty[s], 1); }
         for (int s = 0; s < 2; ++s) { init(&bar_tm_full[s], 1); init(&bar_tm_empty[s], 4); }
         for (int s = 0; s < 2; ++s) { init(&bar_hand_full[s], 4); init(&bar_hand_empty[s], 4); }
+        for (int s = 0; s < 2; ++s) { init(&bar_add_full[s], 1); init(&bar_add_empty[s], 4); }
         asm volatile("fence.mbarrier_init.release.cluster;\n");
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n");
@@ -465,6 +554,7 @@ __global__ void __launch_bounds__(kPipeWarps * 32, 1) crt_umma_pipe_kernel(
                     for (int kc = 0; kc < nkc; ++kc, ++it) {
                         const int s = it % kRR;
                         mbar_wait(smem_u32(&bar_res_empty[s]), ((it / kRR) & 1) ^ 1);
+                        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
                         mbar_expect_tx(smem_u32(&bar_res_full[s]), (uint32_t)kResStage);
                         asm volatile(
                             "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
@@ -524,6 +614,26 @@ __global__ void __launch_bounds__(kPipeWarps * 32, 1) crt_umma_pipe_kernel(
                 umma_commit(smem_u32(&bar_tm_full[tb]));
             }
         }
+    } else if (warp == kAddWarp) {
+        // ---------------- addend producer (fused finish) ----------------
+        if (FUSED && lane == 0) {
+            int ij = 0;
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
+                for (int h = 0; h < jpt; ++h, ++ij) {
+                    const int oy = tile / tpo, cb = (tile - oy * tpo) * kRows;
+                    const int ubase = tb0 + h * kJobCols - sw - (sbit ? 1 : 0);
+                    const int s = ij & 1;
+                    mbar_wait(smem_u32(&bar_add_empty[s]), ((ij >> 1) & 1) ^ 1);
+                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                    mbar_expect_tx(smem_u32(&bar_add_full[s]), (uint32_t)kAddStage);
+                    asm volatile(
+                        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                        " [%0], [%1, {%2, %3}], [%4];\n"
+                        ::"r"(smem_u32(s_add + s * (kAddStage / 4))), "l"(reinterpret_cast<uint64_t>(&add_map)),
+                        "r"(cb), "r"(oy * out_w + ubase), "r"(smem_u32(&bar_add_full[s]))
+                        : "memory");
+                }
+        }
     } else if (warp < kEpiWarp0) {
         // ---------------- converters ----------------
         // warp pair (c, c + 4) owns coefficients 32c .. 32c+31; each takes 16 of a chunk's 32 primes
@@ -566,6 +676,9 @@ __global__ void __launch_bounds__(kPipeWarps * 32, 1) crt_umma_pipe_kernel(
                         if (j0 + u == P) y[u] = v;
                 }
                 mbar_wait(smem_u32(&bar_a_empty[sa_]), ((ia / kRA) & 1) ^ 1);
+                // WAR across proxies: the tensor core's (async-proxy) reads of this stage must be
+                // ordered before our generic stores
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
                 uint8_t* dst = s_a + sa_ * kAStage + (g * 8 + 4 * half) * 128 + rr * 16;
 #pragma unroll
                 for (int c = 0; c < 4; ++c)
@@ -580,9 +693,9 @@ __global__ void __launch_bounds__(kPipeWarps * 32, 1) crt_umma_pipe_kernel(
         // ---------------- epilogue ----------------
         const int q = warp & 3;
         const int n = q * 32 + lane;
-        const uint32_t top_mask = (out_bits & 31) ? ((1u << (out_bits & 31)) - 1u) : 0xffffffffu;
         const int round_col = shift > 0 ? ((shift - 1) >> 5) : -1;
         const uint32_t round_bit = shift > 0 ? (1u << ((shift - 1) & 31)) : 0u;
+        const uint32_t top_l = (out_bits & 31) ? ((1u << (out_bits & 31)) - 1u) : 0xffffffffu;
         // two groups take alternate jobs (job parity = TMEM buffer); within a tile the carry
         // state moves from the group that finished column block h to the one taking h+1
         const int grp = (warp - kEpiWarp0) >> 2;
@@ -596,7 +709,10 @@ __global__ void __launch_bounds__(kPipeWarps * 32, 1) crt_umma_pipe_kernel(
             if ((ij & 1) != grp) continue;
             const int oy = tile / tpo, cb = (tile - oy * tpo) * kRows;
             uint32_t* out = oy == 0 ? outs.out[0] : oy == 1 ? outs.out[1] : oy == 2 ? outs.out[2] : outs.out[3];
+            const uint32_t* addp = oy == 0 ? fin.add[0] : oy == 1 ? fin.add[1] : oy == 2 ? fin.add[2] : fin.add[3];
             const int i = cb + n;
+            Emitter em;
+            em.init(out, N, i, out_bits, fin, FUSED ? addp : nullptr);
             if (h == 0) {
                 carry = 0;
                 prev = 0;
@@ -605,16 +721,23 @@ __global__ void __launch_bounds__(kPipeWarps * 32, 1) crt_umma_pipe_kernel(
                 const int sl = 1 - grp;
                 mbar_wait(smem_u32(&bar_hand_full[sl]), nrd & 1);
                 const uint4 hv = s_hand[sl][n];
+                const uint2 hv2 = s_hand2[sl][n];
                 __syncwarp();
                 if (lane == 0) mbar_arrive(smem_u32(&bar_hand_empty[sl]));
                 ++nrd;
                 carry = ((uint64_t)hv.y << 32) | hv.x;
                 prev = hv.z;
                 amb = hv.w != 0;
+                em.c2 = hv2.x;
+                em.prev2 = hv2.y;
             }
             const int tb = ij & 1;
             const int c0 = tb0 + h * kJobCols;
             const int ncols = job_cols(h);
+            // the job's addend words (output word u = c0 + k - sw - (sbit != 0)), loaded before
+            // the accumulator wait so their latency is off the carry chain
+            const uint32_t* av = s_add + tb * (kAddStage / 4) + n;   // addend word k at av[k * 128]
+            if (FUSED) mbar_wait(smem_u32(&bar_add_full[tb]), (ij >> 1) & 1);
             mbar_wait(smem_u32(&bar_tm_full[tb]), (ij >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;\n");
             const uint32_t lane_addr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(tb * 256);
@@ -644,30 +767,37 @@ __global__ void __launch_bounds__(kPipeWarps * 32, 1) crt_umma_pipe_kernel(
                     if (t < sw) {
                         if (t == tb0 + 1) amb = word >= 0xFFFFFF00u;
                         else if (t > tb0 + 1) amb = amb && (word == 0xffffffffu);
-                    } else if (sbit == 0) {
-                        const int u = t - sw;
-                        out[(size_t)u * N + i] = (u == out_w - 1) ? (word & top_mask) : word;
-                    } else if (t > sw) {
-                        const int u = t - sw - 1;
-                        const uint32_t o = (prev >> sbit) | (word << (32 - sbit));
-                        out[(size_t)u * N + i] = (u == out_w - 1) ? (o & top_mask) : o;
+                    } else if (sbit == 0 || t > sw) {
+                        const uint32_t o = sbit == 0 ? word : (prev >> sbit) | (word << (32 - sbit));
+                        const int u = t - sw - (sbit ? 1 : 0);
+                        if (FUSED) em.put(u, o, av[(tl + hh) * kRows]);
+                        else out[(size_t)u * N + i] = (u == out_w - 1) ? (o & top_l) : o;
                     }
                     prev = word;
                 }
             }
+            if (FUSED) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(smem_u32(&bar_add_empty[tb]));
+            }
+            if (FUSED && h == jpt - 1) em.flush();
             asm volatile("tcgen05.fence::before_thread_sync;\n");
             __syncwarp();
             if (lane == 0) mbar_arrive(smem_u32(&bar_tm_empty[tb]));
             if (h < jpt - 1) {
                 mbar_wait(smem_u32(&bar_hand_empty[grp]), (nwr & 1) ^ 1);
                 s_hand[grp][n] = make_uint4((uint32_t)carry, (uint32_t)(carry >> 32), prev, amb ? 1u : 0u);
+                if (FUSED) s_hand2[grp][n] = make_uint2(em.c2, em.prev2);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(smem_u32(&bar_hand_full[grp]));
                 ++nwr;
             }
-            if (h == jpt - 1 && tb0 > 0 && amb)
+            if (h == jpt - 1 && tb0 > 0 && amb) {
+                Emitter fresh;
+                fresh.init(out, N, i, out_bits, fin, FUSED ? addp : nullptr);
                 pipe_rescan_exact(res + (size_t)oy * P * N, P, N, W, pinfo, cinv, cinv_sh, invp, Mtab,
-                                  negQ, shift, out_bits, out, i);
+                                  negQ, shift, out_bits, fresh);
+            }
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n");
@@ -688,22 +818,40 @@ bool hg_crt_umma_pipe_ok(const CrtTable* tab, int N, int shift, int out_bits, in
 
 int hg_crt_umma_pipe_launch(hg_ctx* ctx, const CrtTable* tab, const uint32_t* res, int nouts, int P,
                             int shift, int out_bits, int tb0, uint32_t* const* outs_in,
-                            cudaStream_t st) {
+                            cudaStream_t st, const CrtFinish* finish) {
     static int nsm = 0;
     if (!nsm) {
-        HG_CUDA_TRY(cudaFuncSetAttribute(crt_umma_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)kPipeSmem));
+        HG_CUDA_TRY(cudaFuncSetAttribute(crt_umma_pipe_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)pipe_smem<false>()));
+        HG_CUDA_TRY(cudaFuncSetAttribute(crt_umma_pipe_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)pipe_smem<true>()));
         HG_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device));
     }
     UOuts o{};
     for (int k = 0; k < nouts; ++k) o.out[k] = outs_in[k];
     const int ntiles = nouts * (ctx->N / kRows);
     const int grid = ntiles < nsm ? ntiles : nsm;
-    CUtensorMap res_map;
+    CUtensorMap res_map, add_map;
     if (int rc = hg_tmap_2d_u32(&res_map, res, (uint64_t)ctx->N, (uint64_t)nouts * P, kRows, 32)) return rc;
-    crt_umma_pipe_kernel<<<grid, kPipeWarps * 32, kPipeSmem, st>>>(
-        res_map, res, P, tab->P32p, ctx->N, nouts, ctx->d_pinfo, tab->d_Bpipe, tab->d_M, tab->W, tab->d_negQ,
-        tab->d_cinv, tab->d_cinv_sh, tab->d_invp, shift, out_bits, tb0, o);
+    const CrtFinish fin = finish ? *finish : CrtFinish{};
+    const bool fused = finish != nullptr;
+    if (fused) {
+        // the addends are nouts consecutive out_bits-wide polynomials starting at add[0]
+        const int out_w = (out_bits + 31) / 32;
+        for (int k = 0; k < nouts; ++k)
+            if (fin.kinv != 0 || fin.add[k] != fin.add[0] + (size_t)k * out_w * ctx->N)
+                return hg_fail(HG_EINVAL, "fused CRT finish: addends must be consecutive, no automorphism");
+        if (int rc = hg_tmap_2d_u32(&add_map, fin.add[0], (uint64_t)ctx->N, (uint64_t)nouts * out_w, kRows,
+                                    kJobCols))
+            return rc;
+        crt_umma_pipe_kernel<true><<<grid, PipeCfg<true>::kWarps * 32, pipe_smem<true>(), st>>>(
+            res_map, add_map, res, P, tab->P32p, ctx->N, nouts, ctx->d_pinfo, tab->d_Bpipe, tab->d_M, tab->W,
+            tab->d_negQ, tab->d_cinv, tab->d_cinv_sh, tab->d_invp, shift, out_bits, tb0, o, fin);
+    } else {
+        crt_umma_pipe_kernel<false><<<grid, PipeCfg<false>::kWarps * 32, pipe_smem<false>(), st>>>(
+            res_map, res_map, res, P, tab->P32p, ctx->N, nouts, ctx->d_pinfo, tab->d_Bpipe, tab->d_M, tab->W,
+            tab->d_negQ, tab->d_cinv, tab->d_cinv_sh, tab->d_invp, shift, out_bits, tb0, o, fin);
+    }
     HG_LAUNCH_CHECK(ctx);
     return HG_OK;
 }

@@ -148,9 +148,17 @@ int hg_crt_umma_launch(hg_ctx* ctx, const CrtTable* tab, const uint32_t* res, in
                        int shift, int out_bits, int tb0, uint32_t* const* outs, cudaStream_t st);
 size_t hg_crt_umma_smem(int P32);
 bool hg_crt_umma_pipe_ok(const CrtTable* tab, int N, int shift, int out_bits, int tb0);
+// Optional fused finish of the pipelined CRT (see Emitter in hg_crt_umma.cu): per output k,
+// out_k = bits [post, out_bits) of (window_k + add_k' + 2^(post-1)) mod 2^out_bits, where
+// add_k' is add_k (out_bits wide, may be null) read through x -> x^k when kinv != 0.
+struct CrtFinish {
+    const uint32_t* add[4] = {nullptr, nullptr, nullptr, nullptr};
+    int64_t kinv = 0;
+    int post = 0;
+};
 int hg_crt_umma_pipe_launch(hg_ctx* ctx, const CrtTable* tab, const uint32_t* res, int nouts, int P,
                             int shift, int out_bits, int tb0, uint32_t* const* outs,
-                            cudaStream_t st);
+                            cudaStream_t st, const CrtFinish* finish = nullptr);
 int hg_modup_umma_launch(hg_ctx* ctx, const uint32_t* const* words, const int* bits,
                          const int* is_signed, int nops, int P, uint32_t* out, int64_t kinv,
                          cudaStream_t st);

@@ -129,6 +129,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) modup_umma_kernel(
                 for (int ch = 0; ch < nch; ++ch, ++ib) {
                     const int s = ib & 1;
                     mbar_wait(smem_u32(&bar_b_empty[s]), ((ib >> 1) & 1) ^ 1);
+                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
                     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(&bar_b_full[s])), "r"(bytes) : "memory");
                     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
                                  ::"r"(smem_u32(s_b + s * kBChunkBytes)), "l"(Bimg + (size_t)ch * kBChunkBytes),
@@ -192,6 +193,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) modup_umma_kernel(
             const int sa_ = ia & 1;
             mbar_wait(smem_u32(&bar_a_empty[sa_]), ((ia >> 1) & 1) ^ 1);
             mbar_wait(smem_u32(&bar_fl_empty[sa_]), ((ia >> 1) & 1) ^ 1);
+            // WAR across proxies: the tensor core's reads of this stage precede our stores
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
             uint8_t* dst = s_a + sa_ * kAStage + (g * 16) * 128 + rr * 16;
             uint32_t any = 0, sign = 0;
             for (int w0 = 0; w0 < W8; w0 += 32) {

@@ -425,27 +425,46 @@ int launch_modup(hg_ctx* ctx, const OperandSet& ops, int nops, int P, uint32_t* 
     return HG_OK;
 }
 
+// columns below shift/32 only feed the carry: keep two of them (plus alignment) as a
+// truncated fixed-point window instead of scanning all of them (exact rescan on doubt)
+int crt_tb0(int shift) {
+    const int sw = shift >> 5;
+    return sw >= 2 ? ((sw - 2) & ~(kCrtCols - 1)) : 0;
+}
+
+bool crt_pipe_enabled(hg_ctx* ctx) {
+    static const bool off = getenv("HG_NO_UMMA") || getenv("HG_NO_MMA") || getenv("HG_NO_PIPE");
+    return ctx->N >= 128 && !off;
+}
+
+// true when launch_crt can take a CrtFinish (the pipelined tcgen05 kernel runs this window)
+bool crt_finish_ok(hg_ctx* ctx, int P, int shift, int out_bits) {
+    if (!crt_pipe_enabled(ctx) || getenv("HG_NO_FUSE")) return false;
+    const CrtTable* tab = nullptr;
+    if (hg_get_crt(ctx, P, &tab)) return false;
+    return hg_crt_umma_pipe_ok(tab, ctx->N, shift, out_bits, crt_tb0(shift));
+}
+
 int launch_crt(hg_ctx* ctx, const uint32_t* res, int nouts, int P, int shift, int out_bits,
-               const OutSet& outs, cudaStream_t st) {
+               const OutSet& outs, cudaStream_t st, const CrtFinish* finish = nullptr) {
     const CrtTable* tab = nullptr;
     int rc = hg_get_crt(ctx, P, &tab);
     if (rc) return rc;
     int sw = shift >> 5;
     int T = sw + words_for_bits(out_bits) + ((shift & 31) ? 1 : 0);
     if (T > tab->W) return hg_fail(HG_ERANGE, "CRT window exceeds table width");
-    // columns below shift/32 only feed the carry: keep two of them (plus alignment) as a
-    // truncated fixed-point window instead of scanning all of them (exact rescan on doubt)
-    const int tb0 = sw >= 2 ? ((sw - 2) & ~(kCrtCols - 1)) : 0;
+    const int tb0 = crt_tb0(shift);
     const int N = ctx->N;
     const int threads = N < kCrtThreads ? N : kCrtThreads;
     size_t smem = (size_t)tab->P4 * threads * 4;
     dim3 grid(N / threads, nouts);
-    if (N >= 128 && !getenv("HG_NO_UMMA") && !getenv("HG_NO_MMA") && !getenv("HG_NO_PIPE") &&
-        hg_crt_umma_pipe_ok(tab, N, shift, out_bits, tb0)) {
+    if (crt_pipe_enabled(ctx) && hg_crt_umma_pipe_ok(tab, N, shift, out_bits, tb0)) {
         // persistent warp-specialised tcgen05 path
         HgTimed tm(ctx, st, HG_K_CRT, (double)nouts * N * (double)P * (T - tb0));
-        return hg_crt_umma_pipe_launch(ctx, tab, res, nouts, P, shift, out_bits, tb0, outs.out, st);
+        return hg_crt_umma_pipe_launch(ctx, tab, res, nouts, P, shift, out_bits, tb0, outs.out, st,
+                                       finish);
     }
+    if (finish) return hg_fail(HG_EINVAL, "fused CRT finish needs the pipelined kernel");
     if (N >= 128 && !getenv("HG_NO_UMMA") && !getenv("HG_NO_MMA") &&
         hg_crt_umma_smem(tab->P32) <= 220 * 1024) {
         // tcgen05 path (UTCIMMA, accumulators in TMEM)
@@ -645,11 +664,20 @@ static int64_t inverse_mod_2n(int64_t k, int64_t n2) {
     return (int64_t)(inv & (uint64_t)(n2 - 1));
 }
 
+static int keyswitch_impl(hg_ctx* ctx, const hg_key* key, const uint32_t* x, int64_t automorph_k,
+                          uint32_t* out0, uint32_t* out1, cudaStream_t st, const CrtFinish* fin);
+
 extern "C" int hg_keyswitch(hg_ctx* ctx, const hg_key* key, const uint32_t* x,
                             int64_t automorph_k, uint32_t* out0, uint32_t* out1, void* stream) {
     if (!ctx || !key || !x || !out0 || !out1 || key->ctx != ctx)
         return hg_fail(HG_EINVAL, "hg_keyswitch: bad arguments");
-    cudaStream_t st = (cudaStream_t)stream;
+    return keyswitch_impl(ctx, key, x, automorph_k, out0, out1, (cudaStream_t)stream, nullptr);
+}
+
+// out = window [L, L+level) of x * (kb, ka), x read through x -> x^k; `fin` (optional) fuses
+// the caller's add / rescale into the CRT epilogue
+static int keyswitch_impl(hg_ctx* ctx, const hg_key* key, const uint32_t* x, int64_t automorph_k,
+                          uint32_t* out0, uint32_t* out1, cudaStream_t st, const CrtFinish* fin) {
     const int N = ctx->N;
     const int P = key->P;
     int64_t kinv = 0;
@@ -681,7 +709,7 @@ extern "C" int hg_keyswitch(hg_ctx* ctx, const hg_key* key, const uint32_t* x,
     }
     OutSet outs{};
     outs.out[0] = out0; outs.out[1] = out1;
-    return launch_crt(ctx, t, 2, P, key->big_l, key->level, outs, st);
+    return launch_crt(ctx, t, 2, P, key->big_l, key->level, outs, st, fin);
 }
 
 // ---- fused scheme ops ------------------------------------------------------------------------------
@@ -689,6 +717,14 @@ extern "C" int hg_keyswitch(hg_ctx* ctx, const hg_key* key, const uint32_t* x,
 static int ct_mult_finish(hg_ctx* ctx, const hg_key* evk, uint32_t* d0, uint32_t* d1,
                           uint32_t* d2, uint32_t* e0, uint32_t* e1, int level, int rescale_bits,
                           uint32_t* out0, uint32_t* out1, cudaStream_t st) {
+    if (crt_finish_ok(ctx, evk->P, evk->big_l, level)) {
+        // relinearise, add (d0, d1) and rescale in the key switch's CRT epilogue
+        CrtFinish fin;
+        fin.add[0] = d0;
+        fin.add[1] = d1;
+        fin.post = rescale_bits;
+        return keyswitch_impl(ctx, evk, d2, 1, out0, out1, st, &fin);
+    }
     int rc = hg_keyswitch(ctx, evk, d2, 1, e0, e1, st);
     if (rc) return rc;
     if (rescale_bits == 0) {
