@@ -325,8 +325,8 @@ __global__ void __launch_bounds__(2 * kRows) crt_umma_kernel(
 constexpr int kConvWarp0 = 3, kEpiWarp0 = 11, kAddWarp = 19;
 template <bool FUSED> struct PipeCfg {
     static constexpr int kWarps = FUSED ? 20 : 19;
-    static constexpr int kRA = FUSED ? 2 : 4;
-    static constexpr int kRB = 3;
+    static constexpr int kRA = 4;
+    static constexpr int kRB = FUSED ? 2 : 3;
 };
 constexpr int kRR = 3;
 constexpr int kJobCols = 32;                     // output words per job (N = 256)
