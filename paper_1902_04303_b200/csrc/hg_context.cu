@@ -3,9 +3,19 @@
 #include "hg_internal.cuh"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <string>
+
+// HG_DEBUG_BUILD=1: report host-side table builds (they run on first use of a prime count)
+static void build_note(const char* what, int P, std::chrono::steady_clock::time_point t0) {
+    static const bool on = getenv("HG_DEBUG_BUILD") != nullptr;
+    if (!on) return;
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    fprintf(stderr, "[hg build] %s P=%d %.1f ms\n", what, P, ms);
+}
 
 static thread_local std::string g_last_error;
 
@@ -52,11 +62,6 @@ static bool is_prime_u32(uint32_t n) {
 }
 static uint32_t shoup_of(uint32_t w, uint32_t p) {
     return (uint32_t)(((uint64_t)w << 32) / p);
-}
-static uint32_t bitrev(uint32_t x, int bits) {
-    uint32_t r = 0;
-    for (int i = 0; i < bits; ++i) { r = (r << 1) | (x & 1); x >>= 1; }
-    return r;
 }
 
 // ---- context ----------------------------------------------------------------------------
@@ -235,15 +240,41 @@ int hg_primes_for_bits(const hg_ctx* ctx, double bits) {
 // ---- twiddles ----------------------------------------------------------------------------
 // psi_rev[k] = psi^bitrev(k), ipsi_rev[k] = psi^-bitrev(k) for a primitive 2N-th root psi
 // (merged negacyclic Cooley-Tukey forward / Gentleman-Sande inverse).
+// psi^bitrev(k) and psi^-bitrev(k) with their Shoup companions, one thread per (prime, k)
+__global__ void twiddle_kernel(uint2* __restrict__ fwd, uint2* __restrict__ inv,
+                               const uint32_t* __restrict__ roots, const uint32_t* __restrict__ primes,
+                               int logn) {
+    const int N = 1 << logn;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= N) return;
+    const int j = blockIdx.y;
+    const uint64_t p = primes[j], root = roots[j];
+    auto pw = [&](uint32_t e) {
+        uint64_t r = 1, b = root;
+        while (e) {
+            if (e & 1) r = r * b % p;
+            b = b * b % p;
+            e >>= 1;
+        }
+        return (uint32_t)r;
+    };
+    const uint32_t e = __brev((uint32_t)k) >> (32 - logn);
+    const uint32_t w = pw(e);
+    const uint32_t iw = e == 0 ? 1u : (uint32_t)(p - pw(N - e));   // psi^-e = -psi^(N-e)
+    const size_t o = (size_t)j * N + k;
+    fwd[o] = make_uint2(w, (uint32_t)(((uint64_t)w << 32) / p));
+    inv[o] = make_uint2(iw, (uint32_t)(((uint64_t)iw << 32) / p));
+}
+
 int hg_ensure_twiddles(hg_ctx* ctx, int P) {
     std::lock_guard<std::mutex> lk(ctx->mu);
     if (P <= ctx->tw_ready) return HG_OK;
-    const int N = ctx->N, logn = ctx->log_n;
-    int j0 = ctx->tw_ready;
-    size_t cnt = (size_t)(P - j0) * N;
-    std::vector<uint2> psi(cnt), ipsi(cnt);
-    std::vector<uint32_t> pw(N);
-    for (int j = j0; j < P; ++j) {
+    const auto t_start = std::chrono::steady_clock::now();
+    const int N = ctx->N;
+    // materialise every prime at once (the tables are allocated for all of them)
+    const int j0 = ctx->tw_ready, j1 = ctx->nprimes;
+    std::vector<uint32_t> roots(j1 - j0);
+    for (int j = j0; j < j1; ++j) {
         uint32_t p = ctx->primes[j];
         uint64_t root = 0;
         for (uint64_t g = 2; g < p; ++g) {
@@ -251,21 +282,22 @@ int hg_ensure_twiddles(hg_ctx* ctx, int P) {
             if (powmod(cand, N, p) == p - 1) { root = cand; break; }
         }
         if (!root) return hg_fail(HG_EINVAL, "no primitive 2N-th root");
-        uint64_t v = 1;
-        for (int i = 0; i < N; ++i) { pw[i] = (uint32_t)v; v = mulmod64(v, root, p); }
-        size_t base = (size_t)(j - j0) * N;
-        for (int k = 0; k < N; ++k) {
-            uint32_t e = bitrev((uint32_t)k, logn);
-            uint32_t w = pw[e];
-            uint32_t iw = e == 0 ? 1u : (uint32_t)(p - pw[N - e]);  // psi^-e = -psi^(N-e)
-            psi[base + k] = make_uint2(w, shoup_of(w, p));
-            ipsi[base + k] = make_uint2(iw, shoup_of(iw, p));
-        }
+        roots[j - j0] = (uint32_t)root;
     }
-    size_t off = (size_t)j0 * N;
-    HG_CUDA_TRY(cudaMemcpy(ctx->d_tw_fwd + off, psi.data(), cnt * 8, cudaMemcpyHostToDevice));
-    HG_CUDA_TRY(cudaMemcpy(ctx->d_tw_inv + off, ipsi.data(), cnt * 8, cudaMemcpyHostToDevice));
-    ctx->tw_ready = P;
+    uint32_t *d_roots = nullptr, *d_primes = nullptr;
+    HG_CUDA_TRY(cudaMalloc(&d_roots, roots.size() * 4));
+    HG_CUDA_TRY(cudaMalloc(&d_primes, roots.size() * 4));
+    HG_CUDA_TRY(cudaMemcpy(d_roots, roots.data(), roots.size() * 4, cudaMemcpyHostToDevice));
+    HG_CUDA_TRY(cudaMemcpy(d_primes, ctx->primes.data() + j0, roots.size() * 4, cudaMemcpyHostToDevice));
+    const size_t off = (size_t)j0 * N;
+    twiddle_kernel<<<dim3((N + 255) / 256, j1 - j0), 256>>>(ctx->d_tw_fwd + off, ctx->d_tw_inv + off, d_roots,
+                                                         d_primes, ctx->log_n);
+    HG_CUDA_TRY(cudaGetLastError());
+    HG_CUDA_TRY(cudaDeviceSynchronize());
+    cudaFree(d_roots);
+    cudaFree(d_primes);
+    ctx->tw_ready = j1;
+    build_note("twiddles", j1, t_start);
     return HG_OK;
 }
 
@@ -314,6 +346,7 @@ int hg_get_crt(hg_ctx* ctx, int P, const CrtTable** out) {
         auto it = ctx->crt.find(P);
         if (it != ctx->crt.end()) { *out = &it->second; return HG_OK; }
     }
+    const auto t_start = std::chrono::steady_clock::now();
     CrtTable t;
     t.P = P;
     t.P4 = (P + 3) & ~3;
@@ -337,17 +370,18 @@ int hg_get_crt(hg_ctx* ctx, int P, const CrtTable** out) {
             borrow = (Q[w] != 0 || borrow) ? 1 : 0;
         }
     }
+    // W >= bits(Q)/32 + 2, so Q is exact in W words and Q/p_j is an exact multiword division
     for (int j = 0; j < P; ++j) {
-        std::vector<uint32_t> Qj(W, 0u);
-        Qj[0] = 1;
         uint64_t qmodp = 1;
         uint32_t pj = ctx->primes[j];
-        for (int i = 0; i < P; ++i) {
-            if (i == j) continue;
-            mul_small_trunc(Qj, ctx->primes[i]);
-            qmodp = mulmod64(qmodp, ctx->primes[i] % pj, pj);
+        for (int i = 0; i < P; ++i)
+            if (i != j) qmodp = mulmod64(qmodp, ctx->primes[i] % pj, pj);
+        uint64_t rem = 0;
+        for (int w = W - 1; w >= 0; --w) {
+            const uint64_t cur = (rem << 32) | Q[w];
+            M[(size_t)j * W + w] = (uint32_t)(cur / pj);
+            rem = cur % pj;
         }
-        for (int w = 0; w < W; ++w) M[(size_t)j * W + w] = Qj[w];
         uint64_t inv = powmod(qmodp, pj - 2, pj);
         uint64_t ninv = powmod(ctx->N % pj, pj - 2, pj);
         uint64_t r32 = (1ull << 32) % pj;
@@ -368,14 +402,8 @@ int hg_get_crt(hg_ctx* ctx, int P, const CrtTable** out) {
     HG_CUDA_TRY(cudaMemcpy(t.d_invp, invp.data(), P * 8, cudaMemcpyHostToDevice));
     t.P32 = (P + 31) & ~31;
     {
-        std::vector<uint32_t> frag;
-        hg_crt_build_fragments(t, P, t.P32, frag, M);
-        HG_CUDA_TRY(cudaMalloc(&t.d_Bfrag, frag.size() * 4));
-        HG_CUDA_TRY(cudaMemcpy(t.d_Bfrag, frag.data(), frag.size() * 4, cudaMemcpyHostToDevice));
         std::vector<uint8_t> conv;
-        hg_crt_build_conv(t, P, t.P32, conv, M);
-        HG_CUDA_TRY(cudaMalloc(&t.d_Bconv, conv.size()));
-        HG_CUDA_TRY(cudaMemcpy(t.d_Bconv, conv.data(), conv.size(), cudaMemcpyHostToDevice));
+        // (the fallback kernels' B images are built on their first use: hg_crt_ensure_fallback)
         // pipelined kernel: one more K row (slot P) carries -Q, so v * (-Q) comes out of the GEMM
         t.P32p = (P + 1 + 31) & ~31;
         std::vector<uint32_t> Mp((size_t)W * t.P32p, 0u);
@@ -385,6 +413,7 @@ int hg_get_crt(hg_ctx* ctx, int P, const CrtTable** out) {
         HG_CUDA_TRY(cudaMalloc(&t.d_Bpipe, conv.size()));
         HG_CUDA_TRY(cudaMemcpy(t.d_Bpipe, conv.data(), conv.size(), cudaMemcpyHostToDevice));
     }
+    t.hM = std::move(M);
     std::lock_guard<std::mutex> lk(ctx->mu);
     auto ins = ctx->crt.emplace(P, t);
     if (!ins.second) {  // another thread won the race
@@ -394,5 +423,21 @@ int hg_get_crt(hg_ctx* ctx, int P, const CrtTable** out) {
         cudaFree(t.d_Bpipe);
     }
     *out = &ins.first->second;
+    build_note("crt", P, t_start);
+    return HG_OK;
+}
+
+int hg_crt_ensure_fallback(hg_ctx* ctx, const CrtTable* ctab) {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    CrtTable* t = const_cast<CrtTable*>(ctab);
+    if (t->d_Bfrag && t->d_Bconv) return HG_OK;
+    std::vector<uint32_t> frag;
+    hg_crt_build_fragments(*t, t->P, t->P32, frag, t->hM);
+    HG_CUDA_TRY(cudaMalloc(&t->d_Bfrag, frag.size() * 4));
+    HG_CUDA_TRY(cudaMemcpy(t->d_Bfrag, frag.data(), frag.size() * 4, cudaMemcpyHostToDevice));
+    std::vector<uint8_t> conv;
+    hg_crt_build_conv(*t, t->P, t->P32, conv, t->hM);
+    HG_CUDA_TRY(cudaMalloc(&t->d_Bconv, conv.size()));
+    HG_CUDA_TRY(cudaMemcpy(t->d_Bconv, conv.data(), conv.size(), cudaMemcpyHostToDevice));
     return HG_OK;
 }

@@ -311,6 +311,7 @@ int hg_crt_mma_launch(hg_ctx* ctx, const CrtTable* tab, const uint32_t* res, int
     for (int k = 0; k < nouts; ++k) o.out[k] = outs_in[k];
     const int N = ctx->N;
     dim3 grid(N / kCoefs, nouts);
+    if (int rc = hg_crt_ensure_fallback(ctx, tab)) return rc;
     crt_mma_kernel<<<grid, kWarps * 32, smem, st>>>(res, P, P32, N, ctx->d_pinfo, tab->d_Bfrag,
                                                     tab->d_M, tab->W, tab->d_negQ, tab->d_cinv,
                                                     tab->d_cinv_sh, tab->d_invp, shift, out_bits,

@@ -899,6 +899,7 @@ int hg_crt_umma_launch(hg_ctx* ctx, const CrtTable* tab, const uint32_t* res, in
     UOuts o{};
     for (int k = 0; k < nouts; ++k) o.out[k] = outs_in[k];
     dim3 grid(ctx->N / kRows, nouts);
+    if (int rc = hg_crt_ensure_fallback(ctx, tab)) return rc;
     crt_umma_kernel<<<grid, 2 * kRows, smem, st>>>(res, P, tab->P32, ctx->N, ctx->d_pinfo, tab->d_Bconv,
                                                tab->d_M, tab->W, tab->d_negQ, tab->d_cinv,
                                                tab->d_cinv_sh, tab->d_invp, shift, out_bits, tb0, o);

@@ -52,6 +52,7 @@ struct CrtTable {
     uint8_t* d_Bconv = nullptr;   // digit-layout B as a UMMA smem image (hg_crt_umma.cu)
     int P32p = 0;                 // (P + 1) rounded up to 32: K of the pipelined kernel
     uint8_t* d_Bpipe = nullptr;   // as d_Bconv with row P = -Q mod 2^(32W)
+    std::vector<uint32_t> hM;     // host copy of M (source of the lazily built fallback images)
 };
 
 struct hg_ctx {
@@ -137,6 +138,7 @@ int hg_tmap_2d_u32(CUtensorMap* tm, const void* base, uint64_t inner, uint64_t o
                    uint32_t box_inner, uint32_t box_outer);
 int hg_ensure_twiddles(hg_ctx* ctx, int P);
 int hg_get_crt(hg_ctx* ctx, int P, const CrtTable** out);
+int hg_crt_ensure_fallback(hg_ctx* ctx, const CrtTable* tab);   // d_Bfrag / d_Bconv
 int hg_primes_for_bits(const hg_ctx* ctx, double bits);   // -1 if too wide
 int hg_crt_build_fragments(const CrtTable& t, int P, int P32, std::vector<uint32_t>& out,
                            const std::vector<uint32_t>& M);

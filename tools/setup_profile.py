@@ -41,6 +41,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--log-n", type=int, default=17)
     ap.add_argument("--n", type=int, default=245)
+    ap.add_argument("--reps", type=int, default=2)
     args = ap.parse_args()
     params = hg.CkksParams(log_n=args.log_n, log_l=1700, log_p=45, log_p_small=30)
     sk, pk, evk, rot = hg.keygen(params, 1, device_rng=True)
@@ -50,6 +51,12 @@ def main():
     ds = synth_gwas_dataset(args.n, 4, 512, seed=0)
     cfg = gwas.GwasConfig(n=args.n, d=4, k=512)
     inputs = gwas.encrypt_gwas_inputs(ds, cfg, params, pk, gen, lazy_batches=True)
+    for rep in range(args.reps):
+        print(f"=== pass {rep} ===", flush=True)
+        run_pass(eng, inputs)
+
+
+def run_pass(eng, inputs):
     lr = inputs.logreg
     with T("hom_logreg"):
         beta, p_prev = hom_logreg(eng, lr, 3)
