@@ -9,7 +9,9 @@
 //   ckks._apply_automorphism                            ckks.py:247-253
 #include "hg_internal.cuh"
 
+#include <chrono>
 #include <cmath>
+#include <cstdio>
 
 int hg_ntt_launch(hg_ctx* ctx, uint32_t* data, int rows, int P, int prime_offset, bool forward,
                   cudaStream_t stream);
@@ -622,11 +624,15 @@ extern "C" int hg_key_prepare(hg_ctx* ctx, const uint32_t* kb, const uint32_t* k
     key->big_l = big_l;
     key->P = P;
     key->bytes = (size_t)2 * P * N * 4;
+    const auto t_alloc = std::chrono::steady_clock::now();
     if (cudaMallocAsync(&key->d_kb, key->bytes, st) != cudaSuccess) {  // pool: no device sync
         delete key;
         return hg_fail(HG_ENOMEM, "key allocation failed");
     }
     key->d_ka = key->d_kb + (size_t)P * N;
+    if (getenv("HG_DEBUG_BUILD"))
+        fprintf(stderr, "[hg build] key P=%d alloc %.2f ms\n", P,
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_alloc).count());
     OperandSet ops{};
     ops.words[0] = kb; ops.bits[0] = kbits; ops.is_signed[0] = 1;   // reduce_to(l+L), centered
     ops.words[1] = ka; ops.bits[1] = kbits; ops.is_signed[1] = 1;

@@ -9,16 +9,17 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 CASES = [(13, lv) for lv in range(140, 1701, 70)] + [(13, 1088), (13, 1152), (13, 1024), (12, 1550), (17, 1550)]
+QUICK = [(13, 1120), (13, 1540), (13, 230), (12, 1550)]
 
 
-def arm(path):
+def arm(path, cases=None):
     import numpy as np
     import torch
 
     import paper_1902_04303_b200 as hg
 
     out = {}
-    for log_n, level in CASES:
+    for log_n, level in cases or CASES:
         params = hg.CkksParams(log_n=log_n, log_l=1700, log_p=45, log_p_small=30)
         sk, pk, evk, rot = hg.keygen(params, 3, device_rng=True)
         eng = hg.HeEngine(params, evk, rot)
@@ -39,17 +40,18 @@ def arm(path):
     np.savez(path, **out)
 
 
-def main():
-    if len(sys.argv) > 1:
-        arm(sys.argv[1])
-        return
+def compare(quick=False, workdir="/tmp"):
+    """Run both arms in subprocesses (HG_NO_FUSE is read once per process); returns the number
+    of output arrays that differ."""
     import numpy as np
 
     env = dict(os.environ)
-    subprocess.run([sys.executable, __file__, "/tmp/fused_on.npz"], check=True, env=env)
+    extra = ["--quick"] if quick else []
+    on_path, off_path = os.path.join(workdir, "fused_on.npz"), os.path.join(workdir, "fused_off.npz")
+    subprocess.run([sys.executable, __file__, on_path] + extra, check=True, env=env)
     env["HG_NO_FUSE"] = "1"
-    subprocess.run([sys.executable, __file__, "/tmp/fused_off.npz"], check=True, env=env)
-    on, off = np.load("/tmp/fused_on.npz"), np.load("/tmp/fused_off.npz")
+    subprocess.run([sys.executable, __file__, off_path] + extra, check=True, env=env)
+    on, off = np.load(on_path), np.load(off_path)
     bad = 0
     for k in off.files:
         d = on[k] != off[k]
@@ -69,6 +71,14 @@ def main():
         else:
             print(f"ok {k} {off[k].shape}")
     print("mismatching arrays:", bad)
+    return bad
+
+
+def main():
+    if len(sys.argv) > 1 and sys.argv[1] != "--quick":
+        arm(sys.argv[1], QUICK if "--quick" in sys.argv else None)
+        return
+    compare(quick="--quick" in sys.argv)
 
 
 if __name__ == "__main__":
