@@ -14,7 +14,8 @@ import threading
 from .errors import HegwasError, ParameterError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhegwas_b200.so")
+# HG_LIB_PATH: load an alternative build of the same C-ABI (kernel experiments)
+LIB_PATH = os.environ.get("HG_LIB_PATH") or os.path.join(_HERE, "libhegwas_b200.so")
 
 HG_OK = 0
 HG_EINVAL = 1
