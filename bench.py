@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--log-n", type=int, default=17)
     ap.add_argument("--log-l", type=int, default=1700)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-primitives", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -283,12 +284,59 @@ def run_ours(args, world, rank, local):
                "ms_per_step": round(1e3 * t_e2e / args.steps, 2)}
 
     peaks = probe_integer_peaks(ctx, torch)
+    prims = None if args.no_primitives else measure_primitives(torch, hg, _lib)
     return {
         "params": params, "tau": tau, "t_setup": t_setup, "t_steps": t_steps,
         "launches": launches, "kstats": kstats, "clocks": clocks.summary(), "e2e": e2e,
-        "peaks": peaks, "t_keys_inputs": t_keys_inputs,
+        "peaks": peaks, "t_keys_inputs": t_keys_inputs, "primitives": prims,
         "key_cache_gb": round(__import__("paper_1902_04303_b200.ckks", fromlist=["KEY_CACHE"]).KEY_CACHE.bytes / 1e9, 2),
     }
+
+
+def measure_primitives(torch, hg, _lib, log_n: int = 16, level: int = 1550, reps: int = 20):
+    """BASELINE's secondary metric: key switches / NTTs per second at N=2^16 (device-timed,
+    inputs resident).  Key switch = the relinearisation switch of a level-1550 ciphertext
+    (ModUp to the key basis, NTT, x.key fused into the inverse NTT, CRT window [L, L+l));
+    NTT = one length-2^16 negacyclic transform over one 30-bit prime (batches of 163 rows)."""
+    import ctypes  # noqa: F401
+    import numpy as np
+
+    from paper_1902_04303_b200 import ckks
+
+    params = hg.CkksParams(log_n=log_n, log_l=1700, log_p=45, log_p_small=30)
+    sk, pk, evk, rot = hg.keygen(params, 5, device_rng=True)
+    eng = hg.HeEngine(params, evk, rot)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(11)
+    v = np.random.default_rng(2).uniform(-1, 1, params.slot_count)
+    a = hg.mod_down(hg.encrypt_values(v, 45, pk, params, gen), level)
+    b = hg.mod_down(hg.encrypt_values(v[::-1], 45, pk, params, gen), level)
+    key = (evk.b, evk.a)
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(reps):
+            fn()
+        e.record()
+        torch.cuda.synchronize()
+        return s.elapsed_time(e) / 1e3 / reps
+
+    t_ks = timed(lambda: ckks._keyswitch(a.c1, key, level, params.log_l))
+    t_mult = timed(lambda: eng.mult(a, b))
+    t_rot = timed(lambda: eng.rotate(a, 1))
+    ctx = _lib.get_context(log_n)
+    rows = 163
+    buf = torch.randint(0, 1 << 20, (rows, params.n), dtype=torch.int32, device="cuda")
+    t_ntt = timed(lambda: _lib.check(ctx.lib.hg_ntt_forward(ctx.handle, buf.data_ptr(), rows, 0, ctx.stream())))
+    t_intt = timed(lambda: _lib.check(ctx.lib.hg_ntt_inverse(ctx.handle, buf.data_ptr(), rows, 0, ctx.stream())))
+    return {"N": params.n, "level_bits": level, "keyswitch_per_s": round(1 / t_ks, 1),
+            "ct_mult_rescale_per_s": round(1 / t_mult, 1), "rotation_per_s": round(1 / t_rot, 1),
+            "ntt_per_s": round(rows / t_ntt), "intt_per_s": round(rows / t_intt),
+            "ntt_butterflies_per_s": round(rows / t_ntt * (params.n // 2) * log_n / 1e9, 1),
+            "note": "device-timed, resident inputs; NTT = one length-N transform over one prime"}
 
 
 # ---------------------------------------------------------------------------------------------
@@ -415,6 +463,7 @@ def main():
                       "note": "config-3 end to end on device: setup once + 21 batch steps"},
         "e2e": r["e2e"], "gpu_launches": r["launches"], "roofline": roofline, "cpu_baseline": cpu,
         "clocks": r["clocks"], "int_peaks": {k: round(v / 1e9, 1) for k, v in r["peaks"].items()},
+        "primitives": r["primitives"],
         "key_cache_gb": r["key_cache_gb"], "prep_s": round(r["t_keys_inputs"], 1),
     }
     print(json.dumps(line), flush=True)
