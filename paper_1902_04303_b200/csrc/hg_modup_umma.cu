@@ -64,6 +64,9 @@ __device__ __forceinline__ T pick(const T (&a)[4], int k) {
     return k == 0 ? a[0] : k == 1 ? a[1] : k == 2 ? a[2] : a[3];
 }
 
+// SIGNED: some operand is two's complement (else the sign correction is compiled out);
+// AUTOMORPH: the gather runs through x -> x^k (else the negation correction is compiled out)
+template <bool SIGNED, bool AUTOMORPH>
 __global__ void __launch_bounds__(kWarps * 32, 1) modup_umma_kernel(
     MOps ops, int nops, int N, const PrimeInfo* __restrict__ pinfo,
     const uint32_t* __restrict__ modup_tab, const uint8_t* __restrict__ Bimg, int P,
@@ -278,10 +281,14 @@ __global__ void __launch_bounds__(kWarps * 32, 1) modup_umma_kernel(
                         r = min(r, r - 2 * p);
                         r = min(r, r - p);
                         // two's-complement sign: subtract 2^bits; automorphism sign: negate
-                        r += sgn ? cr.x : 0u;
-                        r = min(r, r - p);
-                        r = ng ? cr.y - r : r;   // < 2p
-                        r = min(r, r - p);
+                        if (SIGNED) {
+                            r += sgn ? cr.x : 0u;
+                            r = min(r, r - p);
+                        }
+                        if (AUTOMORPH) {
+                            r = ng ? cr.y - r : r;   // < 2p
+                            r = min(r, r - p);
+                        }
                         if (j < P) outp[(size_t)j * N] = r;
                     }
                 }
@@ -342,7 +349,10 @@ int hg_modup_umma_launch(hg_ctx* ctx, const uint32_t* const* words, const int* b
     if (rc) return -rc;
     static int nsm = 0;
     if (!nsm) {
-        if (cudaFuncSetAttribute(modup_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem) != cudaSuccess)
+        if (cudaFuncSetAttribute(modup_umma_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem) != cudaSuccess ||
+            cudaFuncSetAttribute(modup_umma_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem) != cudaSuccess ||
+            cudaFuncSetAttribute(modup_umma_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem) != cudaSuccess ||
+            cudaFuncSetAttribute(modup_umma_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem) != cudaSuccess)
             return -hg_fail(HG_ECUDA, "modup_umma smem attribute");
         if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device) != cudaSuccess)
             return -hg_fail(HG_ECUDA, "device attribute");
@@ -355,7 +365,11 @@ int hg_modup_umma_launch(hg_ctx* ctx, const uint32_t* const* words, const int* b
     }
     const int ntiles = nops * (ctx->N / kRows);
     const int grid = ntiles < nsm ? ntiles : nsm;
-    modup_umma_kernel<<<grid, kWarps * 32, kSmem, st>>>(o, nops, ctx->N, ctx->d_pinfo, ctx->d_modup,
+    bool any_signed = false;
+    for (int k = 0; k < nops; ++k) any_signed |= is_signed[k] != 0;
+    auto kern = any_signed ? (kinv ? modup_umma_kernel<true, true> : modup_umma_kernel<true, false>)
+                           : (kinv ? modup_umma_kernel<false, true> : modup_umma_kernel<false, false>);
+    kern<<<grid, kWarps * 32, kSmem, st>>>(o, nops, ctx->N, ctx->d_pinfo, ctx->d_modup,
                                                         ctx->d_modup_umma, P, out, kinv);
     ctx->launches.fetch_add(1, std::memory_order_relaxed);
     cudaError_t e = cudaGetLastError();
