@@ -68,6 +68,11 @@ int hg_poly_add(hg_ctx* ctx, uint32_t* out, const uint32_t* a, const uint32_t* b
 /* out = a - b mod 2^bits                                     RingElement.sub  ring.py:123 */
 int hg_poly_sub(hg_ctx* ctx, uint32_t* out, const uint32_t* a, const uint32_t* b,
                 int bits, void* stream);
+/* out = sum_k terms[k] mod 2^bits; `terms` is a HOST array of `count` device pointers.
+ * One pass over the terms (the sum of matrix.py's Sum_i mult(...) loops, e.g. cp_rep_matmul
+ * matrix.py:173-193, instead of count-1 pairwise adds); exact, so order-independent.    */
+int hg_poly_sum(hg_ctx* ctx, uint32_t* out, const uint32_t* const* terms, int count, int bits,
+                void* stream);
 /* out = -a mod 2^bits                                        RingElement.neg  ring.py:132 */
 int hg_poly_neg(hg_ctx* ctx, uint32_t* out, const uint32_t* a, int bits, void* stream);
 /* out = a * k mod 2^bits; k given as (k mod 2^bits) in kw host words (kw <= W)

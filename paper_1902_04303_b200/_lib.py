@@ -73,6 +73,7 @@ SIGNATURES = {
     "hg_bench_mac": (_i, [_vp, _i, _vp, ctypes.POINTER(ctypes.c_double), _vp]),
     "hg_launch_count": (ctypes.c_longlong, [_vp]),
     "hg_set_kernel_timing": (_i, [_vp, _i]),
+    "hg_poly_sum": (_i, [_vp, _vp, ctypes.POINTER(ctypes.c_void_p), _i, _i, _vp]),
     "hg_kernel_stats": (_i, [_vp, _i, ctypes.POINTER(ctypes.c_double),
                              ctypes.POINTER(ctypes.c_longlong), ctypes.POINTER(ctypes.c_double)]),
 }

@@ -184,6 +184,30 @@ __global__ void __launch_bounds__(kThreads) automorphism_kernel(uint32_t* __rest
     }
 }
 
+// out (+)= sum of up to kSumTerms polys: one thread per coefficient, 64-bit column sums with
+// the carry taken word to word; the loads of one word over all terms are independent
+constexpr int kSumTerms = 64;
+struct SumTerms {
+    const uint32_t* p[kSumTerms];
+};
+__global__ void __launch_bounds__(kThreads) sum_kernel(uint32_t* __restrict__ out, SumTerms t,
+                                                       int count, int accumulate, int W, int bits,
+                                                       int N) {
+    const int i = blockIdx.x * kThreads + threadIdx.x;
+    if (i >= N) return;
+    uint64_t carry = 0;
+    for (int w = 0; w < W; ++w) {
+        const size_t o = (size_t)w * N + i;
+        uint64_t acc = carry + (accumulate ? out[o] : 0u);
+#pragma unroll 8
+        for (int k = 0; k < count; ++k) acc += __ldg(t.p[k] + o);
+        uint32_t r = (uint32_t)acc;
+        if (w == W - 1) r &= mask_for(bits);
+        out[o] = r;
+        carry = acc >> 32;
+    }
+}
+
 inline dim3 grid_for(int N) { return dim3((N + kThreads - 1) / kThreads); }
 
 int64_t inv_mod_pow2(int64_t k, int64_t n2) {
@@ -244,6 +268,27 @@ extern "C" int hg_poly_sub(hg_ctx* ctx, uint32_t* out, const uint32_t* a, const 
                            int bits, void* stream) {
     HG_CHECK_ARGS(ctx && out && a && b && bits >= 1, "hg_poly_sub: bad arguments");
     return hg_ew_add(ctx, out, a, b, bits, true, (cudaStream_t)stream);
+}
+
+extern "C" int hg_poly_sum(hg_ctx* ctx, uint32_t* out, const uint32_t* const* terms, int count,
+                           int bits, void* stream) {
+    HG_CHECK_ARGS(ctx && out && terms && count >= 1 && bits >= 1, "hg_poly_sum: bad arguments");
+    const int W = words_for_bits(bits);
+    HgTimed tm(ctx, (cudaStream_t)stream, HG_K_ELEMENTWISE, (double)ctx->N);
+    for (int k0 = 0; k0 < count; k0 += kSumTerms) {
+        SumTerms t{};
+        const int c = count - k0 < kSumTerms ? count - k0 : kSumTerms;
+        for (int k = 0; k < c; ++k) {
+            HG_CHECK_ARGS(terms[k0 + k] != nullptr, "hg_poly_sum: null term");
+            // a later chunk reads `out` as its running sum, so no term may alias it
+            HG_CHECK_ARGS(terms[k0 + k] != out || k0 == 0, "hg_poly_sum: term aliases the output");
+            t.p[k] = terms[k0 + k];
+        }
+        sum_kernel<<<grid_for(ctx->N), kThreads, 0, (cudaStream_t)stream>>>(out, t, c, k0 > 0, W, bits,
+                                                                              ctx->N);
+        HG_LAUNCH_CHECK(ctx);
+    }
+    return HG_OK;
 }
 
 extern "C" int hg_poly_neg(hg_ctx* ctx, uint32_t* out, const uint32_t* a, int bits,

@@ -19,6 +19,7 @@ keys and ciphertexts generated from a ``random.Random`` are identical to the ref
 """
 from __future__ import annotations
 
+import ctypes
 import hashlib
 import math
 import random
@@ -211,6 +212,19 @@ class RingElement:
         ctx = _ctx(self.n)
         _lib.check(ctx.lib.hg_poly_add(ctx.handle, out.words.data_ptr(), self.words.data_ptr(),
                                        other.words.data_ptr(), self.mod_bits, ctx.stream()))
+        return out
+
+    @staticmethod
+    def sum(elements: "list[RingElement]") -> "RingElement":
+        """Exact sum mod 2^bits in one pass over the terms (== a fold of add)."""
+        first = elements[0]
+        for e in elements[1:]:
+            first._require_same(e)
+        out = first._new()
+        ctx = _ctx(first.n)
+        ptrs = (ctypes.c_void_p * len(elements))(*[e.words.data_ptr() for e in elements])
+        _lib.check(ctx.lib.hg_poly_sum(ctx.handle, out.words.data_ptr(), ptrs, len(elements),
+                                       first.mod_bits, ctx.stream()))
         return out
 
     def sub(self, other: "RingElement") -> "RingElement":
