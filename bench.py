@@ -262,12 +262,21 @@ def run_ours(args, world, rank, local):
         hbatch = HostSnpBatch.from_device(batch)
 
         def run_e2e(nsteps):
-            d2h = 0
+            # every step's 3 result ciphertexts are copied to pinned host memory asynchronously
+            # (stream-ordered after the step's kernels); the caller's synchronize() closes the
+            # timed region, so all reads complete inside it without a host stall per step
+            d2h, keep = 0, []
             for b in SnpBatchStream([hbatch] * nsteps, params):
                 out = compute_batch(engine, inputs, inter, m_dup, b)
                 res = [out.num_ct, out.den_even_ct, out.den_odd_ct]
-                host = [(c.c0.words.cpu(), c.c1.words.cpu()) for c in res]
-                d2h = sum(int(a.numel() + b.numel()) * 4 for a, b in host)
+                host = []
+                for c in res:
+                    for w in (c.c0.words, c.c1.words):
+                        h = torch.empty(w.shape, dtype=w.dtype, pin_memory=True)
+                        h.copy_(w, non_blocking=True)
+                        host.append(h)
+                keep.append((out, host))
+                d2h = sum(int(h.numel()) * 4 for h in host)
             return d2h
 
         run_e2e(1)

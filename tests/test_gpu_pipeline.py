@@ -104,3 +104,23 @@ def test_toy_pipeline_bit_exact(toy):
     assert np.array_equal(den, g.arr("den"))
     res = assemble_result(num, den)
     assert np.all(np.isfinite(res.effects[den > 0]))
+
+
+def test_toy_pipeline_streamed_batches_bit_exact(toy):
+    """The same pipeline with the SNP batches uploaded from pinned host memory by
+    SnpBatchStream (side-stream copies, per-row ready events, two device slots reused across
+    batches) reproduces the reference's per-batch outputs."""
+    import paper_1902_04303_b200 as hg
+    from paper_1902_04303_b200.gwas import HostSnpBatch, SnpBatchStream, compute_gwas_encrypted
+
+    g, params, (sk, pk, evk, rot), ds, config, seed = toy
+    enc = _golden_inputs(g, params, config)
+    host = [HostSnpBatch.from_device(b) for b in enc.batches]
+    # three passes over the batches so both device slots are reused while the next one loads
+    stream = SnpBatchStream(host * 3, params)
+    out = compute_gwas_encrypted(hg.HeEngine(params, evk, rot), enc, cache=stream)
+    assert len(out.batch_outputs) == 3 * len(host)
+    for bo in out.batch_outputs:
+        assert_ct_equal(bo.num_ct, g, f"out.b{bo.index}.num")
+        assert_ct_equal(bo.den_even_ct, g, f"out.b{bo.index}.den_even")
+        assert_ct_equal(bo.den_odd_ct, g, f"out.b{bo.index}.den_odd")
