@@ -22,6 +22,7 @@ from __future__ import annotations
 import ctypes
 import hashlib
 import math
+import os
 import random
 
 import numpy as np
@@ -89,7 +90,12 @@ def upload_words(arr: np.ndarray):
     if not arr.flags.writeable:
         arr = arr.copy()
     host = torch.from_numpy(arr.view(np.int32))
-    return host.to(_device(), non_blocking=False)
+    if not torch.cuda.is_available():
+        return host.to(_device())
+    # staged through pinned memory so the copy is stream-ordered instead of synchronising the
+    # host with the device (a pageable copy waits for all queued work); the caching host
+    # allocator keeps the staging block alive until the copy has run
+    return host.pin_memory().to(_device(), non_blocking=True)
 
 
 def download_words(t) -> np.ndarray:
