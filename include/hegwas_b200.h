@@ -138,6 +138,13 @@ int hg_ct_mult_prepared(hg_ctx* ctx, const hg_key* evk, const hg_ctprep* a, cons
  * keyswitch(phi_k(c1)).  Used by rotate (ckks.py:256-273) and conjugate (:276-279). */
 int hg_ct_automorph(hg_ctx* ctx, const hg_key* key, const uint32_t* c0, const uint32_t* c1,
                     int level, int64_t k, uint32_t* out0, uint32_t* out1, void* stream);
+/* `count` independent hg_ct_automorph calls with one key, exponent and level (host arrays of
+ * device pointers; outputs must not alias inputs): up to 4 rotations share each group of
+ * launches.  Used for the rotate-and-add ladders of many independent ciphertexts (matrix.py
+ * replicate / duplicate).  Results are identical to the one-by-one calls.            */
+int hg_ct_automorph_batch(hg_ctx* ctx, const hg_key* key, int count, const uint32_t* const* c0s,
+                          const uint32_t* const* c1s, int level, int64_t k,
+                          uint32_t* const* out0s, uint32_t* const* out1s, void* stream);
 
 /* ---- microbenchmarks / measurement ------------------------------------------------ */
 /* Batched forward+inverse negacyclic NTT over `count` length-N rows of residues

@@ -63,6 +63,8 @@ SIGNATURES = {
     "hg_keyswitch": (_i, [_vp, _vp, _vp, _i64, _vp, _vp, _vp]),
     "hg_ct_mult": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _vp, _vp, _vp]),
     "hg_ct_automorph": (_i, [_vp, _vp, _vp, _vp, _i, _i64, _vp, _vp, _vp]),
+    "hg_ct_automorph_batch": (_i, [_vp, _vp, _i, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _i, _i64,
+                                   ctypes.POINTER(_vp), ctypes.POINTER(_vp), _vp]),
     "hg_ct_prepare": (_i, [_vp, _vp, _vp, _i, _vp, ctypes.POINTER(_vp)]),
     "hg_ctprep_destroy": (_i, [_vp]),
     "hg_ctprep_device_bytes": (ctypes.c_size_t, [_vp]),

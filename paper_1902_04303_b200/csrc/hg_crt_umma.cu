@@ -37,9 +37,15 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     }
 }
 
+constexpr int kMaxOuts = 8;   // outputs per launch (the pipelined kernel; older kernels take 4)
 struct UOuts {
-    uint32_t* out[4];
+    uint32_t* out[kMaxOuts];
 };
+// select, not index: a dynamic index into the parameter struct would copy it to the stack
+__device__ __forceinline__ uint32_t* pick_out(const UOuts& o, int k) {
+    return k == 0 ? o.out[0] : k == 1 ? o.out[1] : k == 2 ? o.out[2] : k == 3 ? o.out[3]
+         : k == 4 ? o.out[4] : k == 5 ? o.out[5] : k == 6 ? o.out[6] : o.out[7];
+}
 
 // exact column scan for one coefficient (rare fallback when the truncated carry window is
 // ambiguous); y_j read back from the A tile (row n, byte 4j)
@@ -708,8 +714,9 @@ __global__ void __launch_bounds__(PipeCfg<FUSED>::kWarps * 32, 1) crt_umma_pipe_
           for (int h = 0; h < jpt; ++h, ++ij) {
             if ((ij & 1) != grp) continue;
             const int oy = tile / tpo, cb = (tile - oy * tpo) * kRows;
-            uint32_t* out = oy == 0 ? outs.out[0] : oy == 1 ? outs.out[1] : oy == 2 ? outs.out[2] : outs.out[3];
-            const uint32_t* addp = oy == 0 ? fin.add[0] : oy == 1 ? fin.add[1] : oy == 2 ? fin.add[2] : fin.add[3];
+            uint32_t* out = pick_out(outs, oy);
+            const uint32_t* addp = oy < 4 ? (oy == 0 ? fin.add[0] : oy == 1 ? fin.add[1] : oy == 2 ? fin.add[2] : fin.add[3])
+                                          : nullptr;
             const int i = cb + n;
             Emitter em;
             em.init(out, N, i, out_bits, fin, FUSED ? addp : nullptr);

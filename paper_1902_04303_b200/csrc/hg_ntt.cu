@@ -326,11 +326,15 @@ __global__ void __launch_bounds__(256) ntt_hi8_kernel(uint32_t* __restrict__ dat
 template <int PRE>
 struct PreRows { static constexpr int value = PRE == 1 ? 2 : (PRE == 2 ? 3 : 1); };
 
+// blockIdx.y selects one of a batch of independent products sharing in1..in3 (PRE 1: several
+// key switches with one key): in0 advances by bstride_in words, out by bstride_out
 template <int K2, int PRE>
 __global__ void __launch_bounds__(256) intt_lo8_fused_kernel(
     uint32_t* out, const uint32_t* in0, const uint32_t* in1, const uint32_t* in2,
     const uint32_t* in3, int log_n, int P, const PrimeInfo* __restrict__ pinfo,
-    const uint2* __restrict__ tw) {
+    const uint2* __restrict__ tw, size_t bstride_in, size_t bstride_out) {
+    out += blockIdx.y * bstride_out;
+    in0 += blockIdx.y * bstride_in;
     constexpr int RB = PreRows<PRE>::value;
     __shared__ __align__(16) uint32_t sm[2 * RB * kSmRow];
     const int N = 1 << log_n;
@@ -381,13 +385,13 @@ __global__ void __launch_bounds__(256) intt_lo8_fused_kernel(
 template <int PRE>
 int launch_fused_lo8(int k2, dim3 grid, cudaStream_t st, uint32_t* out, const uint32_t* i0,
                      const uint32_t* i1, const uint32_t* i2, const uint32_t* i3, int log_n, int P,
-                     const PrimeInfo* pinfo, const uint2* tw) {
+                     const PrimeInfo* pinfo, const uint2* tw, size_t bsi = 0, size_t bso = 0) {
     const int threads = (1 << k2) / 8;
     switch (k2) {
 #define HG_LOF(K)                                                                               \
     case K:                                                                                     \
         intt_lo8_fused_kernel<K, PRE><<<grid, threads, 0, st>>>(out, i0, i1, i2, i3, log_n, P,  \
-                                                                pinfo, tw);                     \
+                                                                pinfo, tw, bsi, bso);           \
         return 0;
         HG_LOF(3) HG_LOF(4) HG_LOF(5) HG_LOF(6) HG_LOF(7) HG_LOF(8) HG_LOF(9) HG_LOF(10) HG_LOF(11)
 #undef HG_LOF
@@ -503,7 +507,7 @@ int hg_ntt_launch(hg_ctx* ctx, uint32_t* data, int rows, int P, int prime_offset
 // RB = 2 / 3 / 1 rows [RB][P][N] for pre = 1 / 2 / 3.  Returns -1 if the shape is not covered
 // (the caller then runs the separate pointwise kernel + hg_ntt_launch).
 int hg_intt_fused(hg_ctx* ctx, int pre, uint32_t* out, const uint32_t* i0, const uint32_t* i1,
-                  const uint32_t* i2, const uint32_t* i3, int P, cudaStream_t st) {
+                  const uint32_t* i2, const uint32_t* i3, int P, cudaStream_t st, int batch) {
     const int log_n = ctx->log_n, N = ctx->N;
     if (log_n < 3 || P > 65535) return -1;
     int rc = hg_ensure_twiddles(ctx, P);
@@ -511,13 +515,16 @@ int hg_intt_fused(hg_ctx* ctx, int pre, uint32_t* out, const uint32_t* i0, const
     const int k1 = log_n <= 11 ? 0 : (log_n <= 14 ? 3 : 6);
     const int k2 = log_n - k1;
     const int rb = pre == 1 ? 2 : (pre == 2 ? 3 : 1);
-    HgTimed tm(ctx, st, HG_K_NTT, (double)rb * P * (N / 2) * log_n);
-    const dim3 g(N >> k2, 1, P);
-    if (pre == 1) launch_fused_lo8<1>(k2, g, st, out, i0, i1, i2, i3, log_n, P, ctx->d_pinfo, ctx->d_tw_inv);
+    if (batch < 1 || (batch > 1 && pre != 1) || batch > 65535) return -1;
+    HgTimed tm(ctx, st, HG_K_NTT, (double)batch * rb * P * (N / 2) * log_n);
+    // batch > 1 (key switch only): input g's x rows at i0 + g P N, its two outputs at out + g 2 P N
+    const dim3 g(N >> k2, batch, P);
+    const size_t bsi = (size_t)P * N, bso = (size_t)rb * P * N;
+    if (pre == 1) launch_fused_lo8<1>(k2, g, st, out, i0, i1, i2, i3, log_n, P, ctx->d_pinfo, ctx->d_tw_inv, bsi, bso);
     else if (pre == 2) launch_fused_lo8<2>(k2, g, st, out, i0, i1, i2, i3, log_n, P, ctx->d_pinfo, ctx->d_tw_inv);
     else launch_fused_lo8<3>(k2, g, st, out, i0, i1, i2, i3, log_n, P, ctx->d_pinfo, ctx->d_tw_inv);
     HG_LAUNCH_CHECK(ctx);
-    if (k1) return ntt_pass<false>(ctx, true, k1, k2, out, rb, P, 0, ctx->d_tw_inv, st);
+    if (k1) return ntt_pass<false>(ctx, true, k1, k2, out, batch * rb, P, 0, ctx->d_tw_inv, st);
     return HG_OK;
 }
 

@@ -22,7 +22,7 @@ int hg_ew_divide_round(hg_ctx* ctx, uint32_t* out, int out_bits, const uint32_t*
 int hg_ew_automorphism(hg_ctx* ctx, uint32_t* out, const uint32_t* a, int bits, int64_t k,
                        cudaStream_t stream);
 int hg_intt_fused(hg_ctx* ctx, int pre, uint32_t* out, const uint32_t* i0, const uint32_t* i1,
-                  const uint32_t* i2, const uint32_t* i3, int P, cudaStream_t st);
+                  const uint32_t* i2, const uint32_t* i3, int P, cudaStream_t st, int batch = 1);
 // pointwise product fused into the inverse NTT unless HG_NO_FUSE is set (A/B checks)
 static bool fuse_pointwise() {
     static const bool on = getenv("HG_NO_FUSE") == nullptr;
@@ -40,7 +40,7 @@ struct OperandSet {
     int is_signed[4];
 };
 struct OutSet {
-    uint32_t* out[4];
+    uint32_t* out[8];   // up to 8 through the pipelined CRT; the older kernels take 4 per launch
 };
 
 // ---- ModUp ---------------------------------------------------------------------------------
@@ -467,6 +467,13 @@ int launch_crt(hg_ctx* ctx, const uint32_t* res, int nouts, int P, int shift, in
                                        finish);
     }
     if (finish) return hg_fail(HG_EINVAL, "fused CRT finish needs the pipelined kernel");
+    if (nouts > 4) {   // the older kernels take 4 outputs per launch
+        OutSet lo{}, hi{};
+        for (int k = 0; k < 4; ++k) lo.out[k] = outs.out[k];
+        for (int k = 4; k < nouts; ++k) hi.out[k - 4] = outs.out[k];
+        if ((rc = launch_crt(ctx, res, 4, P, shift, out_bits, lo, st))) return rc;
+        return launch_crt(ctx, res + (size_t)4 * P * N, nouts - 4, P, shift, out_bits, hi, st);
+    }
     if (N >= 128 && !getenv("HG_NO_UMMA") && !getenv("HG_NO_MMA") &&
         hg_crt_umma_smem(tab->P32) <= 220 * 1024) {
         // tcgen05 path (UTCIMMA, accumulators in TMEM)
@@ -881,4 +888,62 @@ extern "C" int hg_ct_automorph(hg_ctx* ctx, const hg_key* key, const uint32_t* c
     rc = hg_keyswitch(ctx, key, c1, k, e0, out1, stream);
     if (rc) return rc;
     return hg_ew_add(ctx, out0, a0, e0, level, false, st);
+}
+
+// `count` rotations by the same automorphism and key at one level, up to 4 per group of
+// launches: one ModUp of the 4 c1 gathers, one forward NTT over [4][P][N] (twiddle loads
+// shared by the rows of a prime), one batched key product fused into the inverse NTT and one
+// 8-output CRT -- instead of 4 separate chains.  Each output is identical to hg_ct_automorph's.
+extern "C" int hg_ct_automorph_batch(hg_ctx* ctx, const hg_key* key, int count,
+                                     const uint32_t* const* c0s, const uint32_t* const* c1s,
+                                     int level, int64_t k, uint32_t* const* out0s,
+                                     uint32_t* const* out1s, void* stream) {
+    if (!ctx || !key || key->level != level || count < 0 || (count && (!c0s || !c1s || !out0s || !out1s)))
+        return hg_fail(HG_EINVAL, "hg_ct_automorph_batch: bad arguments (key must be prepared at the level)");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int N = ctx->N;
+    const int W = words_for_bits(level);
+    const int P = key->P;
+    const int64_t n2 = 2ll * N;
+    const int64_t kk = ((k % n2) + n2) % n2;
+    if ((kk & 1) == 0) return hg_fail(HG_EINVAL, "automorphism exponent must be odd");
+    const int64_t kinv = kk == 1 ? 0 : inverse_mod_2n(kk, n2);
+    int rc;
+    for (int g0 = 0; g0 < count; g0 += 4) {
+        const int G = count - g0 < 4 ? count - g0 : 4;
+        if (G == 1 || !fuse_pointwise()) {
+            for (int g = 0; g < G; ++g)
+                if ((rc = hg_ct_automorph(ctx, key, c0s[g0 + g], c1s[g0 + g], level, k, out0s[g0 + g],
+                                          out1s[g0 + g], stream)))
+                    return rc;
+            continue;
+        }
+        for (int g = 0; g < G; ++g)
+            if (out0s[g0 + g] == c0s[g0 + g] || out0s[g0 + g] == c1s[g0 + g])
+                return hg_fail(HG_EINVAL, "hg_ct_automorph_batch: outputs must not alias inputs");
+        Scratch res(st), buf(st);
+        HG_CUDA_TRY(res.alloc((size_t)3 * G * P * N * 4));   // x residues [G][P][N], products [G][2][P][N]
+        HG_CUDA_TRY(buf.alloc((size_t)2 * G * W * N * 4));   // automorphed c0 and key-switch e0 per item
+        OperandSet ops{};
+        for (int g = 0; g < G; ++g) {
+            ops.words[g] = c1s[g0 + g]; ops.bits[g] = level; ops.is_signed[g] = 0;   // canonical rep
+        }
+        if ((rc = launch_modup(ctx, ops, G, P, res.u32(), kinv, st))) return rc;
+        if ((rc = hg_ntt_launch(ctx, res.u32(), G * P, P, 0, true, st))) return rc;
+        uint32_t* t = res.u32() + (size_t)G * P * N;
+        rc = hg_intt_fused(ctx, 1, t, res.u32(), key->d_kb, key->d_ka, nullptr, P, st, G);
+        if (rc) return rc < 0 ? hg_fail(HG_EINVAL, "batched key product not available") : rc;
+        OutSet outs{};
+        for (int g = 0; g < G; ++g) {
+            outs.out[2 * g] = buf.u32() + (size_t)(2 * g + 1) * W * N;   // e0_g
+            outs.out[2 * g + 1] = out1s[g0 + g];
+        }
+        if ((rc = launch_crt(ctx, t, 2 * G, P, key->big_l, level, outs, st))) return rc;
+        for (int g = 0; g < G; ++g) {
+            uint32_t* a0 = buf.u32() + (size_t)(2 * g) * W * N;
+            if ((rc = hg_ew_automorphism(ctx, a0, c0s[g0 + g], level, k, st))) return rc;
+            if ((rc = hg_ew_add(ctx, out0s[g0 + g], a0, outs.out[2 * g], level, false, st))) return rc;
+        }
+    }
+    return HG_OK;
 }

@@ -77,7 +77,7 @@ def run_pass(eng, inputs):
     with T("z' = M z"):
         zp = gwas.orthogonalize_z(eng, m, z)
     with T("m_dup"):
-        m_dup = [matrix.duplicate(eng, col, 256) for col in m.cols]
+        m_dup = matrix.duplicate_many(eng, m.cols, 256)
     print("levels: beta", beta.level_bits, "p", p_prev.level_bits, "w", w.level_bits, "w_inv", w_inv.level_bits,
           "z", z.level_bits, "M", m.cols[0].level_bits, "z'", zp.level_bits, "m_dup", m_dup[0].level_bits)
 
