@@ -348,6 +348,29 @@ def measure_primitives(torch, hg, _lib, log_n: int = 16, level: int = 1550, reps
             "note": "device-timed, resident inputs; NTT = one length-N transform over one prime"}
 
 
+def ncu_traffic(dom: str):
+    """DRAM bytes per unit of the dominant kernel from the committed `ncu --set full` capture
+    (profiles/r1_ncu_traffic.json): per row-pass of the contiguous NTT pass (the largest NTT
+    launch), against its algorithmic read+write of 2^17 words."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_ncu_traffic.json")) as f:
+            cap = json.load(f)
+    except OSError:
+        return None
+    if dom != "ntt":
+        return None
+    for ln in cap["launches"]:
+        if ln["kernel"].startswith("void ntt_lo8_kernel<1, 11, 2>"):
+            rows = int(ln["grid_size"]) // 32   # 64 chunks x 2-row blocks per prime: 32 blocks/row
+            scale = {"Mbyte": 1e6, "Gbyte": 1e9, "Kbyte": 1e3}.get(ln["unit"], 1.0)
+            per_row = (ln["dram_read"] + ln["dram_write"]) * scale / rows
+            return {"bytes_per_row_pass": round(per_row), "algorithmic_bytes_per_row_pass": 2 * (1 << 17) * 4,
+                    "ratio": round(per_row / (2 * (1 << 17) * 4), 3),
+                    "source": "profiles/r1_ncu_traffic.json (ncu --set full, ntt_lo8_kernel<1,11,2>, "
+                              f"{rows} rows); the excess over 1.0 is the twiddle table"}
+    return None
+
+
 # ---------------------------------------------------------------------------------------------
 def cpu_mult_sample(log_n: int, level: int, big_l: int, log_p: int, seed: int = 0):
     """Time one HeEngine.mult at (N, level) with the CPU oracle port (gmp-backed exact
@@ -443,7 +466,7 @@ def main():
         "achieved": round(achieved / 1e9, 1), "peak": round(r["peaks"][peak_key] / 1e9, 1),
         "unit": "G" + ("butterflies" if dom == "ntt" else "MAC") + "/s",
         "frac": round(achieved / r["peaks"][peak_key], 4) if r["peaks"][peak_key] else None,
-        "traffic": None,
+        "traffic": ncu_traffic(dom),
         "peak_source": "measured in-run: register-resident probe of the kernel's own instruction mix "
                        "(MEASURED_PEAKS.json has no integer-pipe figure)",
         "share_of_step": round(ks[dom]["ms"] / step_ms_total, 3) if step_ms_total else None,
