@@ -441,13 +441,15 @@ __device__ void pipe_rescan_exact(const uint32_t* __restrict__ r, int P, int N, 
                                   const double* __restrict__ invp,
                                   const uint32_t* __restrict__ Mtab,
                                   const uint32_t* __restrict__ negQ, int shift, int out_bits,
-                                  Emitter em) {
+                                  bool prescaled, Emitter em) {
     const int i = em.i;
+    // prescaled residues already carry the factor (Q/p_j)^-1 N^-1 2^32 and sit in [0, 2p)
+    auto yj = [&](int j) {
+        const uint32_t p = pinfo[j].p, x = r[(size_t)j * N + i];
+        return reduce_2p(prescaled ? x : mul_shoup_lazy(x, cinv[j], cinv_sh[j], p), p);
+    };
     double S = 0.0;
-    for (int j = 0; j < P; ++j) {
-        const uint32_t p = pinfo[j].p;
-        S += (double)reduce_2p(mul_shoup_lazy(r[(size_t)j * N + i], cinv[j], cinv_sh[j], p), p) * invp[j];
-    }
+    for (int j = 0; j < P; ++j) S += (double)yj(j) * invp[j];
     const uint32_t v = (uint32_t)floor(S + 0.5);
     const int sw = shift >> 5, sb = shift & 31;
     const int out_w = (out_bits + 31) >> 5;
@@ -462,9 +464,7 @@ __device__ void pipe_rescan_exact(const uint32_t* __restrict__ r, int P, int N, 
         uint64_t top = (carry >> 32) + (x >> 32);
         uint64_t acc = (uint32_t)x;
         for (int j = 0; j < P; ++j) {
-            const uint32_t p = pinfo[j].p;
-            const uint32_t y = reduce_2p(mul_shoup_lazy(r[(size_t)j * N + i], cinv[j], cinv_sh[j], p), p);
-            acc += (uint64_t)y * Mtab[(size_t)j * W + t];
+            acc += (uint64_t)yj(j) * Mtab[(size_t)j * W + t];
             top += acc >> 32;
             acc &= 0xffffffffull;
         }
@@ -480,7 +480,10 @@ __device__ void pipe_rescan_exact(const uint32_t* __restrict__ r, int P, int N, 
     (void)top_mask;
 }
 
-template <bool FUSED>
+// PRESCALED: the residues were produced from operands pre-multiplied by the per-prime CRT
+// constant (hg_key / hg_ctprep prepared for this window), so y_j = x_j mod p_j is one
+// conditional subtraction instead of a Shoup product
+template <bool FUSED, bool PRESCALED>
 __global__ void __launch_bounds__(PipeCfg<FUSED>::kWarps * 32, 1) crt_umma_pipe_kernel(
     const __grid_constant__ CUtensorMap res_map, const __grid_constant__ CUtensorMap add_map,
     const uint32_t* __restrict__ res, int P, int P32p, int N, int nouts,
@@ -504,14 +507,17 @@ __global__ void __launch_bounds__(PipeCfg<FUSED>::kWarps * 32, 1) crt_umma_pipe_
     __shared__ uint4 s_hand[2][kRows];             // carry lo/hi, previous word, ambiguity
     __shared__ uint2 s_hand2[2][kRows];            // emitter state: carry, previous word
     __shared__ uint32_t tmem_base;
-    __shared__ uint4 s_pc[HG_MAX_PRIMES + 32];     // p, cinv, cinv_sh, floor(2^53/p) (1,0,0,0 padding)
+    // p, cinv, cinv_sh, floor(2^53/p) (1,0,0,0 padding); PRESCALED: p, ~0, 0, floor(2^53/p)
+    __shared__ uint4 s_pc[HG_MAX_PRIMES + 32];
     __shared__ uint64_t s_acc[2][kRows];
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     for (int j = tid; j < P32p; j += blockDim.x) {
         const bool ok = j < P;
         const uint32_t p = ok ? pinfo[j].p : 1u;
-        s_pc[j] = ok ? make_uint4(p, cinv[j], cinv_sh[j], (uint32_t)((1ull << 53) / p)) : make_uint4(1u, 0u, 0u, 0u);
+        s_pc[j] = !ok ? make_uint4(1u, 0u, 0u, 0u)
+              : PRESCALED ? make_uint4(p, 0xffffffffu, 0u, (uint32_t)((1ull << 53) / p))
+                          : make_uint4(p, cinv[j], cinv_sh[j], (uint32_t)((1ull << 53) / p));
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base)), "n"(512));
@@ -665,9 +671,10 @@ __global__ void __launch_bounds__(PipeCfg<FUSED>::kWarps * 32, 1) crt_umma_pipe_
                 if (lane == 0) mbar_arrive(smem_u32(&bar_res_empty[s]));
 #pragma unroll
                 for (int u = 0; u < 16; ++u) {
-                    // padding primes: x is stale but cinv = 0 gives y = 0
+                    // padding primes: x is stale but cinv = 0 (PRESCALED: mask 0) gives y = 0
                     const uint4 pc = s_pc[j0 + u];
-                    y[u] = reduce_2p(mul_shoup_lazy(y[u], pc.y, pc.z, pc.x), pc.x);
+                    y[u] = PRESCALED ? reduce_2p(y[u] & pc.y, pc.x)
+                                     : reduce_2p(mul_shoup_lazy(y[u], pc.y, pc.z, pc.x), pc.x);
                     acc += (uint64_t)y[u] * pc.w;
                 }
                 if (kc == nkc - 1) {
@@ -803,7 +810,7 @@ __global__ void __launch_bounds__(PipeCfg<FUSED>::kWarps * 32, 1) crt_umma_pipe_
                 Emitter fresh;
                 fresh.init(out, N, i, out_bits, fin, FUSED ? addp : nullptr);
                 pipe_rescan_exact(res + (size_t)oy * P * N, P, N, W, pinfo, cinv, cinv_sh, invp, Mtab,
-                                  negQ, shift, out_bits, fresh);
+                                  negQ, shift, out_bits, PRESCALED, fresh);
             }
         }
     }
@@ -825,13 +832,17 @@ bool hg_crt_umma_pipe_ok(const CrtTable* tab, int N, int shift, int out_bits, in
 
 int hg_crt_umma_pipe_launch(hg_ctx* ctx, const CrtTable* tab, const uint32_t* res, int nouts, int P,
                             int shift, int out_bits, int tb0, uint32_t* const* outs_in,
-                            cudaStream_t st, const CrtFinish* finish) {
+                            cudaStream_t st, const CrtFinish* finish, bool prescaled) {
     static int nsm = 0;
     if (!nsm) {
-        HG_CUDA_TRY(cudaFuncSetAttribute(crt_umma_pipe_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)pipe_smem<false>()));
-        HG_CUDA_TRY(cudaFuncSetAttribute(crt_umma_pipe_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)pipe_smem<true>()));
+        HG_CUDA_TRY(cudaFuncSetAttribute(crt_umma_pipe_kernel<false, false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pipe_smem<false>()));
+        HG_CUDA_TRY(cudaFuncSetAttribute(crt_umma_pipe_kernel<false, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pipe_smem<false>()));
+        HG_CUDA_TRY(cudaFuncSetAttribute(crt_umma_pipe_kernel<true, false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pipe_smem<true>()));
+        HG_CUDA_TRY(cudaFuncSetAttribute(crt_umma_pipe_kernel<true, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pipe_smem<true>()));
         HG_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device));
     }
     UOuts o{};
@@ -851,11 +862,13 @@ int hg_crt_umma_pipe_launch(hg_ctx* ctx, const CrtTable* tab, const uint32_t* re
         if (int rc = hg_tmap_2d_u32(&add_map, fin.add[0], (uint64_t)ctx->N, (uint64_t)nouts * out_w, kRows,
                                     kJobCols))
             return rc;
-        crt_umma_pipe_kernel<true><<<grid, PipeCfg<true>::kWarps * 32, pipe_smem<true>(), st>>>(
+        auto kern = prescaled ? crt_umma_pipe_kernel<true, true> : crt_umma_pipe_kernel<true, false>;
+        kern<<<grid, PipeCfg<true>::kWarps * 32, pipe_smem<true>(), st>>>(
             res_map, add_map, res, P, tab->P32p, ctx->N, nouts, ctx->d_pinfo, tab->d_Bpipe, tab->d_M, tab->W,
             tab->d_negQ, tab->d_cinv, tab->d_cinv_sh, tab->d_invp, shift, out_bits, tb0, o, fin);
     } else {
-        crt_umma_pipe_kernel<false><<<grid, PipeCfg<false>::kWarps * 32, pipe_smem<false>(), st>>>(
+        auto kern = prescaled ? crt_umma_pipe_kernel<false, true> : crt_umma_pipe_kernel<false, false>;
+        kern<<<grid, PipeCfg<false>::kWarps * 32, pipe_smem<false>(), st>>>(
             res_map, res_map, res, P, tab->P32p, ctx->N, nouts, ctx->d_pinfo, tab->d_Bpipe, tab->d_M, tab->W,
             tab->d_negQ, tab->d_cinv, tab->d_cinv_sh, tab->d_invp, shift, out_bits, tb0, o, fin);
     }

@@ -111,6 +111,9 @@ struct hg_key {
     uint32_t* d_kb = nullptr;   // [P][N] NTT residues of kb mod 2^(l+L) (centered), in [0,p)
     uint32_t* d_ka = nullptr;
     size_t bytes = 0;
+    // residues pre-multiplied by the key switch CRT constants (Q/p_j)^-1 N^-1 2^32: the
+    // pipelined CRT then skips that product (set when that kernel covers the window)
+    bool prescaled = false;
 };
 
 // ---- error plumbing ------------------------------------------------------------------
@@ -160,7 +163,7 @@ struct CrtFinish {
 };
 int hg_crt_umma_pipe_launch(hg_ctx* ctx, const CrtTable* tab, const uint32_t* res, int nouts, int P,
                             int shift, int out_bits, int tb0, uint32_t* const* outs,
-                            cudaStream_t st, const CrtFinish* finish = nullptr);
+                            cudaStream_t st, const CrtFinish* finish = nullptr, bool prescaled = false);
 int hg_modup_umma_launch(hg_ctx* ctx, const uint32_t* const* words, const int* bits,
                          const int* is_signed, int nops, int P, uint32_t* out, int64_t kinv,
                          cudaStream_t st);

@@ -252,6 +252,18 @@ __global__ void reduce_rows_kernel(uint32_t* __restrict__ a, int N,
         a[off + i] = reduce_4p(a[off + i], p);
 }
 
+// rows [z][P][N] (any 32-bit residues) -> x * c_j mod p_j in [0, p): folds the CRT constant
+// c_j = (Q/p_j)^-1 N^-1 2^32 into a resident operand (the product and the inverse NTT are
+// linear, so the CRT input arrives already multiplied by it)
+__global__ void scale_rows_kernel(uint32_t* __restrict__ a, int P, int N, const PrimeInfo* __restrict__ pinfo,
+                                  const uint32_t* __restrict__ c, const uint32_t* __restrict__ c_sh) {
+    const int j = blockIdx.y;
+    const uint32_t p = pinfo[j].p, w = c[j], wsh = c_sh[j];
+    const size_t off = ((size_t)blockIdx.z * P + j) * N;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x)
+        a[off + i] = reduce_2p(mul_shoup_lazy(a[off + i], w, wsh, p), p);
+}
+
 // ---- CRT reconstruction -----------------------------------------------------------------------
 // Exact c = sum_j y_j Q/p_j - v Q with y_j = r_j (Q/p_j)^-1 N^-1 2^32 mod p_j and
 // v = round(sum_j y_j / p_j) (|c| < Q/8 by the prime-count margin, so the float64 estimate
@@ -447,8 +459,30 @@ bool crt_finish_ok(hg_ctx* ctx, int P, int shift, int out_bits) {
     return hg_crt_umma_pipe_ok(tab, ctx->N, shift, out_bits, crt_tb0(shift));
 }
 
+// true when the residues of this window may arrive prescaled (see scale_rows_kernel): the
+// fused key/tensor product feeds the pipelined CRT
+bool crt_prescale_ok(hg_ctx* ctx, int P, int shift, int out_bits) {
+    if (!crt_pipe_enabled(ctx) || !fuse_pointwise() || getenv("HG_NO_PRESCALE")) return false;
+    const CrtTable* tab = nullptr;
+    if (hg_get_crt(ctx, P, &tab)) return false;
+    return hg_crt_umma_pipe_ok(tab, ctx->N, shift, out_bits, crt_tb0(shift));
+}
+
+dim3 pw_grid(int N, int rows);
+
+int prescale_rows(hg_ctx* ctx, uint32_t* rows, int nrows, int P, cudaStream_t st) {
+    const CrtTable* tab = nullptr;
+    if (int rc = hg_get_crt(ctx, P, &tab)) return rc;
+    dim3 grid = pw_grid(ctx->N, P);
+    grid.z = nrows;
+    scale_rows_kernel<<<grid, 256, 0, st>>>(rows, P, ctx->N, ctx->d_pinfo, tab->d_cinv, tab->d_cinv_sh);
+    HG_LAUNCH_CHECK(ctx);
+    return HG_OK;
+}
+
 int launch_crt(hg_ctx* ctx, const uint32_t* res, int nouts, int P, int shift, int out_bits,
-               const OutSet& outs, cudaStream_t st, const CrtFinish* finish = nullptr) {
+               const OutSet& outs, cudaStream_t st, const CrtFinish* finish = nullptr,
+               bool prescaled = false) {
     const CrtTable* tab = nullptr;
     int rc = hg_get_crt(ctx, P, &tab);
     if (rc) return rc;
@@ -464,9 +498,10 @@ int launch_crt(hg_ctx* ctx, const uint32_t* res, int nouts, int P, int shift, in
         // persistent warp-specialised tcgen05 path
         HgTimed tm(ctx, st, HG_K_CRT, (double)nouts * N * (double)P * (T - tb0));
         return hg_crt_umma_pipe_launch(ctx, tab, res, nouts, P, shift, out_bits, tb0, outs.out, st,
-                                       finish);
+                                       finish, prescaled);
     }
     if (finish) return hg_fail(HG_EINVAL, "fused CRT finish needs the pipelined kernel");
+    if (prescaled) return hg_fail(HG_EINVAL, "prescaled CRT residues need the pipelined kernel");
     if (nouts > 4) {   // the older kernels take 4 outputs per launch
         OutSet lo{}, hi{};
         for (int k = 0; k < 4; ++k) lo.out[k] = outs.out[k];
@@ -645,7 +680,10 @@ extern "C" int hg_key_prepare(hg_ctx* ctx, const uint32_t* kb, const uint32_t* k
     ops.words[1] = ka; ops.bits[1] = kbits; ops.is_signed[1] = 1;
     int rc = launch_modup(ctx, ops, 2, P, key->d_kb, 0, st);
     if (!rc) rc = hg_ntt_launch(ctx, key->d_kb, 2 * P, P, 0, true, st);
-    if (!rc) {
+    if (!rc && crt_prescale_ok(ctx, P, big_l, level)) {
+        rc = prescale_rows(ctx, key->d_kb, 2, P, st);   // d_ka follows d_kb
+        key->prescaled = rc == HG_OK;
+    } else if (!rc) {
         reduce_rows_kernel<<<pw_grid(N, P), 256, 0, st>>>(key->d_kb, N, ctx->d_pinfo);
         ctx->launches++;
         reduce_rows_kernel<<<pw_grid(N, P), 256, 0, st>>>(key->d_ka, N, ctx->d_pinfo);
@@ -722,7 +760,7 @@ static int keyswitch_impl(hg_ctx* ctx, const hg_key* key, const uint32_t* x, int
     }
     OutSet outs{};
     outs.out[0] = out0; outs.out[1] = out1;
-    return launch_crt(ctx, t, 2, P, key->big_l, key->level, outs, st, fin);
+    return launch_crt(ctx, t, 2, P, key->big_l, key->level, outs, st, fin, key->prescaled);
 }
 
 // ---- fused scheme ops ------------------------------------------------------------------------------
@@ -780,6 +818,7 @@ struct hg_ctprep {
     int P = 0;
     uint32_t* d_res = nullptr;   // [2][P][N] forward-NTT residues of c0, c1 (centered reps)
     size_t bytes = 0;
+    bool prescaled = false;      // residues carry the tensor CRT constants (scale_rows_kernel)
 };
 
 static int tensor_primes(hg_ctx* ctx, int level) {
@@ -808,6 +847,10 @@ extern "C" int hg_ct_prepare(hg_ctx* ctx, const uint32_t* c0, const uint32_t* c1
     ops.words[1] = c1; ops.bits[1] = level; ops.is_signed[1] = 1;
     int rc = launch_modup(ctx, ops, 2, P, pr->d_res, 0, st);
     if (!rc) rc = hg_ntt_launch(ctx, pr->d_res, 2 * P, P, 0, true, st);
+    if (!rc && crt_prescale_ok(ctx, P, 0, level)) {
+        rc = prescale_rows(ctx, pr->d_res, 2, P, st);
+        pr->prescaled = rc == HG_OK;
+    }
     if (rc) {
         cudaFreeAsync(pr->d_res, 0);
         delete pr;
@@ -866,7 +909,7 @@ extern "C" int hg_ct_mult_prepared(hg_ctx* ctx, const hg_key* evk, const hg_ctpr
     uint32_t* e1 = e0 + (size_t)W * N;
     OutSet outs{};
     outs.out[0] = d0; outs.out[1] = d1; outs.out[2] = d2;
-    rc = launch_crt(ctx, res.u32(), 3, P, 0, level, outs, st);
+    rc = launch_crt(ctx, res.u32(), 3, P, 0, level, outs, st, nullptr, a->prescaled);
     if (rc) return rc;
     return ct_mult_finish(ctx, evk, d0, d1, d2, e0, e1, level, rescale_bits, out0, out1, st);
 }
@@ -938,7 +981,7 @@ extern "C" int hg_ct_automorph_batch(hg_ctx* ctx, const hg_key* key, int count,
             outs.out[2 * g] = buf.u32() + (size_t)(2 * g + 1) * W * N;   // e0_g
             outs.out[2 * g + 1] = out1s[g0 + g];
         }
-        if ((rc = launch_crt(ctx, t, 2 * G, P, key->big_l, level, outs, st))) return rc;
+        if ((rc = launch_crt(ctx, t, 2 * G, P, key->big_l, level, outs, st, nullptr, key->prescaled))) return rc;
         for (int g = 0; g < G; ++g) {
             uint32_t* a0 = buf.u32() + (size_t)(2 * g) * W * N;
             if ((rc = hg_ew_automorphism(ctx, a0, c0s[g0 + g], level, k, st))) return rc;

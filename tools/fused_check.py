@@ -1,4 +1,5 @@
-"""A/B check of the fused CRT finish: ct-mult (+rescale) outputs with and without HG_NO_FUSE.
+"""A/B check of the fused CRT finish and the prescaled CRT inputs: ct-mult (+rescale), rotation
+and batched-rotation outputs with and without HG_NO_FUSE + HG_NO_PRESCALE.
 
     python tools/fused_check.py            # runs both arms in subprocesses and compares
 """
@@ -32,11 +33,14 @@ def arm(path, cases=None):
         r = eng.rotate(a, 3)
         m0 = hg.ckks.mult(a, b, evk)                       # no rescale
         pc = eng.mult(eng.prepare(a), b)                   # resident left operand
+        rm = eng.rotate_many([a, b, a], 5)                 # batched key switches
         out[f"{log_n}_{level}_c0"] = c.c0.words.cpu().numpy()
         out[f"{log_n}_{level}_c1"] = c.c1.words.cpu().numpy()
         out[f"{log_n}_{level}_r0"] = r.c0.words.cpu().numpy()
         out[f"{log_n}_{level}_m0"] = m0.c0.words.cpu().numpy()
         out[f"{log_n}_{level}_p1"] = pc.c1.words.cpu().numpy()
+        for k, x in enumerate(rm):
+            out[f"{log_n}_{level}_b{k}"] = torch.cat([x.c0.words, x.c1.words]).cpu().numpy()
     np.savez(path, **out)
 
 
@@ -50,6 +54,7 @@ def compare(quick=False, workdir="/tmp"):
     on_path, off_path = os.path.join(workdir, "fused_on.npz"), os.path.join(workdir, "fused_off.npz")
     subprocess.run([sys.executable, __file__, on_path] + extra, check=True, env=env)
     env["HG_NO_FUSE"] = "1"
+    env["HG_NO_PRESCALE"] = "1"
     subprocess.run([sys.executable, __file__, off_path] + extra, check=True, env=env)
     on, off = np.load(on_path), np.load(off_path)
     bad = 0
