@@ -120,6 +120,7 @@ extern "C" int hg_ctx_create(int log_n, int device, hg_ctx** out) {
     cudaMemcpy(ctx->d_modup, modup.data(), modup.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
     // keep freed stream-ordered allocations cached in the pool (residue scratch is reused
     // every op; returning it to the driver would serialise on cudaFree)
+    cudaStreamCreateWithFlags(&ctx->upload_stream, cudaStreamNonBlocking);   // created once: no lock in hg_upload
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
         uint64_t thr = UINT64_MAX;
@@ -136,6 +137,7 @@ extern "C" int hg_ctx_create(int log_n, int device, hg_ctx** out) {
 
 extern "C" int hg_ctx_destroy(hg_ctx* ctx) {
     if (!ctx) return HG_OK;
+    if (ctx->upload_stream) cudaStreamDestroy(ctx->upload_stream);
     cudaFree(ctx->d_pinfo);
     cudaFree(ctx->d_modup);
     cudaFree(ctx->d_tw_fwd);
@@ -329,6 +331,12 @@ int hg_tmap_2d_u32(CUtensorMap* tm, const void* base, uint64_t inner, uint64_t o
     return HG_OK;
 }
 
+int hg_upload(hg_ctx* ctx, void* dst, const void* src, size_t bytes) {
+    HG_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->upload_stream));
+    HG_CUDA_TRY(cudaStreamSynchronize(ctx->upload_stream));   // the copy only, not the compute queue
+    return HG_OK;
+}
+
 // ---- CRT tables ---------------------------------------------------------------------------
 // multiply a little-endian word array (truncated to W words) by a 32-bit value in place
 static void mul_small_trunc(std::vector<uint32_t>& a, uint32_t m) {
@@ -395,11 +403,11 @@ int hg_get_crt(hg_ctx* ctx, int P, const CrtTable** out) {
     HG_CUDA_TRY(cudaMalloc(&t.d_cinv, P * 4));
     HG_CUDA_TRY(cudaMalloc(&t.d_cinv_sh, P * 4));
     HG_CUDA_TRY(cudaMalloc(&t.d_invp, P * 8));
-    HG_CUDA_TRY(cudaMemcpy(t.d_M, M.data(), M.size() * 4, cudaMemcpyHostToDevice));
-    HG_CUDA_TRY(cudaMemcpy(t.d_negQ, negQ.data(), negQ.size() * 4, cudaMemcpyHostToDevice));
-    HG_CUDA_TRY(cudaMemcpy(t.d_cinv, cinv.data(), P * 4, cudaMemcpyHostToDevice));
-    HG_CUDA_TRY(cudaMemcpy(t.d_cinv_sh, cinv_sh.data(), P * 4, cudaMemcpyHostToDevice));
-    HG_CUDA_TRY(cudaMemcpy(t.d_invp, invp.data(), P * 8, cudaMemcpyHostToDevice));
+    if (int rc = hg_upload(ctx, t.d_M, M.data(), M.size() * 4)) return rc;
+    if (int rc = hg_upload(ctx, t.d_negQ, negQ.data(), negQ.size() * 4)) return rc;
+    if (int rc = hg_upload(ctx, t.d_cinv, cinv.data(), P * 4)) return rc;
+    if (int rc = hg_upload(ctx, t.d_cinv_sh, cinv_sh.data(), P * 4)) return rc;
+    if (int rc = hg_upload(ctx, t.d_invp, invp.data(), P * 8)) return rc;
     t.P32 = (P + 31) & ~31;
     {
         std::vector<uint8_t> conv;
@@ -411,7 +419,7 @@ int hg_get_crt(hg_ctx* ctx, int P, const CrtTable** out) {
         std::copy(negQ.begin(), negQ.end(), Mp.begin() + (size_t)W * P);
         hg_crt_build_conv(t, P + 1, t.P32p, conv, Mp);
         HG_CUDA_TRY(cudaMalloc(&t.d_Bpipe, conv.size()));
-        HG_CUDA_TRY(cudaMemcpy(t.d_Bpipe, conv.data(), conv.size(), cudaMemcpyHostToDevice));
+        if (int rc = hg_upload(ctx, t.d_Bpipe, conv.data(), conv.size())) return rc;
     }
     t.hM = std::move(M);
     std::lock_guard<std::mutex> lk(ctx->mu);
@@ -434,10 +442,10 @@ int hg_crt_ensure_fallback(hg_ctx* ctx, const CrtTable* ctab) {
     std::vector<uint32_t> frag;
     hg_crt_build_fragments(*t, t->P, t->P32, frag, t->hM);
     HG_CUDA_TRY(cudaMalloc(&t->d_Bfrag, frag.size() * 4));
-    HG_CUDA_TRY(cudaMemcpy(t->d_Bfrag, frag.data(), frag.size() * 4, cudaMemcpyHostToDevice));
+    if (int rc = hg_upload(ctx, t->d_Bfrag, frag.data(), frag.size() * 4)) return rc;
     std::vector<uint8_t> conv;
     hg_crt_build_conv(*t, t->P, t->P32, conv, t->hM);
     HG_CUDA_TRY(cudaMalloc(&t->d_Bconv, conv.size()));
-    HG_CUDA_TRY(cudaMemcpy(t->d_Bconv, conv.data(), conv.size(), cudaMemcpyHostToDevice));
+    if (int rc = hg_upload(ctx, t->d_Bconv, conv.data(), conv.size())) return rc;
     return HG_OK;
 }

@@ -37,6 +37,20 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     }
 }
 
+// HG_CRT_PROF (diagnostic builds only): per-CTA, per-warp cycles spent in each barrier wait of
+// the pipelined kernel, read back with hg_crt_prof_read
+#ifdef HG_CRT_PROF
+__device__ unsigned long long g_crt_prof[160][20][8];
+#define PWAIT(cat, bar, par)                                  \
+    do {                                                      \
+        const long long _t = clock64();                       \
+        mbar_wait(bar, par);                                  \
+        prof[cat] += (unsigned long long)(clock64() - _t);    \
+    } while (0)
+#else
+#define PWAIT(cat, bar, par) mbar_wait(bar, par)
+#endif
+
 constexpr int kMaxOuts = 8;   // outputs per launch (the pipelined kernel; older kernels take 4)
 struct UOuts {
     uint32_t* out[kMaxOuts];
@@ -346,6 +360,13 @@ constexpr size_t pipe_smem() {
            (FUSED ? 2 * (size_t)kAddStage : 0);
 }
 
+// a * b + c, 32 x 32 -> 64-bit multiply-add (one IMAD.WIDE)
+__device__ __forceinline__ uint64_t madw(uint32_t a, uint32_t b, uint64_t c) {
+    uint64_t d;
+    asm("mad.wide.u32 %0, %1, %2, %3;\n" : "=l"(d) : "r"(a), "r"(b), "l"(c));
+    return d;
+}
+
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
 }
@@ -422,7 +443,7 @@ struct Emitter {
         } else {
             const int v = u - rw - 1;
             if (v >= 0 && v < out2_w)
-                out[(size_t)v * N + i] = ((prev2 >> rb) | (w << (32 - rb))) & (v == out2_w - 1 ? top2 : 0xffffffffu);
+                out[(size_t)v * N + i] = __funnelshift_r(prev2, w, rb) & (v == out2_w - 1 ? top2 : 0xffffffffu);
             prev2 = w;
         }
     }
@@ -539,6 +560,10 @@ __global__ void __launch_bounds__(PipeCfg<FUSED>::kWarps * 32, 1) crt_umma_pipe_
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n");
     const uint32_t tmem = tmem_base;
+#ifdef HG_CRT_PROF
+    unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const long long t_start = clock64();
+#endif
 
     const int tpo = N / kRows;
     const int sw = shift >> 5, sbit = shift & 31;
@@ -565,7 +590,7 @@ __global__ void __launch_bounds__(PipeCfg<FUSED>::kWarps * 32, 1) crt_umma_pipe_
                     const int oy = tile / tpo, cb = (tile - oy * tpo) * kRows;
                     for (int kc = 0; kc < nkc; ++kc, ++it) {
                         const int s = it % kRR;
-                        mbar_wait(smem_u32(&bar_res_empty[s]), ((it / kRR) & 1) ^ 1);
+                        PWAIT(0, smem_u32(&bar_res_empty[s]), ((it / kRR) & 1) ^ 1);
                         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
                         mbar_expect_tx(smem_u32(&bar_res_full[s]), (uint32_t)kResStage);
                         asm volatile(
@@ -587,7 +612,7 @@ __global__ void __launch_bounds__(PipeCfg<FUSED>::kWarps * 32, 1) crt_umma_pipe_
                 const uint8_t* bsrc = Bpipe + (size_t)((tb0 >> 3) + h * (kJobCols / 8)) * 8192;
                 for (int kc = 0; kc < nkc; ++kc, ++it) {
                     const int s = it % kRB;
-                    mbar_wait(smem_u32(&bar_b_empty[s]), ((it / kRB) & 1) ^ 1);
+                    PWAIT(0, smem_u32(&bar_b_empty[s]), ((it / kRB) & 1) ^ 1);
                     mbar_expect_tx(smem_u32(&bar_b_full[s]), bytes);
                     bulk_g2s(smem_u32(s_b + s * kBStagePipe), bsrc + (size_t)kc * (W >> 3) * 8192, bytes,
                              smem_u32(&bar_b_full[s]));
@@ -604,12 +629,12 @@ __global__ void __launch_bounds__(PipeCfg<FUSED>::kWarps * 32, 1) crt_umma_pipe_
                 const uint32_t Nn = 8u * (uint32_t)job_cols(h);
                 const uint32_t idesc = (2u << 4) | ((Nn >> 3) << 17) | ((uint32_t)(kRows >> 4) << 24);
                 const int tb = ij & 1;
-                mbar_wait(smem_u32(&bar_tm_empty[tb]), ((ij >> 1) & 1) ^ 1);
+                PWAIT(0, smem_u32(&bar_tm_empty[tb]), ((ij >> 1) & 1) ^ 1);
                 asm volatile("tcgen05.fence::after_thread_sync;\n");
                 for (int kc = 0; kc < nkc; ++kc, ++ia, ++ib) {
                     const int sa_ = ia % kRA, sb_ = ib % kRB;
-                    mbar_wait(smem_u32(&bar_a_full[sa_]), (ia / kRA) & 1);
-                    mbar_wait(smem_u32(&bar_b_full[sb_]), (ib / kRB) & 1);
+                    PWAIT(1, smem_u32(&bar_a_full[sa_]), (ia / kRA) & 1);
+                    PWAIT(2, smem_u32(&bar_b_full[sb_]), (ib / kRB) & 1);
                     asm volatile("tcgen05.fence::after_thread_sync;\n");
 #pragma unroll
                     for (int k = 0; k < kKChunk / 32; ++k) {
@@ -635,7 +660,7 @@ __global__ void __launch_bounds__(PipeCfg<FUSED>::kWarps * 32, 1) crt_umma_pipe_
                     const int oy = tile / tpo, cb = (tile - oy * tpo) * kRows;
                     const int ubase = tb0 + h * kJobCols - sw - (sbit ? 1 : 0);
                     const int s = ij & 1;
-                    mbar_wait(smem_u32(&bar_add_empty[s]), ((ij >> 1) & 1) ^ 1);
+                    PWAIT(0, smem_u32(&bar_add_empty[s]), ((ij >> 1) & 1) ^ 1);
                     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
                     mbar_expect_tx(smem_u32(&bar_add_full[s]), (uint32_t)kAddStage);
                     asm volatile(
@@ -660,7 +685,7 @@ __global__ void __launch_bounds__(PipeCfg<FUSED>::kWarps * 32, 1) crt_umma_pipe_
             uint64_t acc = 0;
             for (int kc = 0; kc < nkc; ++kc, ++ir, ++ia) {
                 const int s = ir % kRR, sa_ = ia % kRA;
-                mbar_wait(smem_u32(&bar_res_full[s]), (ir / kRR) & 1);
+                PWAIT(0, smem_u32(&bar_res_full[s]), (ir / kRR) & 1);
                 const uint32_t* stg = reinterpret_cast<const uint32_t*>(s_res + s * kResStage) + half * 16 * kRows;
                 const int j0 = kc * 32 + half * 16;
                 uint32_t y[16];
@@ -678,6 +703,9 @@ __global__ void __launch_bounds__(PipeCfg<FUSED>::kWarps * 32, 1) crt_umma_pipe_
                     acc += (uint64_t)y[u] * pc.w;
                 }
                 if (kc == nkc - 1) {
+#ifdef HG_CRT_PROF
+                    const long long t_bs = clock64();
+#endif
                     // slot P of the last chunk carries v (its B row holds -Q): combine the halves
                     s_acc[half][n] = acc;
                     asm volatile("bar.sync 1, %0;\n" ::"n"(8 * 32) : "memory");
@@ -687,11 +715,19 @@ __global__ void __launch_bounds__(PipeCfg<FUSED>::kWarps * 32, 1) crt_umma_pipe_
 #pragma unroll
                     for (int u = 0; u < 16; ++u)
                         if (j0 + u == P) y[u] = v;
+#ifdef HG_CRT_PROF
+                    prof[3] += (unsigned long long)(clock64() - t_bs);
+#endif
                 }
-                mbar_wait(smem_u32(&bar_a_empty[sa_]), ((ia / kRA) & 1) ^ 1);
+                PWAIT(1, smem_u32(&bar_a_empty[sa_]), ((ia / kRA) & 1) ^ 1);
+#ifdef HG_CRT_PROF
+                const long long t_st = clock64();
+#endif
                 // WAR across proxies: the tensor core's (async-proxy) reads of this stage must be
                 // ordered before our generic stores
+#ifndef HG_EXP_NO_WAR_FENCE
                 asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+#endif
                 uint8_t* dst = s_a + sa_ * kAStage + (g * 8 + 4 * half) * 128 + rr * 16;
 #pragma unroll
                 for (int c = 0; c < 4; ++c)
@@ -700,6 +736,9 @@ __global__ void __launch_bounds__(PipeCfg<FUSED>::kWarps * 32, 1) crt_umma_pipe_
                 asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
                 __syncwarp();
                 if (lane == 0) mbar_arrive(smem_u32(&bar_a_full[sa_]));
+#ifdef HG_CRT_PROF
+                prof[2] += (unsigned long long)(clock64() - t_st);
+#endif
             }
         }
     } else {
@@ -712,8 +751,18 @@ __global__ void __launch_bounds__(PipeCfg<FUSED>::kWarps * 32, 1) crt_umma_pipe_
         // two groups take alternate jobs (job parity = TMEM buffer); within a tile the carry
         // state moves from the group that finished column block h to the one taking h+1
         const int grp = (warp - kEpiWarp0) >> 2;
+        // fused finish (see Emitter): window word u -> s = u + addend + c2 (+ the rescale's
+        // rounding bit), output word v = bits [post, l) of s; the pipelined launcher takes no
+        // automorphism on the addend
+        const int post = FUSED ? fin.post : 0;
+        const int rw = post >> 5, rb = post & 31, vsh = rb ? 1 : 0, ush = sbit ? 1 : 0;
+        const int bits2 = out_bits - post;
+        const int out2_w = (bits2 + 31) >> 5;
+        const uint32_t top2 = (bits2 & 31) ? ((1u << (bits2 & 31)) - 1u) : 0xffffffffu;
+        const int rw2 = post > 0 ? (post - 1) >> 5 : -1;
+        const uint32_t rbit2 = post > 0 ? 1u << ((post - 1) & 31) : 0u;
         uint64_t carry = 0;
-        uint32_t prev = 0;
+        uint32_t prev = 0, c2 = 0, prev2 = 0;
         bool amb = false;
         int nwr = 0, nrd = 0;   // handoffs written to slot grp / read from slot 1 - grp
         int ij = 0;
@@ -725,15 +774,16 @@ __global__ void __launch_bounds__(PipeCfg<FUSED>::kWarps * 32, 1) crt_umma_pipe_
             const uint32_t* addp = oy < 4 ? (oy == 0 ? fin.add[0] : oy == 1 ? fin.add[1] : oy == 2 ? fin.add[2] : fin.add[3])
                                           : nullptr;
             const int i = cb + n;
-            Emitter em;
-            em.init(out, N, i, out_bits, fin, FUSED ? addp : nullptr);
+            uint32_t* const outi = out + i;
             if (h == 0) {
                 carry = 0;
                 prev = 0;
                 amb = false;
+                c2 = 0;
+                prev2 = 0;
             } else {
                 const int sl = 1 - grp;
-                mbar_wait(smem_u32(&bar_hand_full[sl]), nrd & 1);
+                PWAIT(0, smem_u32(&bar_hand_full[sl]), nrd & 1);
                 const uint4 hv = s_hand[sl][n];
                 const uint2 hv2 = s_hand2[sl][n];
                 __syncwarp();
@@ -742,8 +792,8 @@ __global__ void __launch_bounds__(PipeCfg<FUSED>::kWarps * 32, 1) crt_umma_pipe_
                 carry = ((uint64_t)hv.y << 32) | hv.x;
                 prev = hv.z;
                 amb = hv.w != 0;
-                em.c2 = hv2.x;
-                em.prev2 = hv2.y;
+                c2 = hv2.x;
+                prev2 = hv2.y;
             }
             const int tb = ij & 1;
             const int c0 = tb0 + h * kJobCols;
@@ -751,12 +801,18 @@ __global__ void __launch_bounds__(PipeCfg<FUSED>::kWarps * 32, 1) crt_umma_pipe_
             // the job's addend words (output word u = c0 + k - sw - (sbit != 0)), loaded before
             // the accumulator wait so their latency is off the carry chain
             const uint32_t* av = s_add + tb * (kAddStage / 4) + n;   // addend word k at av[k * 128]
-            if (FUSED) mbar_wait(smem_u32(&bar_add_full[tb]), (ij >> 1) & 1);
-            mbar_wait(smem_u32(&bar_tm_full[tb]), (ij >> 1) & 1);
+            if (FUSED) PWAIT(1, smem_u32(&bar_add_full[tb]), (ij >> 1) & 1);
+            PWAIT(2, smem_u32(&bar_tm_full[tb]), (ij >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;\n");
             const uint32_t lane_addr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(tb * 256);
+#ifdef HG_CRT_PROF
+            const long long t_loop = clock64();
+#endif
             for (int tl = 0; tl < ncols; tl += 4) {
                 uint32_t e[32];
+#ifdef HG_CRT_PROF
+                const long long t_ld = clock64();
+#endif
                 asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
                              "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
                              : "=r"(e[0]), "=r"(e[1]), "=r"(e[2]), "=r"(e[3]), "=r"(e[4]), "=r"(e[5]),
@@ -767,45 +823,82 @@ __global__ void __launch_bounds__(PipeCfg<FUSED>::kWarps * 32, 1) crt_umma_pipe_
                                "=r"(e[30]), "=r"(e[31])
                              : "r"(lane_addr + (uint32_t)(tl * 8)));
                 asm volatile("tcgen05.wait::ld.sync.aligned;\n");
+#ifdef HG_CRT_PROF
+                prof[4] += (unsigned long long)(clock64() - t_ld);
+#endif
+                // the four columns' digit sums first (independent of the carry), then the short
+                // carry chain, then emission: column value = lo + hi * 2^32 (digit 7 is zero);
+                // columns past T (padding of the last batch) only disturb the dead carry
+                uint64_t lo[4], hi[4];
+#pragma unroll
+                for (int hh = 0; hh < 4; ++hh) {
+                    const uint32_t* E = e + 8 * hh;
+                    lo[hh] = madw(E[3], 1u << 24, madw(E[2], 1u << 16, madw(E[1], 256u, (uint64_t)E[0])));
+                    hi[hh] = madw(E[6], 1u << 16, madw(E[5], 256u, (uint64_t)E[4]));
+                }
+                uint32_t wv[4];
+#pragma unroll
+                for (int hh = 0; hh < 4; ++hh) {
+                    const uint64_t x = lo[hh] + carry + (c0 + tl + hh == round_col ? round_bit : 0u);
+                    wv[hh] = (uint32_t)x;
+                    carry = (x >> 32) + hi[hh];
+                }
+                // emission, predicated rather than branched (every condition is warp-uniform):
+                // window word u = t - sw - (sbit != 0) is valid for 0 <= u < out_w (so t < T)
 #pragma unroll
                 for (int hh = 0; hh < 4; ++hh) {
                     const int t = c0 + tl + hh;
-                    if (t >= T) break;
-                    const uint32_t* E = e + 8 * hh;
-                    // column value = lo + hi * 2^32 (digit 7 is identically zero)
-                    const uint64_t lo = (uint64_t)E[0] + ((uint64_t)E[1] << 8) + ((uint64_t)E[2] << 16) + ((uint64_t)E[3] << 24);
-                    const uint64_t hi = (uint64_t)E[4] + ((uint64_t)E[5] << 8) + ((uint64_t)E[6] << 16);
-                    const uint64_t sum = (lo & 0xffffffffull) + (carry & 0xffffffffull) + (t == round_col ? round_bit : 0u);
-                    const uint32_t word = (uint32_t)sum;
-                    carry = (sum >> 32) + (lo >> 32) + hi + (carry >> 32);
-                    if (t < sw) {
+                    const uint32_t word = wv[hh];
+                    if (t < sw) {   // below the window: the truncated-column ambiguity flag
                         if (t == tb0 + 1) amb = word >= 0xFFFFFF00u;
                         else if (t > tb0 + 1) amb = amb && (word == 0xffffffffu);
-                    } else if (sbit == 0 || t > sw) {
-                        const uint32_t o = sbit == 0 ? word : (prev >> sbit) | (word << (32 - sbit));
-                        const int u = t - sw - (sbit ? 1 : 0);
-                        if (FUSED) em.put(u, o, av[(tl + hh) * kRows]);
-                        else out[(size_t)u * N + i] = (u == out_w - 1) ? (o & top_l) : o;
                     }
+                    const int u = t - sw - ush;
+                    const uint32_t o = sbit ? __funnelshift_r(prev, word, sbit) : word;
                     prev = word;
+                    if (u >= 0 && u < out_w) {
+                        const uint32_t mu = u == out_w - 1 ? top_l : 0xffffffffu;
+                        if (FUSED) {
+                            const uint64_t sum = (uint64_t)(o & mu) + av[(tl + hh) * kRows] + c2 +
+                                                 (u == rw2 ? rbit2 : 0u);
+                            const uint32_t w = (uint32_t)sum & mu;
+                            c2 = (uint32_t)(sum >> 32);
+                            const int v = u - rw - vsh;
+                            const uint32_t ov = rb ? __funnelshift_r(prev2, w, rb) : w;
+                            prev2 = w;
+                            if (v >= 0 && v < out2_w) outi[(size_t)v * N] = ov & (v == out2_w - 1 ? top2 : 0xffffffffu);
+                        } else {
+                            outi[(size_t)u * N] = o & mu;
+                        }
+                    }
                 }
             }
             if (FUSED) {
                 __syncwarp();
                 if (lane == 0) mbar_arrive(smem_u32(&bar_add_empty[tb]));
             }
-            if (FUSED && h == jpt - 1) em.flush();
+#ifdef HG_CRT_PROF
+            const long long t_post = clock64();
+            prof[6] += (unsigned long long)(t_post - t_loop);
+#endif
+            if (FUSED && h == jpt - 1 && rb) {   // the last output word: the top bits of prev2
+                const int v = out_w - 1 - rw;
+                if (v >= 0 && v < out2_w) outi[(size_t)v * N] = (prev2 >> rb) & (v == out2_w - 1 ? top2 : 0xffffffffu);
+            }
             asm volatile("tcgen05.fence::before_thread_sync;\n");
             __syncwarp();
             if (lane == 0) mbar_arrive(smem_u32(&bar_tm_empty[tb]));
             if (h < jpt - 1) {
-                mbar_wait(smem_u32(&bar_hand_empty[grp]), (nwr & 1) ^ 1);
+                PWAIT(3, smem_u32(&bar_hand_empty[grp]), (nwr & 1) ^ 1);
                 s_hand[grp][n] = make_uint4((uint32_t)carry, (uint32_t)(carry >> 32), prev, amb ? 1u : 0u);
-                if (FUSED) s_hand2[grp][n] = make_uint2(em.c2, em.prev2);
+                if (FUSED) s_hand2[grp][n] = make_uint2(c2, prev2);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(smem_u32(&bar_hand_full[grp]));
                 ++nwr;
             }
+#ifdef HG_CRT_PROF
+            prof[7] += (unsigned long long)(clock64() - t_post);
+#endif
             if (h == jpt - 1 && tb0 > 0 && amb) {
                 Emitter fresh;
                 fresh.init(out, N, i, out_bits, fin, FUSED ? addp : nullptr);
@@ -814,6 +907,11 @@ __global__ void __launch_bounds__(PipeCfg<FUSED>::kWarps * 32, 1) crt_umma_pipe_
             }
         }
     }
+#ifdef HG_CRT_PROF
+    prof[5] = (unsigned long long)(clock64() - t_start);
+    if (lane == 0 && blockIdx.x < 160)
+        for (int c = 0; c < 8; ++c) g_crt_prof[blockIdx.x][warp][c] = prof[c];
+#endif
     asm volatile("tcgen05.fence::before_thread_sync;\n");
     __syncthreads();
     if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(512));
@@ -926,3 +1024,10 @@ int hg_crt_umma_launch(hg_ctx* ctx, const CrtTable* tab, const uint32_t* res, in
     HG_LAUNCH_CHECK(ctx);
     return HG_OK;
 }
+
+#ifdef HG_CRT_PROF
+// copies the wait-cycle table of the last pipelined CRT launch: [160][20][6] u64
+extern "C" int hg_crt_prof_read(unsigned long long* out) {
+    return cudaMemcpyFromSymbol(out, g_crt_prof, sizeof(g_crt_prof)) == cudaSuccess ? 0 : 1;
+}
+#endif

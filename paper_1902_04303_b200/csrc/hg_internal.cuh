@@ -74,6 +74,7 @@ struct hg_ctx {
     int modup_frag_ks = 0;
     std::map<int, CrtTable> crt;
     std::mutex mu;
+    cudaStream_t upload_stream = nullptr;   // non-blocking: table uploads never drain the compute queue
     std::atomic<long long> launches{0};
     // live kernel timing (hg_set_kernel_timing)
     struct Timer {
@@ -141,6 +142,10 @@ int hg_tmap_2d_u32(CUtensorMap* tm, const void* base, uint64_t inner, uint64_t o
                    uint32_t box_inner, uint32_t box_outer);
 int hg_ensure_twiddles(hg_ctx* ctx, int P);
 int hg_get_crt(hg_ctx* ctx, int P, const CrtTable** out);
+// host -> device copy of a lazily built table on the context's private non-blocking stream: a
+// plain cudaMemcpy would synchronise with the legacy default stream and so wait for every
+// queued kernel (a first-use table build mid-pipeline would drain the GPU)
+int hg_upload(hg_ctx* ctx, void* dst, const void* src, size_t bytes);
 int hg_crt_ensure_fallback(hg_ctx* ctx, const CrtTable* tab);   // d_Bfrag / d_Bconv
 int hg_primes_for_bits(const hg_ctx* ctx, double bits);   // -1 if too wide
 int hg_crt_build_fragments(const CrtTable& t, int P, int P32, std::vector<uint32_t>& out,
