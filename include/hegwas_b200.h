@@ -169,6 +169,14 @@ long long hg_launch_count(const hg_ctx* ctx);
  * timed region can bracket only the class whose roofline it reports).                */
 int hg_set_kernel_timing(hg_ctx* ctx, int enabled);
 int hg_kernel_stats(hg_ctx* ctx, int kind, double* ms, long long* launches, double* work);
+/* Device arena for the library's long-lived objects (prepared switching keys and
+ * prepared operands): reserve one more slab of `bytes` up front, so a job's first uses
+ * carve keys out of it instead of growing device memory piece by piece.  Replaces the
+ * capacity sizing of the reference's CiphertextCache (cache.py:78-97) for the objects
+ * that stay resident.  `stream` is unused (the slab is not stream-ordered).
+ * hg_pool_bytes: reserved bytes (in_use = 0) or bytes held by live objects (in_use = 1). */
+int hg_pool_reserve(hg_ctx* ctx, size_t bytes, void* stream);
+size_t hg_pool_bytes(const hg_ctx* ctx, int in_use);
 
 #ifdef __cplusplus
 }

@@ -76,6 +76,8 @@ SIGNATURES = {
     "hg_launch_count": (ctypes.c_longlong, [_vp]),
     "hg_set_kernel_timing": (_i, [_vp, _i]),
     "hg_poly_sum": (_i, [_vp, _vp, ctypes.POINTER(ctypes.c_void_p), _i, _i, _vp]),
+    "hg_pool_reserve": (_i, [_vp, ctypes.c_size_t, _vp]),
+    "hg_pool_bytes": (ctypes.c_size_t, [_vp, _i]),
     "hg_kernel_stats": (_i, [_vp, _i, ctypes.POINTER(ctypes.c_double),
                              ctypes.POINTER(ctypes.c_longlong), ctypes.POINTER(ctypes.c_double)]),
 }
@@ -113,6 +115,25 @@ def check(rc: int):
     if rc in (HG_EINVAL, HG_ERANGE):
         raise ParameterError(msg)
     raise DeviceError(f"native error {rc}: {msg}")
+
+
+def check_alloc(call, evict=None):
+    """check(call()) for an entry point that allocates from the device arena.  On HG_ENOMEM
+    the device memory torch's caching allocator holds unused is handed back (and, failing
+    that, ``evict()`` drops cached prepared keys) before one retry: the two allocators
+    share the HBM and neither can take memory the other has cached."""
+    rc = call()
+    if rc == HG_ENOMEM:
+        import torch
+
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        rc = call()
+        if rc == HG_ENOMEM and evict is not None:
+            evict()
+            torch.cuda.synchronize()
+            rc = call()
+    check(rc)
 
 
 def operand(words, bits: int, signed: bool) -> Operand:
@@ -158,6 +179,13 @@ class Context:
         else:
             code = sum(1 << KERNEL_KINDS[k] for k in kinds) << 1
         check(self.lib.hg_set_kernel_timing(self.handle, code))
+
+    def pool_reserve(self, nbytes: int) -> None:
+        """Reserve one more device-arena slab of nbytes (hg_pool_reserve)."""
+        check(self.lib.hg_pool_reserve(self.handle, int(nbytes), self.stream()))
+
+    def pool_bytes(self, in_use: bool = False) -> int:
+        return int(self.lib.hg_pool_bytes(self.handle, 1 if in_use else 0))
 
     def kernel_stats(self, kind: str) -> dict:
         """{'ms', 'launches', 'work'} of the events recorded since timing was enabled."""

@@ -135,6 +135,97 @@ extern "C" int hg_ctx_create(int log_n, int device, hg_ctx** out) {
     return HG_OK;
 }
 
+// ---- device arena (hg_internal.cuh) ---------------------------------------------------
+static constexpr size_t kArenaAlign = 2u << 20;      // 2 MB: slab and object granularity
+static constexpr size_t kArenaSlab = 8ull << 30;     // default growth step
+
+int hg_arena_grow(hg_ctx* ctx, size_t bytes) {
+    bytes = (bytes + kArenaAlign - 1) & ~(kArenaAlign - 1);
+    char* base = nullptr;
+    if (cudaMalloc(&base, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return hg_fail(HG_ENOMEM, "device arena: cudaMalloc of " + std::to_string(bytes >> 20) + " MB failed");
+    }
+    std::lock_guard<std::mutex> g(ctx->arena.mu);
+    DeviceArena::Slab s;
+    s.base = base;
+    s.size = bytes;
+    s.free[0] = bytes;
+    ctx->arena.slabs.push_back(std::move(s));
+    ctx->arena.reserved += bytes;
+    return HG_OK;
+}
+
+static void* arena_take(DeviceArena& a, size_t bytes) {
+    for (size_t i = 0; i < a.slabs.size(); ++i) {
+        auto& fl = a.slabs[i].free;
+        for (auto it = fl.begin(); it != fl.end(); ++it) {
+            if (it->second < bytes) continue;
+            const size_t off = it->first, len = it->second;
+            fl.erase(it);
+            if (len > bytes) fl[off + bytes] = len - bytes;
+            char* p = a.slabs[i].base + off;
+            a.live[p] = {(int)i, bytes};
+            a.in_use += bytes;
+            return p;
+        }
+    }
+    return nullptr;
+}
+
+void* hg_arena_alloc(hg_ctx* ctx, size_t bytes) {
+    if (!bytes) bytes = 1;
+    bytes = (bytes + kArenaAlign - 1) & ~(kArenaAlign - 1);
+    {
+        std::lock_guard<std::mutex> g(ctx->arena.mu);
+        if (void* p = arena_take(ctx->arena, bytes)) return p;
+    }
+    // grow by a default slab (or exactly the request when the device is nearly full)
+    if (hg_arena_grow(ctx, bytes > kArenaSlab ? bytes : kArenaSlab) != HG_OK &&
+        hg_arena_grow(ctx, bytes) != HG_OK)
+        return nullptr;
+    std::lock_guard<std::mutex> g(ctx->arena.mu);
+    return arena_take(ctx->arena, bytes);
+}
+
+void hg_arena_free(hg_ctx* ctx, void* ptr) {
+    if (!ptr) return;
+    std::lock_guard<std::mutex> g(ctx->arena.mu);
+    DeviceArena& a = ctx->arena;
+    auto it = a.live.find((char*)ptr);
+    if (it == a.live.end()) return;
+    const int si = it->second.first;
+    size_t off = (size_t)((char*)ptr - a.slabs[si].base), len = it->second.second;
+    a.in_use -= len;
+    a.live.erase(it);
+    auto& fl = a.slabs[si].free;
+    auto nx = fl.lower_bound(off);
+    if (nx != fl.end() && off + len == nx->first) {   // merge with the following hole
+        len += nx->second;
+        nx = fl.erase(nx);
+    }
+    if (nx != fl.begin()) {                           // merge with the preceding hole
+        auto pv = std::prev(nx);
+        if (pv->first + pv->second == off) {
+            pv->second += len;
+            return;
+        }
+    }
+    fl[off] = len;
+}
+
+extern "C" int hg_pool_reserve(hg_ctx* ctx, size_t bytes, void* stream) {
+    (void)stream;
+    if (!ctx) return hg_fail(HG_EINVAL, "hg_pool_reserve: null context");
+    if (!bytes) return HG_OK;
+    return hg_arena_grow(ctx, bytes);
+}
+
+extern "C" size_t hg_pool_bytes(const hg_ctx* ctx, int in_use) {
+    if (!ctx) return 0;
+    return in_use ? ctx->arena.in_use : ctx->arena.reserved;
+}
+
 extern "C" int hg_ctx_destroy(hg_ctx* ctx) {
     if (!ctx) return HG_OK;
     if (ctx->upload_stream) cudaStreamDestroy(ctx->upload_stream);
@@ -144,6 +235,7 @@ extern "C" int hg_ctx_destroy(hg_ctx* ctx) {
     cudaFree(ctx->d_tw_inv);
     cudaFree(ctx->d_modup_frag);
     cudaFree(ctx->d_modup_umma);
+    for (auto& sl : ctx->arena.slabs) cudaFree(sl.base);
     for (auto& kv : ctx->crt) {
         cudaFree(kv.second.d_M);
         cudaFree(kv.second.d_negQ);

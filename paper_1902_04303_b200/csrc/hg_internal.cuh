@@ -55,6 +55,27 @@ struct CrtTable {
     std::vector<uint32_t> hM;     // host copy of M (source of the lazily built fallback images)
 };
 
+// Device arena for long-lived objects (prepared switching keys, prepared operands):
+// cudaMalloc'd slabs carved first-fit with coalescing frees.  Growing a slab maps ~1 ms/GB
+// against ~11 ms/GB for growing the stream-ordered pool allocation by allocation, and a
+// cold P17 setup prepares ~55 GB of such objects.  Frees are immediate: callers free only
+// once no queued work reads the object (hg_key_destroy / hg_ctprep_destroy synchronise).
+struct DeviceArena {
+    struct Slab {
+        char* base = nullptr;
+        size_t size = 0;
+        std::map<size_t, size_t> free;   // offset -> length, disjoint and non-adjacent
+    };
+    std::vector<Slab> slabs;
+    std::map<char*, std::pair<int, size_t>> live;   // ptr -> (slab, length)
+    std::mutex mu;
+    size_t reserved = 0;
+    size_t in_use = 0;
+};
+void* hg_arena_alloc(hg_ctx* ctx, size_t bytes);   // nullptr when the device is out of memory
+void hg_arena_free(hg_ctx* ctx, void* p);
+int hg_arena_grow(hg_ctx* ctx, size_t bytes);        // one more slab of exactly `bytes`
+
 struct hg_ctx {
     int log_n = 0;
     int N = 0;
@@ -82,6 +103,7 @@ struct hg_ctx {
         int kind = 0;
         double work = 0.0;
     };
+    DeviceArena arena;             // prepared keys / operands
     int timing = 0;                // bitmask of timed kernel classes (1 << kind)
     std::vector<Timer> timers;     // recorded this window
     std::vector<Timer> spare;      // event pairs available for reuse

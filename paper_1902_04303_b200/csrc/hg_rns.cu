@@ -667,7 +667,8 @@ extern "C" int hg_key_prepare(hg_ctx* ctx, const uint32_t* kb, const uint32_t* k
     key->P = P;
     key->bytes = (size_t)2 * P * N * 4;
     const auto t_alloc = std::chrono::steady_clock::now();
-    if (cudaMallocAsync(&key->d_kb, key->bytes, st) != cudaSuccess) {  // pool: no device sync
+    key->d_kb = (uint32_t*)hg_arena_alloc(ctx, key->bytes);
+    if (!key->d_kb) {
         delete key;
         return hg_fail(HG_ENOMEM, "key allocation failed");
     }
@@ -690,7 +691,8 @@ extern "C" int hg_key_prepare(hg_ctx* ctx, const uint32_t* kb, const uint32_t* k
         HG_LAUNCH_CHECK(ctx);
     }
     if (rc) {
-        cudaFreeAsync(key->d_kb, 0);
+        cudaStreamSynchronize(st);   // launches that did go out must finish before reuse
+        hg_arena_free(ctx, key->d_kb);
         delete key;
         return rc;
     }
@@ -700,7 +702,8 @@ extern "C" int hg_key_prepare(hg_ctx* ctx, const uint32_t* kb, const uint32_t* k
 
 extern "C" int hg_key_destroy(hg_key* key) {
     if (!key) return HG_OK;
-    cudaFreeAsync(key->d_kb, 0);
+    cudaDeviceSynchronize();   // the arena reuses the memory at once: no reader may be queued
+    hg_arena_free(key->ctx, key->d_kb);
     delete key;
     return HG_OK;
 }
@@ -838,7 +841,8 @@ extern "C" int hg_ct_prepare(hg_ctx* ctx, const uint32_t* c0, const uint32_t* c1
     pr->level = level;
     pr->P = P;
     pr->bytes = (size_t)2 * P * N * 4;
-    if (cudaMallocAsync(&pr->d_res, pr->bytes, st) != cudaSuccess) {  // pool: no device sync
+    pr->d_res = (uint32_t*)hg_arena_alloc(ctx, pr->bytes);
+    if (!pr->d_res) {
         delete pr;
         return hg_fail(HG_ENOMEM, "prepared operand allocation failed");
     }
@@ -852,7 +856,8 @@ extern "C" int hg_ct_prepare(hg_ctx* ctx, const uint32_t* c0, const uint32_t* c1
         pr->prescaled = rc == HG_OK;
     }
     if (rc) {
-        cudaFreeAsync(pr->d_res, 0);
+        cudaStreamSynchronize(st);
+        hg_arena_free(ctx, pr->d_res);
         delete pr;
         return rc;
     }
@@ -862,7 +867,8 @@ extern "C" int hg_ct_prepare(hg_ctx* ctx, const uint32_t* c0, const uint32_t* c1
 
 extern "C" int hg_ctprep_destroy(hg_ctprep* pr) {
     if (!pr) return HG_OK;
-    cudaFreeAsync(pr->d_res, 0);
+    cudaDeviceSynchronize();
+    hg_arena_free(pr->ctx, pr->d_res);
     delete pr;
     return HG_OK;
 }

@@ -102,6 +102,29 @@ def download_words(t) -> np.ndarray:
     return t.detach().cpu().numpy().view(np.uint32)
 
 
+def reserve_device_bytes(nbytes: int, keep_free: int) -> int:
+    """Grow the device ciphertext pool (torch's caching allocator) by ONE segment of up to
+    ``nbytes``, leaving at least ``keep_free`` bytes to the library's stream-ordered pool
+    (prepared keys, scratch).  The segment goes straight back to the cache, so the thousands
+    of ciphertext allocations that follow are carved out of it instead of each calling
+    cudaMalloc (0.5-0.75 ms apiece at these sizes, measured in a cold P17 setup).
+    Returns the bytes reserved (0 if nothing was needed)."""
+    torch = _torch()
+    dev = _device()
+    free, _ = torch.cuda.mem_get_info(dev)
+    cached = torch.cuda.memory_reserved(dev) - torch.cuda.memory_allocated(dev)
+    want = min(nbytes - cached, free - keep_free)
+    if want < (1 << 30):
+        return 0
+    want &= ~((2 << 20) - 1)
+    try:
+        block = torch.empty(want, dtype=torch.uint8, device=dev)
+    except torch.OutOfMemoryError:
+        return 0
+    del block
+    return want
+
+
 def empty_words(bits: int, n: int):
     torch = _torch()
     return torch.empty((words_for(bits), n), dtype=torch.int32, device=_device())

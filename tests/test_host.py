@@ -150,3 +150,36 @@ def test_synthetic_dataset_shapes():
     assert np.allclose(ds.X[:, 1:].mean(axis=0), 0.0, atol=1e-12)
     assert set(np.unique(ds.y)) <= {0.0, 1.0}
     assert 0.2 < ds.y.mean() < 0.8
+
+
+def test_mask_multi_scale_encode_is_bit_identical():
+    """One FFT per mask serves every scale (encoding.encode_mask_scales): the rounded
+    coefficients equal encode_float's at each scale, for every mask kind, at the ring sizes
+    the pipeline uses (N=2^17 is P17)."""
+    from paper_1902_04303_b200 import CkksParams
+    from paper_1902_04303_b200.encoding import encode_float, encode_mask_scales, mask_vector
+
+    for log_n, specs in [(7, [("slot", 0), ("slot", 63), ("range", 16, 32), ("range_value", 0, 8, 0.5)]),
+                         (13, [("slot", 5), ("range", 0, 245), ("range", 256, 512)]),
+                         (17, [("slot", 244), ("range", 2048, 2304), ("range_value", 0, 245, 0.5)])]:
+        params = CkksParams(log_n=log_n, log_l=1700, log_p=45, log_p_small=30)
+        for spec in specs:
+            scales = (30, 45, 10)
+            got = encode_mask_scales(spec, scales, params)
+            for s, host in zip(scales, got):
+                want = encode_float(mask_vector(spec, params.slot_count), s, params).astype(np.int64)
+                if host[0] == "compact":
+                    from paper_1902_04303_b200.ring import int64_to_words
+                    assert np.array_equal(host[2], int64_to_words(want, host[1])), (log_n, spec, s)
+                else:
+                    assert np.array_equal(host[1], want), (log_n, spec, s)
+
+
+def test_setup_mask_plan_covers_pipeline_masks():
+    from paper_1902_04303_b200 import P17
+    from paper_1902_04303_b200.gwas import GwasConfig, setup_masks
+
+    plan = setup_masks(GwasConfig(n=245, d=4, k=10643), P17)
+    specs = [s for s, _ in plan]
+    assert len(specs) == len(set(specs)) == 2 * 245 + 2
+    assert all(("slot", i) in specs and ("range", 256 * i, 256 * (i + 1)) in specs for i in range(245))
