@@ -66,6 +66,11 @@ def main():
         if only is None or "rot" in only:
             eng.rotate(al, 1)
             rec["rotate1_ms"] = round(timed(lambda: eng.rotate(al, 1), args.reps), 3)
+        if only is None or "rotb" in only:
+            cts = [al, bl, hg.negate(al), hg.negate(bl)]
+            eng.rotate_many(cts, 1)
+            rec["rotate1_x4_ms"] = round(timed(lambda: [eng.rotate(c, 1) for c in cts], args.reps), 3)
+            rec["rotate1_batch4_ms"] = round(timed(lambda: eng.rotate_many(cts, 1), args.reps), 3)
         if only is None or "pmul" in only:
             m = eng.mask(("slot", 3))
             rec["mult_plain_ms"] = round(timed(lambda: eng.mult_plain(al, m), args.reps), 3)
