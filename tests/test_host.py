@@ -183,3 +183,35 @@ def test_setup_mask_plan_covers_pipeline_masks():
     specs = [s for s, _ in plan]
     assert len(specs) == len(set(specs)) == 2 * 245 + 2
     assert all(("slot", i) in specs and ("range", 256 * i, 256 * (i + 1)) in specs for i in range(245))
+
+
+def test_matrix_ext_host_algebra():
+    """Host halves of the config-2 extras: generalized diagonals reproduce A v under right
+    rotations (np.roll), LS sigmoid fits, and the Newton replay converges."""
+    from paper_1902_04303_b200.matrix_ext import (generalized_diagonals, newton_alpha,
+                                                  newton_inverse_replay, periodic_vector,
+                                                  sigmoid_ls_coeffs, sigmoid_poly_eval)
+
+    rs = np.random.default_rng(0)
+    for shape in [(5, 5), (245, 5), (8, 8), (16, 4)]:
+        a = rs.standard_normal(shape)
+        v0 = rs.standard_normal(shape[1])
+        diags, big_r, big_c = generalized_diagonals(a, 512)
+        v = periodic_vector(v0, big_c, 512).real
+        y = sum(d * np.roll(v, i) for i, d in enumerate(diags))
+        assert np.allclose(y[:shape[0]], a @ v0)
+        assert np.allclose(y[big_r:big_r + shape[0]], a @ v0)
+    xs = np.linspace(-8, 8, 1001)
+    errs = [np.max(np.abs(sigmoid_poly_eval(xs, sigmoid_ls_coeffs(d)) - 1 / (1 + np.exp(-xs))))
+            for d in (3, 5, 7)]
+    assert errs[0] > errs[1] > errs[2] and errs[2] < 0.05
+    # the degree-7 least-squares fit is the reference's published sigma7, reflected
+    # (reference oracle.py:18-22 evaluates it at -x)
+    from paper_1902_04303_b200.logreg import SIGMA7_C1, SIGMA7_C3, SIGMA7_C5, SIGMA7_C7
+
+    assert np.allclose(sigmoid_ls_coeffs(7), [-SIGMA7_C1, -SIGMA7_C3, -SIGMA7_C5, -SIGMA7_C7], atol=2e-3)
+    x = rs.standard_normal((245, 5))
+    x[:, 0] = 1
+    a = x.T @ np.diag(rs.uniform(0, 0.25, 245)) @ x
+    e = [np.linalg.norm(newton_inverse_replay(a, newton_alpha(245, 5), k) @ a - np.eye(5)) for k in (1, 3, 6)]
+    assert e[0] > e[1] > e[2]
