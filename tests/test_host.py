@@ -215,3 +215,38 @@ def test_matrix_ext_host_algebra():
     a = x.T @ np.diag(rs.uniform(0, 0.25, 245)) @ x
     e = [np.linalg.norm(newton_inverse_replay(a, newton_alpha(245, 5), k) @ a - np.eye(5)) for k in (1, 3, 6)]
     assert e[0] > e[1] > e[2]
+
+
+def test_scale_gwas_layout_and_identity():
+    """Config-4 reformulation (gwas_scale): the group/block slot layout makes sum_b V_b * ct_b
+    plus a within-block sum equal X^T S, and the projector-free num/den identities equal the
+    reference's M-based statistics (oracle/replay.replay_gwas) in float64."""
+    from oracle.replay import replay_gwas
+    from paper_1902_04303_b200.data import synth_gwas_dataset
+    from paper_1902_04303_b200.gwas_scale import ScaleConfig, group_slots
+
+    ds = synth_gwas_dataset(200, 4, 100, seed=3)
+    cfg = ScaleConfig(n=200, d=4, k=100, block=32)
+    slots = 2048
+    per = slots // cfg.block
+    for g in range(2):
+        for a in range(5):
+            acc = np.zeros(slots)
+            for b in range(cfg.num_blocks()):
+                v = np.zeros(cfg.block)
+                seg = ds.X[b * 32:(b + 1) * 32, a]
+                v[:seg.size] = seg
+                acc += np.tile(v, per) * group_slots(ds.S, g, b, cfg, slots)
+            got = acc.reshape(per, cfg.block).sum(axis=1)
+            want = ds.X[:, a] @ ds.S[:, g * per:(g + 1) * per]
+            assert np.allclose(got[:want.size], want)
+    ref = replay_gwas(ds.X, ds.y, ds.S)
+    x, w, zp, s = ds.X, ref["w"], ref["z_prime"], ds.S
+    g_inv = np.linalg.inv(x.T @ x)
+    a = w * zp
+    t = x.T @ s
+    c = g_inv @ t
+    num = a @ s - (x @ g_inv).T @ a @ t
+    den = (w @ (s * s)) - 2 * np.einsum("aj,aj->j", x.T @ (w[:, None] * s), c) \
+        + np.einsum("aj,ab,bj->j", c, x.T @ (w[:, None] * x), c)
+    assert np.allclose(num, ref["numerator"]) and np.allclose(den, ref["denominator"])
