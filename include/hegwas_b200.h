@@ -128,6 +128,19 @@ int hg_ct_mult(hg_ctx* ctx, const hg_key* evk, const uint32_t* a0, const uint32_
 typedef struct hg_ctprep hg_ctprep;
 int hg_ct_prepare(hg_ctx* ctx, const uint32_t* c0, const uint32_t* c1, int level, void* stream,
                   hg_ctprep** out);
+/* As hg_ct_prepare, with the NTT basis widened for a sum of `terms` such products
+ * (hg_ct_inner_prepared). */
+int hg_ct_prepare_sum(hg_ctx* ctx, const uint32_t* c0, const uint32_t* c1, int level, int terms,
+                      void* stream, hg_ctprep** out);
+/* nq inner products over nb ciphertexts: out[q] = rescale(relinearise(sum_b a[q*nb+b] (x) b_b)),
+ * i.e. sum_b HeEngine.mult without a relinearisation/rescale per term: the tensors are summed
+ * exactly in the NTT domain (every b's forward residues computed once for all q), then one
+ * inverse NTT, CRT and key switch (+ rescale by rescale_bits) per q.  The a operands must be
+ * prepared at `level` with hg_ct_prepare_sum(..., terms >= nb).  No reference counterpart
+ * (config-4 weighted sums, paper_1902_04303_b200/gwas_scale.py). */
+int hg_ct_inner_prepared(hg_ctx* ctx, const hg_key* evk, int nq, int nb, const hg_ctprep* const* a,
+                         const uint32_t* const* b0s, const uint32_t* const* b1s, int level,
+                         int rescale_bits, uint32_t* const* out0s, uint32_t* const* out1s, void* stream);
 int hg_ctprep_destroy(hg_ctprep* prep);
 size_t hg_ctprep_device_bytes(const hg_ctprep* prep);
 /* hg_ct_mult with the left operand prepared (same output, bit for bit). */

@@ -56,3 +56,16 @@ def mult_plain(c0, c1, m, m_bits, level, n):
     """ckks.mult_plain ring part (ckks.py:154-161)."""
     mm = R.reduce_to(m, level) if m_bits >= level else R.lift_centered_to(m, m_bits, level)
     return R.mul(c0, mm, level, n), R.mul(c1, mm, level, n)
+
+
+def engine_inner(a_list, b_list, level, evk_b, evk_a, big_l, log_p, n):
+    """sum_b a_b (x) b_b relinearised and rescaled ONCE (HeEngine.inner_product; no reference
+    counterpart -- composed from the reference's own mul / _keyswitch / divide_round,
+    ckks.py:166-194, 215-219): the three tensor parts are summed mod 2^level first."""
+    d0 = d1 = d2 = [0] * n
+    for (a0, a1), (b0, b1) in zip(a_list, b_list):
+        d0 = R.add(d0, R.mul(a0, b0, level, n), level)
+        d1 = R.add(d1, R.add(R.mul(a0, b1, level, n), R.mul(a1, b0, level, n), level), level)
+        d2 = R.add(d2, R.mul(a1, b1, level, n), level)
+    e0, e1 = keyswitch(d2, evk_b, evk_a, level, big_l, n)
+    return rescale(R.add(d0, e0, level), R.add(d1, e1, level), log_p, level)

@@ -824,17 +824,27 @@ struct hg_ctprep {
     bool prescaled = false;      // residues carry the tensor CRT constants (scale_rows_kernel)
 };
 
-static int tensor_primes(hg_ctx* ctx, int level) {
-    // both operands centered at `level` bits, d1 is a sum of two products
-    return primes_for_product(ctx, 2.0 * (level - 1) + 1, level);
+
+// both operands centered at `level` bits, d1 is a sum of two products; a sum of `terms`
+// tensor products grows by ceil(log2 terms) bits
+static int tensor_sum_primes(hg_ctx* ctx, int level, int terms) {
+    int extra = 0;
+    while ((1 << extra) < terms) ++extra;
+    return primes_for_product(ctx, 2.0 * (level - 1) + 1 + extra, level);
 }
 
 extern "C" int hg_ct_prepare(hg_ctx* ctx, const uint32_t* c0, const uint32_t* c1, int level,
                              void* stream, hg_ctprep** out) {
-    if (!ctx || !c0 || !c1 || !out || level < 2) return hg_fail(HG_EINVAL, "hg_ct_prepare: bad arguments");
+    return hg_ct_prepare_sum(ctx, c0, c1, level, 1, stream, out);
+}
+
+extern "C" int hg_ct_prepare_sum(hg_ctx* ctx, const uint32_t* c0, const uint32_t* c1, int level,
+                                 int terms, void* stream, hg_ctprep** out) {
+    if (!ctx || !c0 || !c1 || !out || level < 2 || terms < 1)
+        return hg_fail(HG_EINVAL, "hg_ct_prepare: bad arguments");
     cudaStream_t st = (cudaStream_t)stream;
     const int N = ctx->N;
-    const int P = tensor_primes(ctx, level);
+    const int P = tensor_sum_primes(ctx, level, terms);
     if (P < 0) return hg_fail(HG_ERANGE, "tensor product exceeds the NTT prime basis");
     hg_ctprep* pr = new hg_ctprep();
     pr->ctx = ctx;
@@ -918,6 +928,124 @@ extern "C" int hg_ct_mult_prepared(hg_ctx* ctx, const hg_key* evk, const hg_ctpr
     rc = launch_crt(ctx, res.u32(), 3, P, 0, level, outs, st, nullptr, a->prescaled);
     if (rc) return rc;
     return ct_mult_finish(ctx, evk, d0, d1, d2, e0, e1, level, rescale_bits, out0, out1, st);
+}
+
+// ---- inner products over prepared operands ------------------------------------------------------
+// acc[q] += A[q][b] (x) B[b] for QG weight sets at once: one thread per (prime, coefficient),
+// the B residues of every b read once, the accumulators in registers.  Montgomery products of
+// operands reduced to [0, 2p) (the same products the fused tensor kernel forms), sums kept in
+// [0, 2p) and reduced to [0, p) on the way out.
+template <int QG>
+__global__ void __launch_bounds__(256) inner_acc_kernel(const uint32_t* const* __restrict__ a_tab, int nq,
+                                                        int nb, const uint32_t* __restrict__ resb,
+                                                        uint32_t* __restrict__ out, int P, int N,
+                                                        const PrimeInfo* __restrict__ pinfo) {
+    const int j = blockIdx.y;
+    const PrimeInfo pi = pinfo[j];
+    const uint32_t p = pi.p, p2 = p << 1;
+    const size_t plane = (size_t)P * N;
+    const int q0 = blockIdx.z * QG;
+    const int nqg = nq - q0 < QG ? nq - q0 : QG;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+        const size_t o = (size_t)j * N + i;
+        uint32_t acc[QG][3];
+#pragma unroll
+        for (int q = 0; q < QG; ++q) acc[q][0] = acc[q][1] = acc[q][2] = 0;
+        for (int b = 0; b < nb; ++b) {
+            uint32_t b0 = resb[(size_t)(2 * b) * plane + o], b1 = resb[(size_t)(2 * b + 1) * plane + o];
+            b0 = min(b0, b0 - p2); b0 = min(b0, b0 - p2);     // [0, 4p) -> [0, 2p)
+            b1 = min(b1, b1 - p2); b1 = min(b1, b1 - p2);
+#pragma unroll
+            for (int q = 0; q < QG; ++q) {
+                if (q >= nqg) break;
+                const uint32_t* a = a_tab[(size_t)(q0 + q) * nb + b];
+                uint32_t a0 = a[o], a1 = a[plane + o];
+                a0 = min(a0, a0 - p2); a0 = min(a0, a0 - p2);
+                a1 = min(a1, a1 - p2); a1 = min(a1, a1 - p2);
+                uint32_t t;
+                t = acc[q][0] + mont_mul(a0, b0, p, pi.pinv_neg);
+                acc[q][0] = min(t, t - p2);
+                t = acc[q][1] + mont_mul(a0, b1, p, pi.pinv_neg);
+                t = min(t, t - p2);
+                t += mont_mul(a1, b0, p, pi.pinv_neg);
+                acc[q][1] = min(t, t - p2);
+                t = acc[q][2] + mont_mul(a1, b1, p, pi.pinv_neg);
+                acc[q][2] = min(t, t - p2);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < QG; ++q) {
+            if (q >= nqg) break;
+            uint32_t* dst = out + (size_t)(q0 + q) * 3 * plane + o;
+#pragma unroll
+            for (int r = 0; r < 3; ++r) dst[(size_t)r * plane] = min(acc[q][r], acc[q][r] - p);
+        }
+    }
+}
+
+extern "C" int hg_ct_inner_prepared(hg_ctx* ctx, const hg_key* evk, int nq, int nb,
+                                    const hg_ctprep* const* a, const uint32_t* const* b0s,
+                                    const uint32_t* const* b1s, int level, int rescale_bits,
+                                    uint32_t* const* out0s, uint32_t* const* out1s, void* stream) {
+    if (!ctx || !evk || nq < 1 || nb < 1 || !a || !b0s || !b1s || !out0s || !out1s ||
+        evk->level != level || rescale_bits < 0 || rescale_bits >= level)
+        return hg_fail(HG_EINVAL, "hg_ct_inner_prepared: bad arguments");
+    const int P = a[0]->P;
+    const bool prescaled = a[0]->prescaled;
+    for (int k = 0; k < nq * nb; ++k)
+        if (!a[k] || a[k]->ctx != ctx || a[k]->level != level || a[k]->P != P || a[k]->prescaled != prescaled)
+            return hg_fail(HG_EINVAL, "hg_ct_inner_prepared: operands differ in level / basis");
+    if (P < tensor_sum_primes(ctx, level, nb))
+        return hg_fail(HG_EINVAL, "hg_ct_inner_prepared: operands prepared for fewer summed terms");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int N = ctx->N;
+    const int W = words_for_bits(level);
+    const size_t plane = (size_t)P * N;
+    Scratch resb(st), acc(st), tab(st), buf(st);
+    HG_CUDA_TRY(resb.alloc((size_t)2 * nb * plane * 4));
+    HG_CUDA_TRY(acc.alloc((size_t)3 * nq * plane * 4));
+    HG_CUDA_TRY(tab.alloc((size_t)nq * nb * sizeof(uint32_t*)));
+    HG_CUDA_TRY(buf.alloc((size_t)5 * W * N * 4));
+    std::vector<const uint32_t*> host(nq * nb);
+    for (int k = 0; k < nq * nb; ++k) host[k] = a[k]->d_res;
+    HG_CUDA_TRY(cudaMemcpyAsync(tab.u32(), host.data(), host.size() * sizeof(uint32_t*),
+                                cudaMemcpyHostToDevice, st));
+    // forward residues of every b: [nb][2][P][N]
+    for (int b0 = 0; b0 < nb; b0 += 2) {
+        const int g = nb - b0 < 2 ? nb - b0 : 2;
+        OperandSet ops{};
+        for (int k = 0; k < g; ++k) {
+            ops.words[2 * k] = b0s[b0 + k]; ops.bits[2 * k] = level; ops.is_signed[2 * k] = 1;
+            ops.words[2 * k + 1] = b1s[b0 + k]; ops.bits[2 * k + 1] = level; ops.is_signed[2 * k + 1] = 1;
+        }
+        if (int rc = launch_modup(ctx, ops, 2 * g, P, resb.u32() + (size_t)2 * b0 * plane, 0, st)) return rc;
+    }
+    if (int rc = hg_ntt_launch(ctx, resb.u32(), 2 * nb * P, P, 0, true, st)) return rc;
+    {
+        constexpr int QG = 4;
+        dim3 grid = pw_grid(N, P);
+        grid.z = (nq + QG - 1) / QG;
+        const int tpw = hg_timer_begin(ctx, st, HG_K_POINTWISE);
+        inner_acc_kernel<QG><<<grid, 256, 0, st>>>(reinterpret_cast<const uint32_t* const*>(tab.u32()), nq, nb,
+                                                   resb.u32(), acc.u32(), P, N, ctx->d_pinfo);
+        hg_timer_end(ctx, tpw, st, HG_K_POINTWISE, (double)nq * nb * 4.0 * plane * 4);
+        HG_LAUNCH_CHECK(ctx);
+    }
+    if (int rc = hg_ntt_launch(ctx, acc.u32(), 3 * nq * P, P, 0, false, st)) return rc;
+    uint32_t* d0 = buf.u32();
+    uint32_t* d1 = d0 + (size_t)W * N;
+    uint32_t* d2 = d1 + (size_t)W * N;
+    uint32_t* e0 = d2 + (size_t)W * N;
+    uint32_t* e1 = e0 + (size_t)W * N;
+    for (int q = 0; q < nq; ++q) {
+        OutSet outs{};
+        outs.out[0] = d0; outs.out[1] = d1; outs.out[2] = d2;
+        if (int rc = launch_crt(ctx, acc.u32() + (size_t)3 * q * plane, 3, P, 0, level, outs, st, nullptr, prescaled))
+            return rc;
+        if (int rc = ct_mult_finish(ctx, evk, d0, d1, d2, e0, e1, level, rescale_bits, out0s[q], out1s[q], st))
+            return rc;
+    }
+    return HG_OK;
 }
 
 extern "C" int hg_ct_automorph(hg_ctx* ctx, const hg_key* key, const uint32_t* c0,

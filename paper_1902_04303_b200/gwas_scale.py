@@ -36,7 +36,8 @@ from .errors import DimensionError, InputError
 from .gwas import assemble_result, compute_z, inverse_slots
 from .keys import PublicKey, SecretKey
 from .logreg import LogRegInputs, hom_logreg
-from .matrix import CPMatrix, cp_matmul, cp_matvec, duplicate_many, pack_cp, replicate, rotate_sum, sum_terms
+from .matrix import (CPMatrix, cp_matmul, cp_matvec, duplicate_many, pack_cp, replicate, rotate_sum,
+                     rotate_sum_many, sum_terms)
 from .matrix_ext import xt_vec, xt_w_x
 from .params import CkksParams
 
@@ -91,6 +92,13 @@ class ScaleSetup:
     v_wx: list[list[Ciphertext]]    # block weights of W X columns [d+1][blocks]
     v_w: list[Ciphertext]           # block weights of w           [blocks]
     v_a: list[Ciphertext]           # block weights of a           [blocks]
+    # fused path (HeEngine.inner_product): the same block weights as HBM-resident NTT residues,
+    # X / W X weights brought down to one level (their sums only feed the (d+1)-dim algebra)
+    fused: bool = False
+    p_xwx: list | None = None       # [2(d+1)][blocks] at level_xwx
+    p_w: list | None = None         # [1][blocks] at level_xwx - log_p (the squares' level)
+    p_a: list | None = None         # [1][blocks]
+    level_xwx: int = 0
 
 
 @dataclass
@@ -114,9 +122,15 @@ def group_slots(s_mat: np.ndarray, g: int, b: int, config: ScaleConfig, slots: i
 
 def pack_snp_group(s_mat: np.ndarray, g: int, config: ScaleConfig, params: CkksParams,
                    pk: PublicKey, rng) -> list[Ciphertext]:
-    """Ciphertexts of SNP group g, one per sample block."""
-    return [encrypt_values(group_slots(s_mat, g, b, config, params.slot_count), params.log_p, pk, params, rng)
-            for b in range(config.num_blocks())]
+    """Ciphertexts of SNP group g, one per sample block.  With a CUDA torch.Generator the
+    encoding runs on the GPU too (encoding.encode_device; config 4 has no reference run)."""
+    from .ckks import _is_torch_generator, encrypt
+    from .encoding import encode_device
+
+    slots = [group_slots(s_mat, g, b, config, params.slot_count) for b in range(config.num_blocks())]
+    if _is_torch_generator(rng):
+        return [encrypt(encode_device(v, params.log_p, params), pk, params, rng) for v in slots]
+    return [encrypt_values(v, params.log_p, pk, params, rng) for v in slots]
 
 
 def encrypt_scale_inputs(X: np.ndarray, y: np.ndarray, s_mat: np.ndarray, config: ScaleConfig,
@@ -163,7 +177,10 @@ def _replicated_entries(engine: HeEngine, m: CPMatrix) -> list[list[Ciphertext]]
     return [[cols[c][r] for c in range(m.cols_logical)] for r in range(m.rows)]
 
 
-def compute_scale_setup(engine: HeEngine, inputs: ScaleInputs) -> ScaleSetup:
+def compute_scale_setup(engine: HeEngine, inputs: ScaleInputs, fused: bool = True) -> ScaleSetup:
+    """Logistic fit, w, z', a, b = H^T a, replicated G / A2 / b entries and the block weights.
+    With ``fused`` (default) the block weights are kept as resident NTT residues for
+    HeEngine.inner_product (one relinearisation per weighted sum instead of one per block)."""
     cfg = inputs.config.check(engine.params)
     lr = inputs.logreg
     beta, p = hom_logreg(engine, lr, cfg.kappa)
@@ -177,7 +194,7 @@ def compute_scale_setup(engine: HeEngine, inputs: ScaleInputs) -> ScaleSetup:
     b = xt_vec(engine, h, a)
     wx = [engine.mult(col, w_m) for col in lr.X.cols]
     a2 = xt_w_x(engine, lr.X, w_m)
-    return ScaleSetup(
+    setup = ScaleSetup(
         beta=beta, p=p, w=w_m, z_prime=z_prime, a=a,
         b_rep=replicate(engine, b, cfg.d + 1),
         g_rep=_replicated_entries(engine, lr.XtX_inv),
@@ -187,6 +204,20 @@ def compute_scale_setup(engine: HeEngine, inputs: ScaleInputs) -> ScaleSetup:
         v_w=block_weights(engine, w_m, cfg),
         v_a=block_weights(engine, a, cfg),
     )
+    if fused and hasattr(engine, "inner_product"):
+        from .ckks import mod_down
+
+        nb = cfg.num_blocks()
+        lvl = min(setup.v_wx[0][0].level_bits, setup.v_w[0].level_bits)
+        setup.level_xwx = lvl
+        setup.p_xwx = [[engine.prepare_sum(mod_down(v, lvl), nb) for v in row]
+                       for row in setup.v_x + setup.v_wx]
+        lw = lvl - engine.params.log_p
+        setup.p_w = [[engine.prepare_sum(mod_down(v, lw), nb) for v in setup.v_w]]
+        setup.p_a = [[engine.prepare_sum(v, nb) for v in setup.v_a]]
+        setup.v_x = setup.v_wx = setup.v_w = setup.v_a = None   # the prepared copies replace them
+        setup.fused = True
+    return setup
 
 
 def compute_scale_group(engine: HeEngine, setup: ScaleSetup, cts: list[Ciphertext], config: ScaleConfig,
@@ -194,10 +225,22 @@ def compute_scale_group(engine: HeEngine, setup: ScaleSetup, cts: list[Ciphertex
     """num and den of one SNP group (SNP pos at slot pos B + B - 1)."""
     blk = config.block
     d1 = config.d + 1
-    t = [weighted_sum(engine, setup.v_x[a], cts, blk) for a in range(d1)]
-    u = [weighted_sum(engine, setup.v_wx[a], cts, blk) for a in range(d1)]
-    q = weighted_sum(engine, setup.v_w, cts, blk, square=True)
-    at_s = weighted_sum(engine, setup.v_a, cts, blk)
+    if setup.fused:
+        from .ckks import _mod_down_view
+
+        tu = engine.inner_product(setup.p_xwx, cts)                      # 2(d+1) sums, one pass
+        views = [_mod_down_view(c, setup.level_xwx) for c in cts]
+        sq = [engine.mult(v, v) for v in views]
+        q_raw = engine.inner_product(setup.p_w, sq)[0]
+        a_raw = engine.inner_product(setup.p_a, cts)[0]
+        tu = rotate_sum_many(engine, tu, 1, blk)
+        t, u = tu[:d1], tu[d1:]
+        q, at_s = (rotate_sum(engine, x, 1, blk) for x in (q_raw, a_raw))
+    else:
+        t = [weighted_sum(engine, setup.v_x[a], cts, blk) for a in range(d1)]
+        u = [weighted_sum(engine, setup.v_wx[a], cts, blk) for a in range(d1)]
+        q = weighted_sum(engine, setup.v_w, cts, blk, square=True)
+        at_s = weighted_sum(engine, setup.v_a, cts, blk)
     # c = G t ; den = q - 2 u.c + c^T A2 c ; num = a^T S - b.t
     c = [sum_terms(engine, [engine.mult(setup.g_rep[r][s], t[s]) for s in range(d1)]) for r in range(d1)]
     uc = sum_terms(engine, [engine.mult(u[r], c[r]) for r in range(d1)])
@@ -211,8 +254,8 @@ def compute_scale_group(engine: HeEngine, setup: ScaleSetup, cts: list[Ciphertex
     return GroupOutput(index=index, num_ct=num, den_ct=den)
 
 
-def compute_scale_gwas(engine: HeEngine, inputs: ScaleInputs):
-    setup = compute_scale_setup(engine, inputs)
+def compute_scale_gwas(engine: HeEngine, inputs: ScaleInputs, fused: bool = True):
+    setup = compute_scale_setup(engine, inputs, fused)
     cfg = inputs.config
     outs = [compute_scale_group(engine, setup, inputs.group_source(g), cfg, g)
             for g in range(cfg.num_groups(engine.params))]

@@ -427,6 +427,28 @@ def small_element(n: int, bits: int, values) -> RingElement:
     return el
 
 
+def signed64_element(n: int, bits: int, values) -> RingElement:
+    """Element from signed int64 coefficients (|c| < 2^62) held in a device tensor, with a
+    64-bit (two-word) compact view: the device-side twin of RingElement.from_int64."""
+    torch = _torch()
+    vals = values.to(torch.int64)
+    w = words_for(bits)
+    if w < 2:
+        raise ParameterError("signed64_element needs at least 64-bit moduli")
+    out = torch.empty((w, n), dtype=torch.int32, device=vals.device)
+    low = vals & 0xFFFFFFFF
+    out[0] = torch.where(low >= 2 ** 31, low - 2 ** 32, low).to(torch.int32)
+    out[1] = (vals >> 32).to(torch.int32)
+    if w > 2:
+        out[2:] = torch.where(vals < 0, -1, 0).to(torch.int32).unsqueeze(0)
+    rem = bits & 31
+    if rem:
+        out[w - 1] = (out[w - 1].to(torch.int64) & ((1 << rem) - 1)).to(torch.int32)
+    el = RingElement(n, bits, words=out)
+    el.compact_words, el.compact_bits = out[:2].clone(), 64
+    return el
+
+
 def uniform_element(n: int, bits: int, gen) -> RingElement:
     """Uniform residues mod 2^bits drawn on the device."""
     torch = _torch()

@@ -4,8 +4,10 @@ levels that exercise one and two CRT column jobs, word-aligned windows and both 
 Both arms also pass the oracle/golden parity tests; this one pins the fused epilogues' corner
 cases (the cross-proxy race it once caught showed up in a handful of 8-coefficient groups)."""
 import os
+import random
 import sys
 
+import numpy as np
 import pytest
 
 pytestmark = pytest.mark.gpu
@@ -18,3 +20,34 @@ def test_fused_matches_unfused(tmp_path):
 
     for _ in range(2):   # repeat: races show up as run-to-run differences
         assert fused_check.compare(quick=True, workdir=str(tmp_path)) == 0
+
+
+@pytest.mark.parametrize("nq,nb,drop", [(1, 1, 0), (3, 5, 0), (6, 7, 90)])
+def test_inner_product_bit_exact_vs_oracle(nq, nb, drop):
+    """HeEngine.inner_product (hg_ct_inner_prepared: tensors summed in the NTT domain, one
+    relinearisation + rescale per output) equals the oracle's sum-then-relinearise, bit for
+    bit; `drop` puts the ciphertexts above the weights' level (mod-down views)."""
+    import paper_1902_04303_b200 as hg
+    from oracle import ckks_oracle as C
+
+    params = hg.CkksParams(log_n=9, log_l=600, log_p=45, log_p_small=30, h=32)
+    sk, pk, evk, rot = hg.keygen(params, seed=5)
+    eng = hg.HeEngine(params, evk, rot)
+    rng = random.Random(8)
+    enc = lambda: hg.encrypt_values([complex(rng.uniform(-1, 1), rng.uniform(-1, 1))  # noqa: E731
+                                     for _ in range(params.slot_count)], params.log_p, pk, params, rng)
+    cts = [enc() for _ in range(nb)]
+    ws = [[hg.mod_down(enc(), params.log_l - drop) for _ in range(nb)] for _ in range(nq)]
+    prepared = [[eng.prepare_sum(w, nb) for w in row] for row in ws]
+    outs = eng.inner_product(prepared, cts)
+    lv = params.log_l - drop
+    for row, out in zip(ws, outs):
+        want = C.engine_inner([(w.c0.coeffs, w.c1.coeffs) for w in row],
+                              [(hg.mod_down(c, lv).c0.coeffs, hg.mod_down(c, lv).c1.coeffs) for c in cts],
+                              lv, evk.b.coeffs, evk.a.coeffs, params.log_l, params.log_p, params.n)
+        assert (out.c0.coeffs, out.c1.coeffs) == want
+        assert out.level_bits == lv - params.log_p
+    # and it decrypts to the sum of slotwise products
+    got = hg.decrypt_values(outs[0], sk)
+    exp = sum(hg.decrypt_values(w, sk) * hg.decrypt_values(c, sk) for w, c in zip(ws[0], cts))
+    assert np.max(np.abs(got - exp)) < 1e-5 * nb
