@@ -190,6 +190,8 @@ int hg_kernel_stats(hg_ctx* ctx, int kind, double* ms, long long* launches, doub
  * hg_pool_bytes: reserved bytes (in_use = 0) or bytes held by live objects (in_use = 1). */
 int hg_pool_reserve(hg_ctx* ctx, size_t bytes, void* stream);
 size_t hg_pool_bytes(const hg_ctx* ctx, int in_use);
+/* Return the arena slabs that hold no live object to the device; returns the bytes freed. */
+size_t hg_pool_trim(hg_ctx* ctx);
 
 #ifdef __cplusplus
 }

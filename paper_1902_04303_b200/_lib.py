@@ -81,6 +81,7 @@ SIGNATURES = {
     "hg_poly_sum": (_i, [_vp, _vp, ctypes.POINTER(ctypes.c_void_p), _i, _i, _vp]),
     "hg_pool_reserve": (_i, [_vp, ctypes.c_size_t, _vp]),
     "hg_pool_bytes": (ctypes.c_size_t, [_vp, _i]),
+    "hg_pool_trim": (ctypes.c_size_t, [_vp]),
     "hg_kernel_stats": (_i, [_vp, _i, ctypes.POINTER(ctypes.c_double),
                              ctypes.POINTER(ctypes.c_longlong), ctypes.POINTER(ctypes.c_double)]),
 }
@@ -127,10 +128,7 @@ def check_alloc(call, evict=None):
     share the HBM and neither can take memory the other has cached."""
     rc = call()
     if rc == HG_ENOMEM:
-        import torch
-
-        torch.cuda.synchronize()
-        torch.cuda.empty_cache()
+        release_device_memory()
         rc = call()
         if rc == HG_ENOMEM and evict is not None:
             evict()
@@ -187,6 +185,9 @@ class Context:
         """Reserve one more device-arena slab of nbytes (hg_pool_reserve)."""
         check(self.lib.hg_pool_reserve(self.handle, int(nbytes), self.stream()))
 
+    def pool_trim(self) -> int:
+        return int(self.lib.hg_pool_trim(self.handle))
+
     def pool_bytes(self, in_use: bool = False) -> int:
         return int(self.lib.hg_pool_bytes(self.handle, 1 if in_use else 0))
 
@@ -206,6 +207,27 @@ class Context:
 
 
 _contexts: dict[tuple[int, int], Context] = {}
+
+
+def release_device_memory() -> int:
+    """Hand back device memory held only by caches: prepared keys of switching keys that no
+    longer exist, arena slabs with no live object, torch's unused cached blocks.  Called on
+    an allocation failure before one retry (the library arena and torch's caching allocator
+    share the HBM and neither can take memory the other holds)."""
+    import torch
+
+    freed = 0
+    try:
+        from .ckks import KEY_CACHE
+
+        KEY_CACHE.purge_dead()
+    except Exception:
+        pass
+    torch.cuda.synchronize()
+    for ctx in list(_contexts.values()):
+        freed += ctx.pool_trim()
+    torch.cuda.empty_cache()
+    return freed
 
 
 def get_context(log_n: int, device: int | None = None) -> Context:

@@ -221,6 +221,30 @@ extern "C" int hg_pool_reserve(hg_ctx* ctx, size_t bytes, void* stream) {
     return hg_arena_grow(ctx, bytes);
 }
 
+extern "C" size_t hg_pool_trim(hg_ctx* ctx) {
+    if (!ctx) return 0;
+    std::lock_guard<std::mutex> g(ctx->arena.mu);
+    DeviceArena& a = ctx->arena;
+    size_t released = 0;
+    std::vector<DeviceArena::Slab> keep;
+    std::vector<int> remap(a.slabs.size(), -1);
+    for (size_t i = 0; i < a.slabs.size(); ++i) {
+        auto& sl = a.slabs[i];
+        const bool empty = sl.free.size() == 1 && sl.free.begin()->first == 0 && sl.free.begin()->second == sl.size;
+        if (empty) {
+            cudaFree(sl.base);
+            released += sl.size;
+        } else {
+            remap[i] = (int)keep.size();
+            keep.push_back(std::move(sl));
+        }
+    }
+    for (auto& kv : a.live) kv.second.first = remap[kv.second.first];
+    a.slabs = std::move(keep);
+    a.reserved -= released;
+    return released;
+}
+
 extern "C" size_t hg_pool_bytes(const hg_ctx* ctx, int in_use) {
     if (!ctx) return 0;
     return in_use ? ctx->arena.in_use : ctx->arena.reserved;

@@ -127,7 +127,11 @@ def reserve_device_bytes(nbytes: int, keep_free: int) -> int:
 
 def empty_words(bits: int, n: int):
     torch = _torch()
-    return torch.empty((words_for(bits), n), dtype=torch.int32, device=_device())
+    try:
+        return torch.empty((words_for(bits), n), dtype=torch.int32, device=_device())
+    except torch.OutOfMemoryError:
+        _lib.release_device_memory()   # caches of the library arena / dead keys, then retry
+        return torch.empty((words_for(bits), n), dtype=torch.int32, device=_device())
 
 
 def _ctx(n: int) -> _lib.Context:

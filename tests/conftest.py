@@ -25,3 +25,22 @@ def golden():
         return cache[name]
 
     return get
+
+
+@pytest.fixture(autouse=True, scope="module")
+def _release_device_caches():
+    """GPU test modules build many engines; hand their cached device memory (prepared keys
+    of dead engines, empty arena slabs, torch's cache) back between modules."""
+    yield
+    try:
+        import torch
+
+        if torch.cuda.is_available():
+            import gc
+
+            from paper_1902_04303_b200 import _lib
+
+            gc.collect()
+            _lib.release_device_memory()
+    except Exception:
+        pass
