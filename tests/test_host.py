@@ -250,3 +250,28 @@ def test_scale_gwas_layout_and_identity():
     den = (w @ (s * s)) - 2 * np.einsum("aj,aj->j", x.T @ (w[:, None] * s), c) \
         + np.einsum("aj,ab,bj->j", c, x.T @ (w[:, None] * x), c)
     assert np.allclose(num, ref["numerator"]) and np.allclose(den, ref["denominator"])
+
+
+def test_cli_io_audit_and_manifest(tmp_path):
+    """CLI host plumbing: audited atomic file access, the reference encrypt manifest read into
+    a GwasConfig, and the argument parser (no GPU work)."""
+    import json
+
+    from paper_1902_04303_b200 import P17, cli
+    from paper_1902_04303_b200 import io as hio
+
+    with hio.audit_file_access() as audit:
+        hio.write_json(tmp_path / "a" / "x.json", {"b": 1, "a": [1.5]})
+        assert hio.read_json(tmp_path / "a" / "x.json") == {"a": [1.5], "b": 1}
+        hio.write_tsv(tmp_path / "t.tsv", ["k", "v"], [("s0", 0.25)])
+    assert [m for m, _ in audit] == ["write", "read", "write"]
+    assert hio.read_tsv(tmp_path / "t.tsv") == (["k", "v"], [["s0", "0.25"]])
+    assert not list(tmp_path.glob("**/*.tmp"))
+    gold = os.path.join(ROOT, "tests", "golden", "cli_toy")
+    m = json.load(open(os.path.join(gold, "encrypted", "manifest.json")))
+    params = cli._load_params(os.path.join(gold, "keys"))
+    cfg = cli._config_from_manifest(m, params)
+    assert (cfg.n, cfg.d, cfg.k, cfg.num_batches) == (8, 4, 16, 1)
+    assert len(m["files"]["batches"][0]) == 8
+    args = cli.build_parser().parse_args(["keygen", "--log-n", "17", "--log-l", "1700", "--outdir", "x"])
+    assert cli._params(args).log_n == P17.log_n
