@@ -128,6 +128,15 @@ int hg_ct_mult(hg_ctx* ctx, const hg_key* evk, const uint32_t* a0, const uint32_
 typedef struct hg_ctprep hg_ctprep;
 int hg_ct_prepare(hg_ctx* ctx, const uint32_t* c0, const uint32_t* c1, int level, void* stream,
                   hg_ctprep** out);
+/* `count` independent hg_ct_mult_prepared products (a[i] (x) b_i -> out_i), two per group of
+ * launches so rows of a prime share twiddle loads and the persistent kernels get twice the
+ * work per launch; outputs identical to hg_ct_mult_prepared's.  Replaces the per-term
+ * HeEngine.mult of cp_rep_matmul (matrix.py:173-193) over the 245 duplicated projector
+ * columns. */
+int hg_ct_mult_prepared_batch(hg_ctx* ctx, const hg_key* evk, int count, const hg_ctprep* const* a,
+                              const uint32_t* const* b0s, const uint32_t* const* b1s, int level,
+                              int rescale_bits, uint32_t* const* out0s, uint32_t* const* out1s,
+                              void* stream);
 /* As hg_ct_prepare, with the NTT basis widened for a sum of `terms` such products
  * (hg_ct_inner_prepared). */
 int hg_ct_prepare_sum(hg_ctx* ctx, const uint32_t* c0, const uint32_t* c1, int level, int terms,
