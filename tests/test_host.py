@@ -175,6 +175,20 @@ def test_mask_multi_scale_encode_is_bit_identical():
                     assert np.array_equal(host[1], want), (log_n, spec, s)
 
 
+def test_mask_batch_encode_is_bit_identical():
+    """Masks encoded in one 2-D FFT (encode_masks_batch) equal the per-mask encodes."""
+    from paper_1902_04303_b200 import CkksParams
+    from paper_1902_04303_b200.encoding import encode_mask_scales, encode_masks_batch
+
+    params = CkksParams(log_n=14, log_l=1700, log_p=45, log_p_small=30)
+    specs = [("slot", 0), ("slot", 200), ("range", 256, 512), ("range_value", 0, 245, 0.5), ("slot", 8191)]
+    batch = encode_masks_batch(specs, (30, 45), params)
+    for spec, got in zip(specs, batch):
+        want = encode_mask_scales(spec, (30, 45), params)
+        for g, w in zip(got, want):
+            assert g[0] == w[0] and g[1] == w[1] and np.array_equal(g[2], w[2])
+
+
 def test_setup_mask_plan_covers_pipeline_masks():
     from paper_1902_04303_b200 import P17
     from paper_1902_04303_b200.gwas import GwasConfig, setup_masks
