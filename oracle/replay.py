@@ -66,3 +66,40 @@ def finalize(num, den):
     se[ok] = np.sqrt(1.0 / den[ok])
     pv[ok] = [math.erfc(abs(e) * math.sqrt(d) / math.sqrt(2.0)) for e, d in zip(eff[ok], den[ok])]
     return eff, se, pv
+
+
+def oracle_modified(X, y, S, beta, p):
+    """Cleartext semi-parallel statistics with the exact 1/w and the unweighted projector
+    M = I - X (X^T X)^-1 X^T (reference oracle.py:141-153 gwas_modified_parts /
+    oracle_gwas_modified); returns (numerator, denominator)."""
+    X, y, S, p = (np.asarray(a, dtype=float) for a in (X, y, S, p))
+    w = p * (1.0 - p)
+    z = X @ beta + (y - p) / w
+    M = np.eye(X.shape[0]) - X @ np.linalg.inv(X.T @ X) @ X.T
+    zp, sp = M @ z, M @ S
+    return (w * zp) @ sp, w @ (sp * sp)
+
+
+def oracle_original(X, y, S, beta, p):
+    """The original (weighted) semi-parallel statistics: S* = S - X (X^T W X)^-1 X^T W S
+    (reference oracle.py:128-138); returns (numerator, denominator)."""
+    X, y, S, p = (np.asarray(a, dtype=float) for a in (X, y, S, p))
+    w = p * (1.0 - p)
+    z = X @ beta + (y - p) / w
+    proj = X @ (np.linalg.inv(X.T @ (w[:, None] * X)) @ (X.T * w))
+    zs, ss = z - proj @ z, S - proj @ S
+    return (w * zs) @ ss, w @ (ss * ss)
+
+
+def accuracy(reference, test, thresholds=(0.1, 0.01, 0.005)) -> dict:
+    """Entry-difference counts per threshold and the least-squares fit line (the paper's
+    accuracy methodology, reference oracle.py:207-220)."""
+    reference = np.asarray(reference, dtype=float)
+    test = np.asarray(test, dtype=float)
+    diff = np.abs(test - reference)
+    slope, intercept = np.polyfit(reference, test, 1) if reference.size >= 2 else (1.0, 0.0)
+    return {"entries": int(reference.size),
+            "above": {str(t): int(np.sum(diff > t)) for t in thresholds},
+            "pct_within": {str(t): round(100.0 * float(np.mean(diff <= t)), 2) for t in thresholds},
+            "max_abs_diff": float(diff.max()) if diff.size else 0.0,
+            "fit": {"slope": float(slope), "intercept": float(intercept)}}
