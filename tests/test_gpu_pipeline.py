@@ -11,18 +11,25 @@ from tests.gpu_helpers import assert_ct_equal, ct_from, params_from, ring_hash
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module")
-def toy(golden):
+def _complex(g) -> bool:
+    return bool(int(g.arr("complex_packing"))) if "complex_packing" in g else True
+
+
+# gwas_toy: k=16 = one full batch; gwas_toy_ragged: k=21 = 16 + 5 SNPs (a partial batch whose
+# last complex column carries one SNP); gwas_toy_real: real packing, k=11 = 8 + 3
+@pytest.fixture(scope="module", params=["gwas_toy", "gwas_toy_ragged", "gwas_toy_real"])
+def toy(request, golden):
     import paper_1902_04303_b200 as hg
     from paper_1902_04303_b200.data import CleartextDataset
     from paper_1902_04303_b200.gwas import GwasConfig
 
-    g = golden("gwas_toy")
+    g = golden(request.param)
     params = params_from(g)
     n, d, k, seed, key_seed = (int(x) for x in g.arr("shape"))
     sk, pk, evk, rot = hg.keygen(params, key_seed)
     ds = CleartextDataset(X=g.arr("X"), S=g.arr("S"), y=g.arr("y"))
-    config = GwasConfig(n=n, d=d, k=k).resolve(params)
+    tau = int(g.arr("tau")) if "tau" in g and int(g.arr("tau")) else None
+    config = GwasConfig(n=n, d=d, k=k, complex_packing=_complex(g), tau=tau).resolve(params)
     return g, params, (sk, pk, evk, rot), ds, config, seed
 
 
@@ -44,11 +51,11 @@ def _golden_inputs(g, params, config):
     for bi in range(int(g.arr("n_batches"))):
         offset = bi * config.tau
         count = min(config.tau, config.k - offset)
-        ncols = (count + 1) // 2
+        ncols = (count + 1) // 2 if config.complex_packing else count
         rows = [ct_from(g, f"in.b{bi}.S{j}", params) for j in range(n)]
         batches.append(SnpBatch(index=bi, S_packed=REPMatrix(rows_ct=rows, repeat=cs, rows=n,
                                                             cols_logical=ncols),
-                                snp_offset=offset, snp_count=count, complex_packing=True))
+                                snp_offset=offset, snp_count=count, complex_packing=config.complex_packing))
     return EncryptedGwasInputs(logreg=LogRegInputs(X=X, Xt_rep=Xt, XtX_inv=XtXinv, y=y),
                                batches=batches, config=config)
 
@@ -98,7 +105,10 @@ def test_toy_pipeline_bit_exact(toy):
     for bo in out.batch_outputs:
         assert_ct_equal(bo.num_ct, g, f"out.b{bo.index}.num")
         assert_ct_equal(bo.den_even_ct, g, f"out.b{bo.index}.den_even")
-        assert_ct_equal(bo.den_odd_ct, g, f"out.b{bo.index}.den_odd")
+        if config.complex_packing:
+            assert_ct_equal(bo.den_odd_ct, g, f"out.b{bo.index}.den_odd")
+        else:
+            assert bo.den_odd_ct is None
     num, den = decrypt_statistics(out.batch_outputs, config, params, sk)
     assert np.array_equal(num, g.arr("num"))
     assert np.array_equal(den, g.arr("den"))
@@ -123,4 +133,5 @@ def test_toy_pipeline_streamed_batches_bit_exact(toy):
     for bo in out.batch_outputs:
         assert_ct_equal(bo.num_ct, g, f"out.b{bo.index}.num")
         assert_ct_equal(bo.den_even_ct, g, f"out.b{bo.index}.den_even")
-        assert_ct_equal(bo.den_odd_ct, g, f"out.b{bo.index}.den_odd")
+        if config.complex_packing:
+            assert_ct_equal(bo.den_odd_ct, g, f"out.b{bo.index}.den_odd")

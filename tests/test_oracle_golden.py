@@ -123,15 +123,38 @@ def test_oracle_decrypt_unit(golden):
     assert m == g.ints("decrypt_eng_mult")[0]
 
 
-def test_replay_oracle_matches_reference_encrypted_run(golden):
+@pytest.mark.parametrize("name", ["gwas_toy", "gwas_toy_ragged", "gwas_toy_real"])
+def test_replay_oracle_matches_reference_encrypted_run(golden, name):
     """The float64 replay of the approximate circuit (oracle/replay.py) agrees with the
-    reference's decrypted encrypted-GWAS statistics (~1e-8)."""
+    reference's decrypted encrypted-GWAS statistics (~1e-8), for a full batch,
+    a ragged last batch and real packing."""
     import numpy as np
 
     from oracle.replay import replay_gwas
 
-    g = golden("gwas_toy")
+    g = golden(name)
     rep = replay_gwas(g.arr("X"), g.arr("y"), g.arr("S"))
     num, den = g.arr("num"), g.arr("den")
     assert np.max(np.abs(rep["numerator"] - num)) < 1e-6
     assert np.max(np.abs(rep["denominator"] - den)) < 1e-6
+
+
+def test_cleartext_oracles_restate_reference_definitions():
+    """oracle_modified is the replay with the exact 1/w (Newton from a good guess converges to
+    it); oracle_original equals oracle_modified when W is constant (weighted == unweighted
+    projector); accuracy() counts as the paper's methodology does."""
+    import numpy as np
+
+    from oracle.replay import accuracy, oracle_modified, oracle_original, replay_gwas
+    from paper_1902_04303_b200.data import synth_gwas_dataset
+
+    ds = synth_gwas_dataset(60, 4, 12, seed=9)
+    rep = replay_gwas(ds.X, ds.y, ds.S, inverse_iters=40, guess=1.0)
+    num, den = oracle_modified(ds.X, ds.y, ds.S, rep["beta"], rep["p"])
+    assert np.allclose(num, rep["numerator"], rtol=1e-9) and np.allclose(den, rep["denominator"], rtol=1e-9)
+    p_const = np.full(60, 0.3)
+    a = oracle_modified(ds.X, ds.y, ds.S, rep["beta"], p_const)
+    b = oracle_original(ds.X, ds.y, ds.S, rep["beta"], p_const)
+    assert np.allclose(a[0], b[0]) and np.allclose(a[1], b[1])
+    rep_acc = accuracy([0.0, 1.0, 2.0], [0.0, 1.02, 2.2])
+    assert rep_acc["above"] == {"0.1": 1, "0.01": 2, "0.005": 2}

@@ -153,8 +153,11 @@ def make_deep():
     st.save("deep_ops.npz")
 
 
-def make_gwas(n=8, d=4, k=16, log_n=7, seed=0, key_seed=5, fname="gwas_toy.npz"):
+def make_gwas(n=8, d=4, k=16, log_n=7, seed=0, key_seed=5, fname="gwas_toy.npz", complex_packing=True,
+              tau=None):
     st = Store()
+    st.arr("complex_packing", np.int64(1 if complex_packing else 0))
+    st.arr("tau", np.int64(tau or 0))
     params = hegwas.CkksParams(log_n=log_n, log_l=1700, log_p=45, log_p_small=30, h=64)
     st.arr("params", params_arr(params))
     st.arr("shape", np.array([n, d, k, seed, key_seed], dtype=np.int64))
@@ -169,7 +172,7 @@ def make_gwas(n=8, d=4, k=16, log_n=7, seed=0, key_seed=5, fname="gwas_toy.npz")
     st.arr("key_hash_names", np.array(sorted(hashes)))
     st.arr("key_hash_values", np.array([hashes[x] for x in sorted(hashes)]))
     print(f"  keygen {time.time() - t0:.1f}s")
-    config = GwasConfig(n=n, d=d, k=k).resolve(params)
+    config = GwasConfig(n=n, d=d, k=k, complex_packing=complex_packing, tau=tau).resolve(params)
     ref_ds = RefDataset(X=ds.X, S=ds.S, y=ds.y)
     rng = random.Random(seed)
     t0 = time.time()
@@ -225,6 +228,13 @@ def main():
         make_gwas()
     if which in ("hegw", "all"):
         make_hegw()
+    if which == "real":
+        make_gwas(k=11, seed=2, key_seed=7, fname="gwas_toy_real.npz", complex_packing=False, tau=8)
+    if which in ("ragged", "all"):
+        # k not a multiple of tau (16 + 5 SNPs, the last complex column half empty), and the
+        # real-packing variant (tau = 8: 8 + 3 SNPs)
+        make_gwas(k=21, seed=1, key_seed=6, fname="gwas_toy_ragged.npz")
+        make_gwas(k=11, seed=2, key_seed=7, fname="gwas_toy_real.npz", complex_packing=False, tau=8)
 
 
 def make_hegw():
