@@ -341,7 +341,32 @@ def measure_primitives(torch, hg, _lib, log_n: int = 16, level: int = 1550, reps
     buf = torch.randint(0, 1 << 20, (rows, params.n), dtype=torch.int32, device="cuda")
     t_ntt = timed(lambda: _lib.check(ctx.lib.hg_ntt_forward(ctx.handle, buf.data_ptr(), rows, 0, ctx.stream())))
     t_intt = timed(lambda: _lib.check(ctx.lib.hg_ntt_inverse(ctx.handle, buf.data_ptr(), rows, 0, ctx.stream())))
+    # automorphism x -> x^5 of a level-1550 polynomial: a pure permutation-with-sign (HBM-bound)
+    # HBM-bound ops over 10 distinct level-1550 polys (10 x 25.7 MB > the 126 MB L2), cycled
+    polys = [hg.mod_down(hg.encrypt_values(v * (1 + 0.01 * i), 45, pk, params, gen), level).c0
+             for i in range(10)]
+    cyc = {"i": 0}
+
+    def nxt():
+        cyc["i"] = (cyc["i"] + 1) % len(polys)
+        return polys[cyc["i"]]
+    t_aut = timed(lambda: nxt().automorphism(5))
+    t_add = timed(lambda: nxt().add(nxt()))
+    peak = (load_peaks().get("hbm_gbs") or 6550.4) * 1e9
+    w64 = lambda bits: -(-bits // 64)  # noqa: E731  (SURVEY §8(d) counts radix-2^64 limbs)
+    ks_bytes = 8 * params.n * (w64(level) + 2 * w64(level + params.log_l) + 2 * w64(level))
+    aut_bytes = 2 * params.n * 4 * -(-level // 32)
     return {"N": params.n, "level_bits": level, "keyswitch_per_s": round(1 / t_ks, 1),
+            "keyswitch_hbm": {"algorithmic_bytes": ks_bytes, "GBps": round(ks_bytes / t_ks / 1e9, 1),
+                              "frac_of_hbm_peak": round(ks_bytes / t_ks / peak, 4),
+                              "note": "SURVEY §8(d) bytes (x, key pair, output pair); the key switch is "
+                                      "integer-pipe / tensor bound (NTT + base conversions), so its HBM "
+                                      "fraction is low by construction"},
+            "automorphism": {"per_s": round(1 / t_aut, 1), "GBps": round(aut_bytes / t_aut / 1e9, 1),
+                             "frac_of_hbm_peak": round(aut_bytes / t_aut / peak, 4),
+                             "bytes": aut_bytes},
+            "add": {"per_s": round(1 / t_add, 1), "GBps": round(1.5 * aut_bytes / t_add / 1e9, 1),
+                    "frac_of_hbm_peak": round(1.5 * aut_bytes / t_add / peak, 4), "bytes": 3 * aut_bytes // 2},
             "ct_mult_rescale_per_s": round(1 / t_mult, 1), "rotation_per_s": round(1 / t_rot, 1),
             "ntt_per_s": round(rows / t_ntt), "intt_per_s": round(rows / t_intt),
             "ntt_butterflies_per_s": round(rows / t_ntt * (params.n // 2) * log_n / 1e9, 1),
