@@ -350,8 +350,19 @@ def measure_primitives(torch, hg, _lib, log_n: int = 16, level: int = 1550, reps
     def nxt():
         cyc["i"] = (cyc["i"] + 1) % len(polys)
         return polys[cyc["i"]]
-    t_aut = timed(lambda: nxt().automorphism(5))
-    t_add = timed(lambda: nxt().add(nxt()))
+    def kernel_time(fn):
+        """device time of the elementwise kernel itself (CUDA events around each launch):
+        one Python-level op costs more host time than its kernel takes"""
+        fn()
+        torch.cuda.synchronize()
+        ctx.set_kernel_timing(True, kinds=("elementwise",))
+        for _ in range(reps):
+            fn()
+        st = ctx.kernel_stats("elementwise")
+        ctx.set_kernel_timing(False)
+        return st["ms"] / 1e3 / max(1, st["launches"])
+    t_aut = kernel_time(lambda: nxt().automorphism(5))
+    t_add = kernel_time(lambda: nxt().add(nxt()))
     peak = (load_peaks().get("hbm_gbs") or 6550.4) * 1e9
     w64 = lambda bits: -(-bits // 64)  # noqa: E731  (SURVEY §8(d) counts radix-2^64 limbs)
     ks_bytes = 8 * params.n * (w64(level) + 2 * w64(level + params.log_l) + 2 * w64(level))
@@ -362,10 +373,10 @@ def measure_primitives(torch, hg, _lib, log_n: int = 16, level: int = 1550, reps
                               "note": "SURVEY §8(d) bytes (x, key pair, output pair); the key switch is "
                                       "integer-pipe / tensor bound (NTT + base conversions), so its HBM "
                                       "fraction is low by construction"},
-            "automorphism": {"per_s": round(1 / t_aut, 1), "GBps": round(aut_bytes / t_aut / 1e9, 1),
+            "automorphism": {"kernel_us": round(t_aut * 1e6, 2), "GBps": round(aut_bytes / t_aut / 1e9, 1),
                              "frac_of_hbm_peak": round(aut_bytes / t_aut / peak, 4),
                              "bytes": aut_bytes},
-            "add": {"per_s": round(1 / t_add, 1), "GBps": round(1.5 * aut_bytes / t_add / 1e9, 1),
+            "add": {"kernel_us": round(t_add * 1e6, 2), "GBps": round(1.5 * aut_bytes / t_add / 1e9, 1),
                     "frac_of_hbm_peak": round(1.5 * aut_bytes / t_add / peak, 4), "bytes": 3 * aut_bytes // 2},
             "ct_mult_rescale_per_s": round(1 / t_mult, 1), "rotation_per_s": round(1 / t_rot, 1),
             "ntt_per_s": round(rows / t_ntt), "intt_per_s": round(rows / t_intt),
