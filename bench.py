@@ -515,7 +515,7 @@ def main():
         "hbm_peak_gbs": peaks_file.get("hbm_gbs"),
     }
     cpu = None
-    if not args.no_cpu_baseline and world >= 1:
+    if not args.no_cpu_baseline and world == 1:   # the contract: rank 0 at N=1 only
         t_cpu = cpu_mult_sample(params.log_n, params.log_l - 150, params.log_l, params.log_p)
         cpu = {"value": round(cpu_snp_rate(t_cpu, tau), 6), "unit": "SNP/s", "cores": 1, "kind": "port",
                "sample": f"one HeEngine.mult at N=2^{params.log_n}, level {params.log_l - 150} via oracle/ "
