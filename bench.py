@@ -201,17 +201,40 @@ def run_ours(args, world, rank, local):
     torch.cuda.synchronize()
     t_keys_inputs = time.time() - t_wall0
 
-    # -- setup (once, timed on the device) ------------------------------------------------------
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.record()
-    beta, p_prev, inter, m_dup = compute_setup(engine, inputs)
-    e.record()
-    torch.cuda.synchronize()
-    t_setup = s.elapsed_time(e) / 1e3
-
     # -- one batch of SNP ciphertexts, resident + a pinned host copy --------------------------------
     batch = build_snp_batch(ds.S, 0, inputs.config, params, pk, gen)
+    hbatch = HostSnpBatch.from_device(batch) if not args.no_e2e else None
     torch.cuda.synchronize()
+
+    def read_back(out, keep):
+        """the step's 3 result ciphertexts -> pinned host memory, stream-ordered (no host stall)"""
+        host = []
+        for c in (out.num_ct, out.den_even_ct, out.den_odd_ct):
+            for w in (c.c0.words, c.c1.words):
+                h = torch.empty(w.shape, dtype=w.dtype, pin_memory=True)
+                h.copy_(w, non_blocking=True)
+                host.append(h)
+        keep.append((out, host))
+        return sum(int(h.numel()) * 4 for h in host)
+
+    # -- the whole config-3 job, cold, end to end: setup once, then all 21 batches streamed from
+    #    pinned host memory (SnpBatchStream: side-stream uploads, per-row ready events) with every
+    #    batch's results read back -- device-timed; the setup is bracketed on its own as well ------
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e_setup = torch.cuda.Event(enable_timing=True)
+    nb = math.ceil(K_PAPER / tau)
+    s.record()
+    beta, p_prev, inter, m_dup = compute_setup(engine, inputs)
+    e_setup.record()
+    job_keep = []
+    if hbatch is not None:
+        for b in SnpBatchStream([hbatch] * nb, params):
+            read_back(compute_batch(engine, inputs, inter, m_dup, b), job_keep)
+    e.record()
+    torch.cuda.synchronize()
+    t_setup = s.elapsed_time(e_setup) / 1e3
+    t_whole = s.elapsed_time(e) / 1e3 if hbatch is not None else None
+    del job_keep
 
     def step_resident():
         return compute_batch(engine, inputs, inter, m_dup, batch)
@@ -259,24 +282,13 @@ def run_ours(args, world, rank, local):
     # side stream while batch i computes; every step's 3 result ciphertexts are read back.
     e2e = None
     if not args.no_e2e:
-        hbatch = HostSnpBatch.from_device(batch)
-
         def run_e2e(nsteps):
             # every step's 3 result ciphertexts are copied to pinned host memory asynchronously
             # (stream-ordered after the step's kernels); the caller's synchronize() closes the
             # timed region, so all reads complete inside it without a host stall per step
             d2h, keep = 0, []
             for b in SnpBatchStream([hbatch] * nsteps, params):
-                out = compute_batch(engine, inputs, inter, m_dup, b)
-                res = [out.num_ct, out.den_even_ct, out.den_odd_ct]
-                host = []
-                for c in res:
-                    for w in (c.c0.words, c.c1.words):
-                        h = torch.empty(w.shape, dtype=w.dtype, pin_memory=True)
-                        h.copy_(w, non_blocking=True)
-                        host.append(h)
-                keep.append((out, host))
-                d2h = sum(int(h.numel()) * 4 for h in host)
+                d2h = read_back(compute_batch(engine, inputs, inter, m_dup, b), keep)
             return d2h
 
         run_e2e(1)
@@ -295,7 +307,7 @@ def run_ours(args, world, rank, local):
     peaks = probe_integer_peaks(ctx, torch)
     prims = None if args.no_primitives else measure_primitives(torch, hg, _lib)
     return {
-        "params": params, "tau": tau, "t_setup": t_setup, "t_steps": t_steps,
+        "params": params, "tau": tau, "t_setup": t_setup, "t_steps": t_steps, "t_whole": t_whole,
         "launches": launches, "kstats": kstats, "clocks": clocks.summary(), "e2e": e2e,
         "peaks": peaks, "t_keys_inputs": t_keys_inputs, "primitives": prims,
         "key_cache_gb": round(__import__("paper_1902_04303_b200.ckks", fromlist=["KEY_CACHE"]).KEY_CACHE.bytes / 1e9, 2),
@@ -493,6 +505,7 @@ def main():
     ms_step = 1e3 * r["t_steps"] / steps
     nb = math.ceil(K_PAPER / tau)
     whole = K_PAPER / (r["t_setup"] + nb * r["t_steps"] / steps)
+    whole_e2e = K_PAPER / r["t_whole"] if r.get("t_whole") else None
     ks = r["kstats"]
     # roofline of the dominant kernel class (integer pipe: CRT reconstruction MACs)
     dom = max(("crt", "modup", "ntt"), key=lambda k: ks[k]["ms"])
@@ -530,8 +543,13 @@ def main():
                    "global_batch_snps": tau * world, "parallelism": f"snp-batch sharding x{world}",
                    "l2": "inputs > L2 (13 GB of batch ciphertexts per step)"},
         "whole_job": {"snps": K_PAPER, "batches": nb, "setup_s": round(r["t_setup"], 2),
-                      "value": round(whole, 3), "unit": "SNP/s",
-                      "note": "config-3 end to end on device: setup once + 21 batch steps"},
+                      "value": round(whole_e2e, 3) if whole_e2e else round(whole, 3), "unit": "SNP/s",
+                      "measured_s": round(r["t_whole"], 2) if r.get("t_whole") else None,
+                      "from_resident_steps": round(whole, 3),
+                      "note": "config-3 whole job, measured cold and end to end: setup once + 21 SNP "
+                              "batches streamed from pinned host memory with every batch's results read "
+                              "back (the batch data is one seeded batch replayed 21 times); "
+                              "from_resident_steps = setup + 21 x the resident step"},
         "e2e": r["e2e"], "gpu_launches": r["launches"], "roofline": roofline, "cpu_baseline": cpu,
         "clocks": r["clocks"], "int_peaks": {k: round(v / 1e9, 1) for k, v in r["peaks"].items()},
         "primitives": r["primitives"],
