@@ -227,12 +227,22 @@ def run_ours(args, world, rank, local):
     beta, p_prev, inter, m_dup = compute_setup(engine, inputs)
     e_setup.record()
     job_keep = []
+    marks = []
     if hbatch is not None:
         for b in SnpBatchStream([hbatch] * nb, params):
             read_back(compute_batch(engine, inputs, inter, m_dup, b), job_keep)
+            if os.environ.get("HG_BENCH_DEBUG"):
+                marks.append(torch.cuda.Event(enable_timing=True))
+                marks[-1].record()
     e.record()
     torch.cuda.synchronize()
     t_setup = s.elapsed_time(e_setup) / 1e3
+    if marks:
+        prev, per = e_setup, []
+        for m in marks:
+            per.append(round(prev.elapsed_time(m), 1))
+            prev = m
+        print(f"[bench] whole-job batch ms: {per}", file=sys.stderr, flush=True)
     t_whole = s.elapsed_time(e) / 1e3 if hbatch is not None else None
     del job_keep
 
