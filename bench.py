@@ -537,6 +537,16 @@ def main():
                            for k, v in ks.items()},
         "hbm_peak_gbs": peaks_file.get("hbm_gbs"),
     }
+    # the tensor-core classes against the i8 dense peak (2x the measured bf16 dense figure on
+    # Blackwell): their work unit is a 32x32-bit MAC = 16 u8 MACs = 32 int8 ops
+    i8_tops = 2 * float(peaks_file.get("bf16_tflops") or 2250.0)
+    for k in ("crt", "modup"):
+        v = ks[k]
+        if v["ms"]:
+            tops = v["work"] * 32 / (v["ms"] / 1e3) / 1e12
+            roofline["kernel_classes"][k]["int8_tops"] = round(tops, 1)
+            roofline["kernel_classes"][k]["frac_of_i8_peak"] = round(tops / i8_tops, 4)
+    roofline["i8_peak_tops"] = round(i8_tops, 1)
     cpu = None
     if not args.no_cpu_baseline and world == 1:   # the contract: rank 0 at N=1 only
         t_cpu = cpu_mult_sample(params.log_n, params.log_l - 150, params.log_l, params.log_p)
@@ -552,6 +562,10 @@ def main():
                                f"P17 (N=2^{params.log_n}, log_l={params.log_l}, log_p=45, log_p_small=30)",
                    "global_batch_snps": tau * world, "parallelism": f"snp-batch sharding x{world}",
                    "l2": "inputs > L2 (13 GB of batch ciphertexts per step)"},
+        "config0_job": {"snps": 256, "s": round(r["t_setup"] + r["t_steps"] / steps, 2),
+                        "value": round(256 / (r["t_setup"] + r["t_steps"] / steps), 2), "unit": "SNP/s",
+                        "note": "config 0 (n=245, 256 SNPs = one batch): the cold setup + one resident "
+                                "batch step of this run (the setup does not depend on k)"},
         "whole_job": {"snps": K_PAPER, "batches": nb, "setup_s": round(r["t_setup"], 2),
                       "value": round(whole_e2e, 3) if whole_e2e else round(whole, 3), "unit": "SNP/s",
                       "measured_s": round(r["t_whole"], 2) if r.get("t_whole") else None,
