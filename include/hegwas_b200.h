@@ -137,6 +137,13 @@ int hg_ct_mult_prepared_batch(hg_ctx* ctx, const hg_key* evk, int count, const h
                               const uint32_t* const* b0s, const uint32_t* const* b1s, int level,
                               int rescale_bits, uint32_t* const* out0s, uint32_t* const* out1s,
                               void* stream);
+/* `count` independent hg_ct_mult products (a_i (x) b_i, relinearised, rescaled by
+ * rescale_bits), two per group of launches; outputs identical to hg_ct_mult's.  Replaces the
+ * per-term HeEngine.mult of cp_matvec (matrix.py:99-106) and other independent products. */
+int hg_ct_mult_batch(hg_ctx* ctx, const hg_key* evk, int count, const uint32_t* const* a0s,
+                     const uint32_t* const* a1s, const uint32_t* const* b0s, const uint32_t* const* b1s,
+                     int level, int rescale_bits, uint32_t* const* out0s, uint32_t* const* out1s,
+                     void* stream);
 /* As hg_ct_prepare, with the NTT basis widened for a sum of `terms` such products
  * (hg_ct_inner_prepared). */
 int hg_ct_prepare_sum(hg_ctx* ctx, const uint32_t* c0, const uint32_t* c1, int level, int terms,

@@ -1013,6 +1013,88 @@ extern "C" int hg_ct_mult_prepared_batch(hg_ctx* ctx, const hg_key* evk, int cou
     return HG_OK;
 }
 
+// `count` products of ciphertext pairs (a_i (x) b_i, relinearised, rescaled), two per group of
+// launches: one ModUp per pair of items' four polynomials, one forward NTT over all eight rows
+// of a prime group, then the same tensor CRT / paired key switch / finish as
+// hg_ct_mult_prepared_batch.  Each output is identical to hg_ct_mult's.
+extern "C" int hg_ct_mult_batch(hg_ctx* ctx, const hg_key* evk, int count, const uint32_t* const* a0s,
+                                const uint32_t* const* a1s, const uint32_t* const* b0s,
+                                const uint32_t* const* b1s, int level, int rescale_bits,
+                                uint32_t* const* out0s, uint32_t* const* out1s, void* stream) {
+    if (!ctx || !evk || count < 0 || (count && (!a0s || !a1s || !b0s || !b1s || !out0s || !out1s)) ||
+        evk->level != level || rescale_bits < 0 || rescale_bits >= level)
+        return hg_fail(HG_EINVAL, "hg_ct_mult_batch: bad arguments");
+    const int N = ctx->N;
+    const int W = words_for_bits(level);
+    const int Pk = evk->P;
+    const bool fused = fuse_pointwise() && crt_finish_ok(ctx, Pk, evk->big_l, level);
+    const int P = tensor_sum_primes(ctx, level, 1);
+    const bool prescale = fused && crt_prescale_ok(ctx, P, 0, level);
+    int rc;
+    for (int g0 = 0; g0 < count; g0 += 2) {
+        const int G = count - g0 < 2 ? count - g0 : 2;
+        if (!fused || G == 1 || P < 0) {
+            for (int g = 0; g < G; ++g)
+                if ((rc = hg_ct_mult(ctx, evk, a0s[g0 + g], a1s[g0 + g], b0s[g0 + g], b1s[g0 + g], level,
+                                     rescale_bits, out0s[g0 + g], out1s[g0 + g], stream)))
+                    return rc;
+            continue;
+        }
+        cudaStream_t st = (cudaStream_t)stream;
+        const size_t plane = (size_t)P * N, kplane = (size_t)Pk * N, wn = (size_t)W * N;
+        Scratch res(st), tens(st), kres(st), buf(st);
+        HG_CUDA_TRY(res.alloc(8 * plane * 4));          // [2 items][a0, a1, b0, b1][P][N]
+        HG_CUDA_TRY(tens.alloc(6 * plane * 4));
+        HG_CUDA_TRY(kres.alloc(6 * kplane * 4));
+        HG_CUDA_TRY(buf.alloc(6 * wn * 4));
+        for (int g = 0; g < 2; ++g) {
+            OperandSet ops{};
+            const uint32_t* src[4] = {a0s[g0 + g], a1s[g0 + g], b0s[g0 + g], b1s[g0 + g]};
+            for (int k = 0; k < 4; ++k) { ops.words[k] = src[k]; ops.bits[k] = level; ops.is_signed[k] = 1; }
+            if ((rc = launch_modup(ctx, ops, 4, P, res.u32() + (size_t)4 * g * plane, 0, st))) return rc;
+        }
+        if ((rc = hg_ntt_launch(ctx, res.u32(), 8 * P, P, 0, true, st))) return rc;
+        // every tensor term has exactly one a factor: carrying the CRT constants on a0, a1
+        // lets the CRT skip its own constant product (as a prepared operand does)
+        if (prescale)
+            for (int g = 0; g < 2; ++g)
+                if ((rc = prescale_rows(ctx, res.u32() + (size_t)4 * g * plane, 2, P, st))) return rc;
+        for (int g = 0; g < 2; ++g) {
+            const uint32_t* r = res.u32() + (size_t)4 * g * plane;
+            rc = hg_intt_fused(ctx, 2, tens.u32() + (size_t)3 * g * plane, r, r + plane, r + 2 * plane,
+                               r + 3 * plane, P, st);
+            if (rc) return rc < 0 ? hg_fail(HG_EINVAL, "fused tensor product not available") : rc;
+        }
+        uint32_t* d = buf.u32();
+        OutSet touts{};
+        for (int g = 0; g < 2; ++g) {
+            touts.out[3 * g] = d + (size_t)(2 * g) * wn;
+            touts.out[3 * g + 1] = d + (size_t)(2 * g + 1) * wn;
+            touts.out[3 * g + 2] = d + (size_t)(4 + g) * wn;
+        }
+        if ((rc = launch_crt(ctx, tens.u32(), 6, P, 0, level, touts, st, nullptr, prescale))) return rc;
+        OperandSet kops{};
+        for (int g = 0; g < 2; ++g) {
+            kops.words[g] = d + (size_t)(4 + g) * wn; kops.bits[g] = level; kops.is_signed[g] = 0;
+        }
+        if ((rc = launch_modup(ctx, kops, 2, Pk, kres.u32(), 0, st))) return rc;
+        if ((rc = hg_ntt_launch(ctx, kres.u32(), 2 * Pk, Pk, 0, true, st))) return rc;
+        uint32_t* t = kres.u32() + 2 * kplane;
+        rc = hg_intt_fused(ctx, 1, t, kres.u32(), evk->d_kb, evk->d_ka, nullptr, Pk, st, 2);
+        if (rc) return rc < 0 ? hg_fail(HG_EINVAL, "batched key product not available") : rc;
+        CrtFinish fin;
+        for (int k = 0; k < 4; ++k) fin.add[k] = d + (size_t)k * wn;
+        fin.post = rescale_bits;
+        OutSet kouts{};
+        for (int g = 0; g < 2; ++g) {
+            kouts.out[2 * g] = out0s[g0 + g];
+            kouts.out[2 * g + 1] = out1s[g0 + g];
+        }
+        if ((rc = launch_crt(ctx, t, 4, Pk, evk->big_l, level, kouts, st, &fin, evk->prescaled))) return rc;
+    }
+    return HG_OK;
+}
+
 // ---- inner products over prepared operands ------------------------------------------------------
 // acc[q] += A[q][b] (x) B[b] for QG weight sets at once: one thread per (prime, coefficient),
 // the B residues of every b read once, the accumulators in registers.  Montgomery products of

@@ -75,3 +75,27 @@ def test_mult_prepared_many_identical_to_one_by_one(log_n, level):
         one = eng.mult(p, c)
         assert torch.equal(one.c0.words, m.c0.words) and torch.equal(one.c1.words, m.c1.words)
         assert (one.level_bits, one.scale_bits, one.depth_ct) == (m.level_bits, m.scale_bits, m.depth_ct)
+
+
+@pytest.mark.parametrize("log_n,level", [(12, 1550), (17, 230)])
+def test_mult_many_identical_to_one_by_one(log_n, level):
+    """hg_ct_mult_batch (pairs of independent products) writes exactly what hg_ct_mult writes
+    for each product (3 products: a pair and a single; mixed input levels aligned down)."""
+    import torch
+
+    import paper_1902_04303_b200 as hg
+
+    params = hg.CkksParams(log_n=log_n, log_l=1700, log_p=45, log_p_small=30)
+    sk, pk, evk, rot = hg.keygen(params, 4, device_rng=True)
+    eng = hg.HeEngine(params, evk, rot)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(6)
+    vals = np.random.default_rng(1).uniform(-1, 1, params.slot_count)
+    enc = lambda: hg.encrypt_values(vals, params.log_p, pk, params, gen)  # noqa: E731
+    lhs = [hg.mod_down(enc(), level) for _ in range(3)]
+    rhs = [enc(), hg.mod_down(enc(), level + 100), enc()]
+    many = eng.mult_many(lhs, rhs)
+    for a, b, m in zip(lhs, rhs, many):
+        one = eng.mult(a, b)
+        assert torch.equal(one.c0.words, m.c0.words) and torch.equal(one.c1.words, m.c1.words)
+        assert (one.level_bits, one.scale_bits, one.depth_ct) == (m.level_bits, m.scale_bits, m.depth_ct)
