@@ -230,7 +230,7 @@ def compute_scale_group(engine: HeEngine, setup: ScaleSetup, cts: list[Ciphertex
 
         tu = engine.inner_product(setup.p_xwx, cts)                      # 2(d+1) sums, one pass
         views = [_mod_down_view(c, setup.level_xwx) for c in cts]
-        sq = [engine.mult(v, v) for v in views]
+        sq = _mults(engine, views, views)
         q_raw = engine.inner_product(setup.p_w, sq)[0]
         a_raw = engine.inner_product(setup.p_a, cts)[0]
         tu = rotate_sum_many(engine, tu, 1, blk)
@@ -241,17 +241,23 @@ def compute_scale_group(engine: HeEngine, setup: ScaleSetup, cts: list[Ciphertex
         u = [weighted_sum(engine, setup.v_wx[a], cts, blk) for a in range(d1)]
         q = weighted_sum(engine, setup.v_w, cts, blk, square=True)
         at_s = weighted_sum(engine, setup.v_a, cts, blk)
-    # c = G t ; den = q - 2 u.c + c^T A2 c ; num = a^T S - b.t
-    c = [sum_terms(engine, [engine.mult(setup.g_rep[r][s], t[s]) for s in range(d1)]) for r in range(d1)]
-    uc = sum_terms(engine, [engine.mult(u[r], c[r]) for r in range(d1)])
-    quad = []
-    for r in range(d1):
-        for s in range(r, d1):
-            term = engine.mult(setup.a2_rep[r][s], engine.mult(c[r], c[s]))
-            quad.append(mult_integer(term, 2) if r != s else term)
+    # c = G t ; den = q - 2 u.c + c^T A2 c ; num = a^T S - b.t   (independent products batched)
+    gt = _mults(engine, [setup.g_rep[r][s] for r in range(d1) for s in range(d1)],
+                [t[s] for r in range(d1) for s in range(d1)])
+    c = [sum_terms(engine, gt[r * d1:(r + 1) * d1]) for r in range(d1)]
+    uc = sum_terms(engine, _mults(engine, u, c))
+    idx = [(r, s) for r in range(d1) for s in range(r, d1)]
+    cc = _mults(engine, [c[r] for r, _ in idx], [c[s] for _, s in idx])
+    terms = _mults(engine, [setup.a2_rep[r][s] for r, s in idx], cc)
+    quad = [mult_integer(term, 2) if r != s else term for (r, s), term in zip(idx, terms)]
     den = engine.add(engine.sub(q, mult_integer(uc, 2)), sum_terms(engine, quad))
-    num = engine.sub(at_s, sum_terms(engine, [engine.mult(setup.b_rep[r], t[r]) for r in range(d1)]))
+    num = engine.sub(at_s, sum_terms(engine, _mults(engine, setup.b_rep, t)))
     return GroupOutput(index=index, num_ct=num, den_ct=den)
+
+
+def _mults(engine: HeEngine, lhs, rhs) -> list[Ciphertext]:
+    many = getattr(engine, "mult_many", None)
+    return many(list(lhs), list(rhs)) if many else [engine.mult(a, b) for a, b in zip(lhs, rhs)]
 
 
 def compute_scale_gwas(engine: HeEngine, inputs: ScaleInputs, fused: bool = True):
