@@ -197,6 +197,14 @@ long long hg_launch_count(const hg_ctx* ctx);
  * 1 = every class, otherwise (mask << 1) with bit k of mask selecting class k (so a
  * timed region can bracket only the class whose roofline it reports).                */
 int hg_set_kernel_timing(hg_ctx* ctx, int enabled);
+/* Host-side replay of CPython's random.Random (MT19937) for the reference's encryption
+ * samplers (ring.py:212-235): `state` is getstate()'s 624 words + position, advanced in place.
+ * hg_rng_ternary: n x getrandbits(2) -> {+1, 0, 0, -1}.  hg_rng_gaussian: rounded
+ * gauss(0, sigma) draws, |x| > 6 sigma redrawn; the Box-Muller spare goes in/out through
+ * gauss_next / has_next.  Bit-identical to the Python samplers (tests/test_host.py). */
+int hg_rng_ternary(uint32_t* state, int n, int8_t* out);
+int hg_rng_gaussian(uint32_t* state, double* gauss_next, int* has_next, int n, double sigma,
+                    int32_t* out);
 int hg_kernel_stats(hg_ctx* ctx, int kind, double* ms, long long* launches, double* work);
 /* Device arena for the library's long-lived objects (prepared switching keys and
  * prepared operands): reserve one more slab of `bytes` up front, so a job's first uses

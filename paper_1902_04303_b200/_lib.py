@@ -83,6 +83,8 @@ SIGNATURES = {
     "hg_launch_count": (ctypes.c_longlong, [_vp]),
     "hg_set_kernel_timing": (_i, [_vp, _i]),
     "hg_poly_sum": (_i, [_vp, _vp, ctypes.POINTER(ctypes.c_void_p), _i, _i, _vp]),
+    "hg_rng_ternary": (_i, [_vp, _i, _vp]),
+    "hg_rng_gaussian": (_i, [_vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i), _i, ctypes.c_double, _vp]),
     "hg_pool_reserve": (_i, [_vp, ctypes.c_size_t, _vp]),
     "hg_pool_bytes": (ctypes.c_size_t, [_vp, _i]),
     "hg_pool_trim": (ctypes.c_size_t, [_vp]),

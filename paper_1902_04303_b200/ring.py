@@ -375,8 +375,53 @@ def sample_uniform(n: int, bits: int, rng: random.Random) -> list[int]:
     return [rng.getrandbits(bits) for _ in range(n)]
 
 
+def _native_rng_call(rng: random.Random, fn):
+    """Run a native sampler on rng's MT19937 state (getstate / setstate round trip): the
+    Python generator then continues exactly after the native draws."""
+    version, internal, gauss_next = rng.getstate()
+    state = (ctypes.c_uint32 * 625)(*internal)
+    g = ctypes.c_double(gauss_next if gauss_next is not None else 0.0)
+    has = ctypes.c_int(0 if gauss_next is None else 1)
+    out = fn(state, g, has)
+    rng.setstate((version, tuple(state), g.value if has.value else None))
+    return out
+
+
+def _native_samplers() -> bool:
+    """The host-side CPython-random replay in libhegwas_b200.so (hg_rng_*); HG_PY_SAMPLERS=1
+    forces the Python loops (the two are bit-identical, tests/test_host.py)."""
+    if os.environ.get("HG_PY_SAMPLERS"):
+        return False
+    try:
+        return hasattr(_lib.load_library(), "hg_rng_ternary")
+    except Exception:
+        return False
+
+
+def sample_gaussian_array(n: int, sigma: float, rng: random.Random) -> np.ndarray:
+    """sample_gaussian as an int64 array (the native replay when available)."""
+    if type(rng) is random.Random and n >= 64 and _native_samplers():
+        buf = np.empty(n, dtype=np.int32)
+        _native_rng_call(rng, lambda st, g, h: _lib.check(_lib.load_library().hg_rng_gaussian(
+            st, ctypes.byref(g), ctypes.byref(h), n, float(sigma), buf.ctypes.data)))
+        return buf.astype(np.int64)
+    return np.asarray(sample_gaussian(n, sigma, rng), dtype=np.int64)
+
+
+def sample_ternary_array(n: int, rng: random.Random) -> np.ndarray:
+    """sample_ternary as an int64 array (the native replay when available)."""
+    if type(rng) is random.Random and n >= 64 and _native_samplers():
+        buf = np.empty(n, dtype=np.int8)
+        _native_rng_call(rng, lambda st, g, h: _lib.check(_lib.load_library().hg_rng_ternary(
+            st, n, buf.ctypes.data)))
+        return buf.astype(np.int64)
+    return np.asarray(sample_ternary(n, rng), dtype=np.int64)
+
+
 def sample_gaussian(n: int, sigma: float, rng: random.Random) -> list[int]:
     """Rounded N(0, sigma^2), redrawing anything beyond 6 sigma."""
+    if type(rng) is random.Random and n >= 64 and _native_samplers():
+        return sample_gaussian_array(n, sigma, rng).tolist()
     cut = 6.0 * sigma
     out: list[int] = []
     gauss = rng.gauss
@@ -399,6 +444,8 @@ def sample_hamming(n: int, h: int, rng: random.Random) -> list[int]:
 
 def sample_ternary(n: int, rng: random.Random) -> list[int]:
     """{-1, 0, 1} with probabilities 1/4, 1/2, 1/4 from two random bits each."""
+    if type(rng) is random.Random and n >= 64 and _native_samplers():
+        return sample_ternary_array(n, rng).tolist()
     table = (1, 0, 0, -1)
     return [table[rng.getrandbits(2)] for _ in range(n)]
 

@@ -289,3 +289,27 @@ def test_cli_io_audit_and_manifest(tmp_path):
     assert len(m["files"]["batches"][0]) == 8
     args = cli.build_parser().parse_args(["keygen", "--log-n", "17", "--log-l", "1700", "--outdir", "x"])
     assert cli._params(args).log_n == P17.log_n
+
+
+def test_native_samplers_replay_cpython_random():
+    """The native CPython-random replay (hg_rng_ternary / hg_rng_gaussian) produces exactly the
+    Python samplers' draws and leaves the generator in exactly the same state (incl. the
+    cached Box-Muller spare), across the MT19937 624-word refill boundary."""
+    import random as pyrandom
+
+    from paper_1902_04303_b200 import ring
+
+    assert ring._native_samplers()
+    for seed, n in [(1, 64), (7, 1000), (123456789, 4097), (2 ** 63 + 5, 3333)]:
+        a, b = pyrandom.Random(seed), pyrandom.Random(seed)
+        b.random()                                   # start mid-block
+        a.random()
+        got = ring.sample_ternary(n, a) + ring.sample_gaussian(n, 3.2, a) + ring.sample_gaussian(n + 1, 3.2, a)
+        os.environ["HG_PY_SAMPLERS"] = "1"
+        try:
+            want = ring.sample_ternary(n, b) + ring.sample_gaussian(n, 3.2, b) + ring.sample_gaussian(n + 1, 3.2, b)
+        finally:
+            del os.environ["HG_PY_SAMPLERS"]
+        assert got == want, seed
+        assert a.getstate() == b.getstate()
+        assert a.getrandbits(64) == b.getrandbits(64) and a.gauss(0, 1) == b.gauss(0, 1)
