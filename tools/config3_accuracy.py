@@ -29,12 +29,25 @@ from paper_1902_04303_b200.gwas import (GwasConfig, assemble_result, compute_gwa
 
 
 def main():
+    import argparse
+    import random
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--host-rng", action="store_true",
+                    help="reference-reproducible keys and encryptions (random.Random draws, the "
+                         "reference's order) instead of device RNG")
+    args = ap.parse_args()
     n, d, k = 245, 4, 10643
     params = hg.CkksParams(log_n=17, log_l=1700, log_p=45, log_p_small=30)
-    sk, pk, evk, rot = hg.keygen(params, 5, device_rng=True)
+    t_keys = time.time()
+    sk, pk, evk, rot = hg.keygen(params, 5, device_rng=not args.host_rng)
+    t_keys = time.time() - t_keys
     eng = hg.HeEngine(params, evk, rot)
-    gen = torch.Generator(device="cuda")
-    gen.manual_seed(3)
+    if args.host_rng:
+        gen = random.Random(3)
+    else:
+        gen = torch.Generator(device="cuda")
+        gen.manual_seed(3)
     ds = synth_gwas_dataset(n, d, k, seed=0)
     cfg = GwasConfig(n=n, d=d, k=k).resolve(params)
     inputs = encrypt_gwas_inputs(ds, cfg, params, pk, gen, lazy_batches=True)
@@ -53,8 +66,12 @@ def main():
     print(json.dumps({
         "config": f"config 3: n={n}, d={d}, k={k}, P17 (N=2^17, log_l=1700, log_p=45, log_p_small=30), "
                   f"{cfg.num_batches} batches of {cfg.tau} SNPs",
-        "data": "synthetic (seeded; config-3 shapes), device-RNG encryption",
+        "data": "synthetic (seeded; config-3 shapes), " + (
+            "reference-reproducible keygen and encryption (random.Random, the reference's draw order)"
+            if args.host_rng else "device-RNG encryption"),
+        "keygen_s": round(t_keys, 1),
         "compute_wall_s": round(t_compute, 2), "snps_per_s_wall": round(k / t_compute, 1),
+        "note": "compute_wall_s includes encrypting each SNP batch on demand (client side)",
         "encrypted_vs_replay": {"numerator_max_rel": rel(num, rep["numerator"]),
                                 "denominator_max_rel": rel(den, rep["denominator"]),
                                 "beta": accuracy(b_rep, enc.effects, (1e-3, 1e-4, 1e-5))},
