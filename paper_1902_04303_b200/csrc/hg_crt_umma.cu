@@ -771,8 +771,8 @@ __global__ void __launch_bounds__(PipeCfg<FUSED>::kWarps * 32, 1) crt_umma_pipe_
             if ((ij & 1) != grp) continue;
             const int oy = tile / tpo, cb = (tile - oy * tpo) * kRows;
             uint32_t* out = pick_out(outs, oy);
-            const uint32_t* addp = oy < 4 ? (oy == 0 ? fin.add[0] : oy == 1 ? fin.add[1] : oy == 2 ? fin.add[2] : fin.add[3])
-                                          : nullptr;
+            // the launcher requires the addends to be consecutive out_bits-wide polynomials
+            const uint32_t* addp = fin.add[0] ? fin.add[0] + (size_t)oy * ((out_bits + 31) >> 5) * N : nullptr;
             const int i = cb + n;
             uint32_t* const outi = out + i;
             if (h == 0) {

@@ -184,7 +184,7 @@ bool hg_crt_umma_pipe_ok(const CrtTable* tab, int N, int shift, int out_bits, in
 // out_k = bits [post, out_bits) of (window_k + add_k' + 2^(post-1)) mod 2^out_bits, where
 // add_k' is add_k (out_bits wide, may be null) read through x -> x^k when kinv != 0.
 struct CrtFinish {
-    const uint32_t* add[4] = {nullptr, nullptr, nullptr, nullptr};
+    const uint32_t* add[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     int64_t kinv = 0;
     int post = 0;
 };

@@ -947,68 +947,84 @@ extern "C" int hg_ct_mult_prepared_batch(hg_ctx* ctx, const hg_key* evk, int cou
     const int W = words_for_bits(level);
     const int Pk = evk->P;
     const bool fused = fuse_pointwise() && crt_finish_ok(ctx, Pk, evk->big_l, level);
+    static const int gmax = getenv("HG_BATCH_G") ? atoi(getenv("HG_BATCH_G")) : 4;
     int rc;
-    for (int g0 = 0; g0 < count; g0 += 2) {
-        const int G = count - g0 < 2 ? count - g0 : 2;
-        const hg_ctprep* a0 = a[g0];
-        const hg_ctprep* a1 = G > 1 ? a[g0 + 1] : nullptr;
-        if (!fused || G == 1 || !a0 || !a1 || a0->P != a1->P || a0->prescaled != a1->prescaled ||
-            a0->level != level || a1->level != level || a0->ctx != ctx || a1->ctx != ctx) {
+    for (int g0 = 0; g0 < count;) {
+        int G = count - g0 < gmax ? count - g0 : gmax;
+        if (G > 4) G = 4;
+        bool ok = fused && G > 1;
+        for (int g = 0; ok && g < G; ++g) {
+            const hg_ctprep* ag = a[g0 + g];
+            ok = ag && ag->ctx == ctx && ag->level == level && ag->P == a[g0]->P &&
+                 ag->prescaled == a[g0]->prescaled;
+        }
+        if (!ok) {
             for (int g = 0; g < G; ++g)
                 if ((rc = hg_ct_mult_prepared(ctx, evk, a[g0 + g], b0s[g0 + g], b1s[g0 + g], level,
                                               rescale_bits, out0s[g0 + g], out1s[g0 + g], stream)))
                     return rc;
+            g0 += G;
             continue;
         }
         cudaStream_t st = (cudaStream_t)stream;
-        const int P = a0->P;
+        const int P = a[g0]->P;
         const size_t plane = (size_t)P * N, kplane = (size_t)Pk * N, wn = (size_t)W * N;
         Scratch res(st), tens(st), kres(st), buf(st);
-        HG_CUDA_TRY(res.alloc(4 * plane * 4));          // [2 items][b0, b1][P][N]
-        HG_CUDA_TRY(tens.alloc(6 * plane * 4));         // [2][d0, d1, d2][P][N]
-        HG_CUDA_TRY(kres.alloc(6 * kplane * 4));        // x [2][P'][N], products [2][2][P'][N]
-        HG_CUDA_TRY(buf.alloc(6 * wn * 4));             // d0_0 d1_0 d0_1 d1_1 (addends) d2_0 d2_1
-        OperandSet ops{};
-        for (int g = 0; g < 2; ++g) {
-            ops.words[2 * g] = b0s[g0 + g]; ops.bits[2 * g] = level; ops.is_signed[2 * g] = 1;
-            ops.words[2 * g + 1] = b1s[g0 + g]; ops.bits[2 * g + 1] = level; ops.is_signed[2 * g + 1] = 1;
+        HG_CUDA_TRY(res.alloc((size_t)2 * G * plane * 4));     // [G items][b0, b1][P][N]
+        HG_CUDA_TRY(tens.alloc((size_t)3 * G * plane * 4));    // [G][d0, d1, d2][P][N]
+        HG_CUDA_TRY(kres.alloc((size_t)3 * G * kplane * 4));   // x [G][P'][N], products [G][2][P'][N]
+        HG_CUDA_TRY(buf.alloc((size_t)3 * G * wn * 4));        // (d0_g, d1_g) addends, then d2_g
+        for (int h = 0; h < G; h += 2) {                        // ModUp: two items (4 polys) per launch
+            const int gh = G - h < 2 ? G - h : 2;
+            OperandSet ops{};
+            for (int k = 0; k < gh; ++k) {
+                ops.words[2 * k] = b0s[g0 + h + k]; ops.bits[2 * k] = level; ops.is_signed[2 * k] = 1;
+                ops.words[2 * k + 1] = b1s[g0 + h + k]; ops.bits[2 * k + 1] = level; ops.is_signed[2 * k + 1] = 1;
+            }
+            if ((rc = launch_modup(ctx, ops, 2 * gh, P, res.u32() + (size_t)2 * h * plane, 0, st))) return rc;
         }
-        if ((rc = launch_modup(ctx, ops, 4, P, res.u32(), 0, st))) return rc;
-        if ((rc = hg_ntt_launch(ctx, res.u32(), 4 * P, P, 0, true, st))) return rc;
-        const hg_ctprep* ap[2] = {a0, a1};
-        for (int g = 0; g < 2; ++g) {
+        if ((rc = hg_ntt_launch(ctx, res.u32(), 2 * G * P, P, 0, true, st))) return rc;
+        for (int g = 0; g < G; ++g) {
+            const hg_ctprep* ag = a[g0 + g];
             const uint32_t* bg = res.u32() + (size_t)2 * g * plane;
-            rc = hg_intt_fused(ctx, 2, tens.u32() + (size_t)3 * g * plane, ap[g]->d_res, ap[g]->d_res + plane,
+            rc = hg_intt_fused(ctx, 2, tens.u32() + (size_t)3 * g * plane, ag->d_res, ag->d_res + plane,
                                bg, bg + plane, P, st);
             if (rc) return rc < 0 ? hg_fail(HG_EINVAL, "fused tensor product not available") : rc;
         }
         uint32_t* d = buf.u32();
-        OutSet touts{};
-        for (int g = 0; g < 2; ++g) {
-            touts.out[3 * g] = d + (size_t)(2 * g) * wn;          // d0_g
-            touts.out[3 * g + 1] = d + (size_t)(2 * g + 1) * wn;  // d1_g
-            touts.out[3 * g + 2] = d + (size_t)(4 + g) * wn;      // d2_g
+        for (int h = 0; h < G; h += 2) {                        // tensor CRT: two items (6 outputs) per launch
+            const int gh = G - h < 2 ? G - h : 2;
+            OutSet touts{};
+            for (int k = 0; k < gh; ++k) {
+                const int g = h + k;
+                touts.out[3 * k] = d + (size_t)(2 * g) * wn;            // d0_g
+                touts.out[3 * k + 1] = d + (size_t)(2 * g + 1) * wn;    // d1_g
+                touts.out[3 * k + 2] = d + (size_t)(2 * G + g) * wn;    // d2_g
+            }
+            if ((rc = launch_crt(ctx, tens.u32() + (size_t)3 * h * plane, 3 * gh, P, 0, level, touts, st,
+                                 nullptr, a[g0]->prescaled)))
+                return rc;
         }
-        if ((rc = launch_crt(ctx, tens.u32(), 6, P, 0, level, touts, st, nullptr, a0->prescaled))) return rc;
-        // relinearise both d2 together; the finish adds (d0_g, d1_g) and rescales
+        // relinearise all d2 together; the finish adds (d0_g, d1_g) and rescales
         OperandSet kops{};
-        for (int g = 0; g < 2; ++g) {
-            kops.words[g] = d + (size_t)(4 + g) * wn; kops.bits[g] = level; kops.is_signed[g] = 0;   // canonical
+        for (int g = 0; g < G; ++g) {
+            kops.words[g] = d + (size_t)(2 * G + g) * wn; kops.bits[g] = level; kops.is_signed[g] = 0;   // canonical
         }
-        if ((rc = launch_modup(ctx, kops, 2, Pk, kres.u32(), 0, st))) return rc;
-        if ((rc = hg_ntt_launch(ctx, kres.u32(), 2 * Pk, Pk, 0, true, st))) return rc;
-        uint32_t* t = kres.u32() + 2 * kplane;
-        rc = hg_intt_fused(ctx, 1, t, kres.u32(), evk->d_kb, evk->d_ka, nullptr, Pk, st, 2);
+        if ((rc = launch_modup(ctx, kops, G, Pk, kres.u32(), 0, st))) return rc;
+        if ((rc = hg_ntt_launch(ctx, kres.u32(), G * Pk, Pk, 0, true, st))) return rc;
+        uint32_t* t = kres.u32() + (size_t)G * kplane;
+        rc = hg_intt_fused(ctx, 1, t, kres.u32(), evk->d_kb, evk->d_ka, nullptr, Pk, st, G);
         if (rc) return rc < 0 ? hg_fail(HG_EINVAL, "batched key product not available") : rc;
         CrtFinish fin;
-        for (int k = 0; k < 4; ++k) fin.add[k] = d + (size_t)k * wn;   // d0_0 d1_0 d0_1 d1_1
+        for (int k = 0; k < 2 * G; ++k) fin.add[k] = d + (size_t)k * wn;   // d0_0 d1_0 d0_1 d1_1 ...
         fin.post = rescale_bits;
         OutSet kouts{};
-        for (int g = 0; g < 2; ++g) {
+        for (int g = 0; g < G; ++g) {
             kouts.out[2 * g] = out0s[g0 + g];
             kouts.out[2 * g + 1] = out1s[g0 + g];
         }
-        if ((rc = launch_crt(ctx, t, 4, Pk, evk->big_l, level, kouts, st, &fin, evk->prescaled))) return rc;
+        if ((rc = launch_crt(ctx, t, 2 * G, Pk, evk->big_l, level, kouts, st, &fin, evk->prescaled))) return rc;
+        g0 += G;
     }
     return HG_OK;
 }
