@@ -99,3 +99,40 @@ def test_mult_many_identical_to_one_by_one(log_n, level):
         one = eng.mult(a, b)
         assert torch.equal(one.c0.words, m.c0.words) and torch.equal(one.c1.words, m.c1.words)
         assert (one.level_bits, one.scale_bits, one.depth_ct) == (m.level_bits, m.scale_bits, m.depth_ct)
+
+
+def test_batched_products_rescan_with_addends():
+    """Four prepared products in one group whose relinearisation lands in the CRT's ambiguous
+    carry band (d2 = 1 and evk coefficients at 2^(L-1) - 1, 2^(L-1), ...): the exact rescan of
+    the fused finish must add each item's own (d0, d1) -- outputs 0..7 of one CRT launch --
+    and match the oracle's HeEngine.mult bit for bit."""
+    import paper_1902_04303_b200 as hg
+    from oracle import ckks_oracle as C
+    from paper_1902_04303_b200.ckks import Ciphertext
+    from paper_1902_04303_b200.keys import EvaluationKey
+    from paper_1902_04303_b200.ring import RingElement
+
+    n, level, big_l = 256, 400, 500
+    params = hg.CkksParams(log_n=8, log_l=big_l, log_p=45, log_p_small=30, h=16)
+    half = 1 << (big_l - 1)
+    kb = [0] * n
+    kb[0], kb[1] = half - 1, half
+    kb[2] = (1 << (2 * big_l)) - half - 1
+    kb[3] = (1 << big_l) + half - 1
+    rng = random.Random(21)
+    ka = [rng.getrandbits(2 * big_l) for _ in range(n)]
+    evk = EvaluationKey(b=RingElement(n, 2 * big_l, kb), a=RingElement(n, 2 * big_l, ka))
+    eng = hg.HeEngine(params, evk, None)
+    one = [1] + [0] * (n - 1)
+
+    def ct():
+        return Ciphertext(c0=RingElement(n, level, [rng.getrandbits(level) for _ in range(n)]),
+                          c1=RingElement(n, level, one), level_bits=level, scale_bits=45,
+                          slots=params.slot_count, params=params)
+
+    lhs, rhs = [ct() for _ in range(4)], [ct() for _ in range(4)]
+    outs = eng.mult_prepared_many([eng.prepare(a) for a in lhs], rhs)
+    for a, b, o in zip(lhs, rhs, outs):
+        want = C.engine_mult(a.c0.coeffs, a.c1.coeffs, b.c0.coeffs, b.c1.coeffs, level, kb, ka,
+                             big_l, 45, n)
+        assert (o.c0.coeffs, o.c1.coeffs) == want
