@@ -128,7 +128,7 @@ int hg_ct_mult(hg_ctx* ctx, const hg_key* evk, const uint32_t* a0, const uint32_
 typedef struct hg_ctprep hg_ctprep;
 int hg_ct_prepare(hg_ctx* ctx, const uint32_t* c0, const uint32_t* c1, int level, void* stream,
                   hg_ctprep** out);
-/* `count` independent hg_ct_mult_prepared products (a[i] (x) b_i -> out_i), two per group of
+/* `count` independent hg_ct_mult_prepared products (a[i] (x) b_i -> out_i), up to four per group of
  * launches so rows of a prime share twiddle loads and the persistent kernels get twice the
  * work per launch; outputs identical to hg_ct_mult_prepared's.  Replaces the per-term
  * HeEngine.mult of cp_rep_matmul (matrix.py:173-193) over the 245 duplicated projector
@@ -138,7 +138,7 @@ int hg_ct_mult_prepared_batch(hg_ctx* ctx, const hg_key* evk, int count, const h
                               int rescale_bits, uint32_t* const* out0s, uint32_t* const* out1s,
                               void* stream);
 /* `count` independent hg_ct_mult products (a_i (x) b_i, relinearised, rescaled by
- * rescale_bits), two per group of launches; outputs identical to hg_ct_mult's.  Replaces the
+ * rescale_bits), up to four per group of launches; outputs identical to hg_ct_mult's.  Replaces the
  * per-term HeEngine.mult of cp_matvec (matrix.py:99-106) and other independent products. */
 int hg_ct_mult_batch(hg_ctx* ctx, const hg_key* evk, int count, const uint32_t* const* a0s,
                      const uint32_t* const* a1s, const uint32_t* const* b0s, const uint32_t* const* b1s,

@@ -930,12 +930,12 @@ extern "C" int hg_ct_mult_prepared(hg_ctx* ctx, const hg_key* evk, const hg_ctpr
     return ct_mult_finish(ctx, evk, d0, d1, d2, e0, e1, level, rescale_bits, out0, out1, st);
 }
 
-// `count` products with resident left operands, two per group of launches: one ModUp of both
-// right operands, one forward NTT over [2][2][P][N] (rows of a prime adjacent: twiddles shared),
-// one 6-output tensor CRT, and for the relinearisation one ModUp of both d2, one forward NTT
-// over [2][P'][N] (two rows per block instead of one), one batched key product fused into the
-// inverse NTT and one 4-output CRT with the add + rescale finish.  Each output is identical to
-// hg_ct_mult_prepared's.
+// `count` products with resident left operands, up to four per group of launches: ModUps of the
+// right operands two items at a time, one forward NTT over all of the group's rows (rows of a
+// prime adjacent: twiddles shared), 6-output tensor CRTs, and for the relinearisation one
+// ModUp of all d2, one forward NTT over [G][P'][N] (two rows per block instead of one), one
+// batched key product fused into the inverse NTT and one 2G-output CRT with the add + rescale
+// finish.  Each output is identical to hg_ct_mult_prepared's.
 extern "C" int hg_ct_mult_prepared_batch(hg_ctx* ctx, const hg_key* evk, int count,
                                          const hg_ctprep* const* a, const uint32_t* const* b0s,
                                          const uint32_t* const* b1s, int level, int rescale_bits,
@@ -1029,10 +1029,10 @@ extern "C" int hg_ct_mult_prepared_batch(hg_ctx* ctx, const hg_key* evk, int cou
     return HG_OK;
 }
 
-// `count` products of ciphertext pairs (a_i (x) b_i, relinearised, rescaled), two per group of
-// launches: one ModUp per pair of items' four polynomials, one forward NTT over all eight rows
-// of a prime group, then the same tensor CRT / paired key switch / finish as
-// hg_ct_mult_prepared_batch.  Each output is identical to hg_ct_mult's.
+// `count` products of ciphertext pairs (a_i (x) b_i, relinearised, rescaled), up to four per group
+// of launches: one ModUp per item's four polynomials, one forward NTT over all rows of the
+// group, then the same tensor CRT / batched key switch / finish as hg_ct_mult_prepared_batch.
+// Each output is identical to hg_ct_mult's.
 extern "C" int hg_ct_mult_batch(hg_ctx* ctx, const hg_key* evk, int count, const uint32_t* const* a0s,
                                 const uint32_t* const* a1s, const uint32_t* const* b0s,
                                 const uint32_t* const* b1s, int level, int rescale_bits,
@@ -1045,68 +1045,76 @@ extern "C" int hg_ct_mult_batch(hg_ctx* ctx, const hg_key* evk, int count, const
     const int Pk = evk->P;
     const bool fused = fuse_pointwise() && crt_finish_ok(ctx, Pk, evk->big_l, level);
     const int P = tensor_sum_primes(ctx, level, 1);
-    const bool prescale = fused && crt_prescale_ok(ctx, P, 0, level);
+    const bool prescale = fused && P > 0 && crt_prescale_ok(ctx, P, 0, level);
     int rc;
-    for (int g0 = 0; g0 < count; g0 += 2) {
-        const int G = count - g0 < 2 ? count - g0 : 2;
+    for (int g0 = 0; g0 < count;) {
+        const int G = count - g0 < 4 ? count - g0 : 4;
         if (!fused || G == 1 || P < 0) {
             for (int g = 0; g < G; ++g)
                 if ((rc = hg_ct_mult(ctx, evk, a0s[g0 + g], a1s[g0 + g], b0s[g0 + g], b1s[g0 + g], level,
                                      rescale_bits, out0s[g0 + g], out1s[g0 + g], stream)))
                     return rc;
+            g0 += G;
             continue;
         }
         cudaStream_t st = (cudaStream_t)stream;
         const size_t plane = (size_t)P * N, kplane = (size_t)Pk * N, wn = (size_t)W * N;
         Scratch res(st), tens(st), kres(st), buf(st);
-        HG_CUDA_TRY(res.alloc(8 * plane * 4));          // [2 items][a0, a1, b0, b1][P][N]
-        HG_CUDA_TRY(tens.alloc(6 * plane * 4));
-        HG_CUDA_TRY(kres.alloc(6 * kplane * 4));
-        HG_CUDA_TRY(buf.alloc(6 * wn * 4));
-        for (int g = 0; g < 2; ++g) {
+        HG_CUDA_TRY(res.alloc((size_t)4 * G * plane * 4));     // [G items][a0, a1, b0, b1][P][N]
+        HG_CUDA_TRY(tens.alloc((size_t)3 * G * plane * 4));
+        HG_CUDA_TRY(kres.alloc((size_t)3 * G * kplane * 4));
+        HG_CUDA_TRY(buf.alloc((size_t)3 * G * wn * 4));
+        for (int g = 0; g < G; ++g) {
             OperandSet ops{};
             const uint32_t* src[4] = {a0s[g0 + g], a1s[g0 + g], b0s[g0 + g], b1s[g0 + g]};
             for (int k = 0; k < 4; ++k) { ops.words[k] = src[k]; ops.bits[k] = level; ops.is_signed[k] = 1; }
             if ((rc = launch_modup(ctx, ops, 4, P, res.u32() + (size_t)4 * g * plane, 0, st))) return rc;
         }
-        if ((rc = hg_ntt_launch(ctx, res.u32(), 8 * P, P, 0, true, st))) return rc;
+        if ((rc = hg_ntt_launch(ctx, res.u32(), 4 * G * P, P, 0, true, st))) return rc;
         // every tensor term has exactly one a factor: carrying the CRT constants on a0, a1
         // lets the CRT skip its own constant product (as a prepared operand does)
         if (prescale)
-            for (int g = 0; g < 2; ++g)
+            for (int g = 0; g < G; ++g)
                 if ((rc = prescale_rows(ctx, res.u32() + (size_t)4 * g * plane, 2, P, st))) return rc;
-        for (int g = 0; g < 2; ++g) {
+        for (int g = 0; g < G; ++g) {
             const uint32_t* r = res.u32() + (size_t)4 * g * plane;
             rc = hg_intt_fused(ctx, 2, tens.u32() + (size_t)3 * g * plane, r, r + plane, r + 2 * plane,
                                r + 3 * plane, P, st);
             if (rc) return rc < 0 ? hg_fail(HG_EINVAL, "fused tensor product not available") : rc;
         }
         uint32_t* d = buf.u32();
-        OutSet touts{};
-        for (int g = 0; g < 2; ++g) {
-            touts.out[3 * g] = d + (size_t)(2 * g) * wn;
-            touts.out[3 * g + 1] = d + (size_t)(2 * g + 1) * wn;
-            touts.out[3 * g + 2] = d + (size_t)(4 + g) * wn;
+        for (int h = 0; h < G; h += 2) {
+            const int gh = G - h < 2 ? G - h : 2;
+            OutSet touts{};
+            for (int k = 0; k < gh; ++k) {
+                const int g = h + k;
+                touts.out[3 * k] = d + (size_t)(2 * g) * wn;
+                touts.out[3 * k + 1] = d + (size_t)(2 * g + 1) * wn;
+                touts.out[3 * k + 2] = d + (size_t)(2 * G + g) * wn;
+            }
+            if ((rc = launch_crt(ctx, tens.u32() + (size_t)3 * h * plane, 3 * gh, P, 0, level, touts, st,
+                                 nullptr, prescale)))
+                return rc;
         }
-        if ((rc = launch_crt(ctx, tens.u32(), 6, P, 0, level, touts, st, nullptr, prescale))) return rc;
         OperandSet kops{};
-        for (int g = 0; g < 2; ++g) {
-            kops.words[g] = d + (size_t)(4 + g) * wn; kops.bits[g] = level; kops.is_signed[g] = 0;
+        for (int g = 0; g < G; ++g) {
+            kops.words[g] = d + (size_t)(2 * G + g) * wn; kops.bits[g] = level; kops.is_signed[g] = 0;
         }
-        if ((rc = launch_modup(ctx, kops, 2, Pk, kres.u32(), 0, st))) return rc;
-        if ((rc = hg_ntt_launch(ctx, kres.u32(), 2 * Pk, Pk, 0, true, st))) return rc;
-        uint32_t* t = kres.u32() + 2 * kplane;
-        rc = hg_intt_fused(ctx, 1, t, kres.u32(), evk->d_kb, evk->d_ka, nullptr, Pk, st, 2);
+        if ((rc = launch_modup(ctx, kops, G, Pk, kres.u32(), 0, st))) return rc;
+        if ((rc = hg_ntt_launch(ctx, kres.u32(), G * Pk, Pk, 0, true, st))) return rc;
+        uint32_t* t = kres.u32() + (size_t)G * kplane;
+        rc = hg_intt_fused(ctx, 1, t, kres.u32(), evk->d_kb, evk->d_ka, nullptr, Pk, st, G);
         if (rc) return rc < 0 ? hg_fail(HG_EINVAL, "batched key product not available") : rc;
         CrtFinish fin;
-        for (int k = 0; k < 4; ++k) fin.add[k] = d + (size_t)k * wn;
+        for (int k = 0; k < 2 * G; ++k) fin.add[k] = d + (size_t)k * wn;
         fin.post = rescale_bits;
         OutSet kouts{};
-        for (int g = 0; g < 2; ++g) {
+        for (int g = 0; g < G; ++g) {
             kouts.out[2 * g] = out0s[g0 + g];
             kouts.out[2 * g + 1] = out1s[g0 + g];
         }
-        if ((rc = launch_crt(ctx, t, 4, Pk, evk->big_l, level, kouts, st, &fin, evk->prescaled))) return rc;
+        if ((rc = launch_crt(ctx, t, 2 * G, Pk, evk->big_l, level, kouts, st, &fin, evk->prescaled))) return rc;
+        g0 += G;
     }
     return HG_OK;
 }
