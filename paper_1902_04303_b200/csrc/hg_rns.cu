@@ -1275,8 +1275,10 @@ extern "C" int hg_ct_automorph_batch(hg_ctx* ctx, const hg_key* key, int count,
     if ((kk & 1) == 0) return hg_fail(HG_EINVAL, "automorphism exponent must be odd");
     const int64_t kinv = kk == 1 ? 0 : inverse_mod_2n(kk, n2);
     int rc;
-    for (int g0 = 0; g0 < count; g0 += 4) {
-        const int G = count - g0 < 4 ? count - g0 : 4;
+    static const int gmax = getenv("HG_ROT_G") ? atoi(getenv("HG_ROT_G")) : 4;   // 8: no gain measured
+    for (int g0 = 0; g0 < count; g0 += gmax) {
+        int G = count - g0 < gmax ? count - g0 : gmax;
+        if (G > 8) G = 8;
         if (G == 1 || !fuse_pointwise()) {
             for (int g = 0; g < G; ++g)
                 if ((rc = hg_ct_automorph(ctx, key, c0s[g0 + g], c1s[g0 + g], level, k, out0s[g0 + g],
@@ -1290,25 +1292,33 @@ extern "C" int hg_ct_automorph_batch(hg_ctx* ctx, const hg_key* key, int count,
         Scratch res(st), buf(st);
         HG_CUDA_TRY(res.alloc((size_t)3 * G * P * N * 4));   // x residues [G][P][N], products [G][2][P][N]
         HG_CUDA_TRY(buf.alloc((size_t)2 * G * W * N * 4));   // automorphed c0 and key-switch e0 per item
-        OperandSet ops{};
-        for (int g = 0; g < G; ++g) {
-            ops.words[g] = c1s[g0 + g]; ops.bits[g] = level; ops.is_signed[g] = 0;   // canonical rep
+        for (int h = 0; h < G; h += 4) {   // ModUp: up to 4 gathered c1 per launch
+            const int gh = G - h < 4 ? G - h : 4;
+            OperandSet ops{};
+            for (int g = 0; g < gh; ++g) {
+                ops.words[g] = c1s[g0 + h + g]; ops.bits[g] = level; ops.is_signed[g] = 0;   // canonical rep
+            }
+            if ((rc = launch_modup(ctx, ops, gh, P, res.u32() + (size_t)h * P * N, kinv, st))) return rc;
         }
-        if ((rc = launch_modup(ctx, ops, G, P, res.u32(), kinv, st))) return rc;
         if ((rc = hg_ntt_launch(ctx, res.u32(), G * P, P, 0, true, st))) return rc;
         uint32_t* t = res.u32() + (size_t)G * P * N;
         rc = hg_intt_fused(ctx, 1, t, res.u32(), key->d_kb, key->d_ka, nullptr, P, st, G);
         if (rc) return rc < 0 ? hg_fail(HG_EINVAL, "batched key product not available") : rc;
-        OutSet outs{};
-        for (int g = 0; g < G; ++g) {
-            outs.out[2 * g] = buf.u32() + (size_t)(2 * g + 1) * W * N;   // e0_g
-            outs.out[2 * g + 1] = out1s[g0 + g];
+        for (int h = 0; h < G; h += 4) {   // CRT: up to 8 outputs (4 items) per launch
+            const int gh = G - h < 4 ? G - h : 4;
+            OutSet outs{};
+            for (int g = 0; g < gh; ++g) {
+                outs.out[2 * g] = buf.u32() + (size_t)(2 * (h + g) + 1) * W * N;   // e0
+                outs.out[2 * g + 1] = out1s[g0 + h + g];
+            }
+            if ((rc = launch_crt(ctx, t + (size_t)2 * h * P * N, 2 * gh, P, key->big_l, level, outs, st,
+                                 nullptr, key->prescaled)))
+                return rc;
         }
-        if ((rc = launch_crt(ctx, t, 2 * G, P, key->big_l, level, outs, st, nullptr, key->prescaled))) return rc;
         for (int g = 0; g < G; ++g) {
             uint32_t* a0 = buf.u32() + (size_t)(2 * g) * W * N;
             if ((rc = hg_ew_automorphism(ctx, a0, c0s[g0 + g], level, k, st))) return rc;
-            if ((rc = hg_ew_add(ctx, out0s[g0 + g], a0, outs.out[2 * g], level, false, st))) return rc;
+            if ((rc = hg_ew_add(ctx, out0s[g0 + g], a0, a0 + (size_t)W * N, level, false, st))) return rc;
         }
     }
     return HG_OK;
