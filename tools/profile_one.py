@@ -32,8 +32,11 @@ def main():
     a = hg.mod_down(hg.encrypt_values(vals, 45, pk, params, gen), args.level)
     b = hg.mod_down(hg.encrypt_values(vals[::-1], 45, pk, params, gen), args.level)
     mask = eng.mask(("slot", 3))
+    preps = [eng.prepare(a) for _ in range(4)]
     ops = {"mult": lambda: eng.mult(a, b), "rotate": lambda: eng.rotate(a, 1),
-           "mult_plain": lambda: eng.mult_plain(a, mask)}
+           "mult_plain": lambda: eng.mult_plain(a, mask),
+           # the batch step's unit of work: four products with resident left operands
+           "mult4": lambda: eng.mult_prepared_many(preps, [b] * 4)}
     fn = ops[args.op]
     for _ in range(2):
         fn()
