@@ -19,8 +19,12 @@
 namespace {
 
 constexpr int kTile = 2048;  // words per shared-memory tile
+// occupancy bounds (minimum resident blocks per SM), measured on the config-3 batch step:
 #ifndef HG_FUSED_MINB
-#define HG_FUSED_MINB 4   // 64 registers: 4 blocks per SM instead of 3 (measured -2.7 ms of NTT per step)
+#define HG_FUSED_MINB 4   // fused inverse pass, 72 -> 64 registers, 3 -> 4 blocks: -2.7 ms of NTT
+#endif
+#ifndef HG_HI_MINB
+#define HG_HI_MINB 5      // strided pass (3-row variant 64 -> 48 registers): -15 ms of NTT
 #endif
 
 __device__ __forceinline__ void fwd_bfly(uint32_t& x, uint32_t& y, uint2 w, uint32_t p) {
@@ -264,7 +268,7 @@ __global__ void __launch_bounds__(256) ntt_lo8_kernel(uint32_t* __restrict__ dat
 // Strided stages [0, K1), K1 in {3, 6}: tile of 2^K1 rows (stride 2^k2) x (2048 >> K1)
 // columns; thread = (column c, row group g) holding 8 rows.  K1 = 3 needs no shared memory.
 template <bool FWD, int K1, int RB>
-__global__ void __launch_bounds__(256) ntt_hi8_kernel(uint32_t* __restrict__ data, int log_n,
+__global__ void __launch_bounds__(256, HG_HI_MINB) ntt_hi8_kernel(uint32_t* __restrict__ data, int log_n,
                                                       int P, int bb0, int prime_offset,
                                                       const PrimeInfo* __restrict__ pinfo,
                                                       const uint2* __restrict__ tw) {
