@@ -23,6 +23,9 @@ constexpr int kTile = 2048;  // words per shared-memory tile
 #ifndef HG_FUSED_MINB
 #define HG_FUSED_MINB 4   // fused inverse pass, 72 -> 64 registers, 3 -> 4 blocks: -2.7 ms of NTT
 #endif
+#ifndef HG_LO_MINB
+#define HG_LO_MINB 1      // contiguous pass: 40 registers already give 6 blocks
+#endif
 #ifndef HG_HI_MINB
 #define HG_HI_MINB 5      // strided pass (3-row variant 64 -> 48 registers): -15 ms of NTT
 #endif
@@ -242,7 +245,7 @@ __device__ __forceinline__ void lo_round(uint32_t (&x)[RB][8], uint32_t* __restr
 // grid = (N >> K2 chunks, batch-row groups of RB, primes): prime-major scheduling keeps the
 // prime's twiddles in L2 while its batch rows pass.
 template <bool FWD, int K2, int RB>
-__global__ void __launch_bounds__(256) ntt_lo8_kernel(uint32_t* __restrict__ data, int log_n,
+__global__ void __launch_bounds__(256, HG_LO_MINB) ntt_lo8_kernel(uint32_t* __restrict__ data, int log_n,
                                                       int P, int bb0, int prime_offset,
                                                       const PrimeInfo* __restrict__ pinfo,
                                                       const uint2* __restrict__ tw) {
