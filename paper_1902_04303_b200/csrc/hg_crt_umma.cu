@@ -570,12 +570,23 @@ __global__ void __launch_bounds__(PipeCfg<FUSED>::kWarps * 32, 1) crt_umma_pipe_
     const int out_w = (out_bits + 31) >> 5;
     const int T = sw + out_w + (sbit ? 1 : 0);
     const int jpt = (T - tb0 + kJobCols - 1) / kJobCols;   // jobs (column blocks) per tile
+    // job width: the tile's columns split evenly over its jobs, in multiples of 8 words (the B
+    // image granule), the last job taking the remainder (<= 32).  The two epilogue groups take
+    // alternate jobs and the carry chain runs through them in order, so an even split keeps
+    // one group from waiting on a 32-column job while the other has a short tail.
+    const int jc = [&] {
+        const int total = T - tb0;
+        int w = (((total + jpt - 1) / jpt) / 8) * 8;
+        if (w < 8) w = 8;
+        if (total - (jpt - 1) * w > kJobCols) w += 8;
+        return w > kJobCols ? kJobCols : w;
+    }();
     const int ntiles = nouts * tpo;
     const int nkc = P32p / 32;
     // columns of job block h: [tb0 + 32h, min(T, tb0 + 32h + 32)), padded to an even count
     auto job_cols = [&](int h) {
-        const int c0 = tb0 + h * kJobCols;
-        const int c = (T - c0 < kJobCols ? T - c0 : kJobCols);
+        const int c0 = tb0 + h * jc;
+        const int c = h == jpt - 1 ? T - c0 : (T - c0 < jc ? T - c0 : jc);
         return (c + 1) & ~1;
     };
 
@@ -609,7 +620,7 @@ __global__ void __launch_bounds__(PipeCfg<FUSED>::kWarps * 32, 1) crt_umma_pipe_
             for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
               for (int h = 0; h < jpt; ++h) {
                 const uint32_t bytes = (uint32_t)((job_cols(h) + 7) >> 3) * 8192u;
-                const uint8_t* bsrc = Bpipe + (size_t)((tb0 >> 3) + h * (kJobCols / 8)) * 8192;
+                const uint8_t* bsrc = Bpipe + (size_t)((tb0 >> 3) + h * (jc / 8)) * 8192;
                 for (int kc = 0; kc < nkc; ++kc, ++it) {
                     const int s = it % kRB;
                     PWAIT(0, smem_u32(&bar_b_empty[s]), ((it / kRB) & 1) ^ 1);
@@ -658,7 +669,7 @@ __global__ void __launch_bounds__(PipeCfg<FUSED>::kWarps * 32, 1) crt_umma_pipe_
             for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
                 for (int h = 0; h < jpt; ++h, ++ij) {
                     const int oy = tile / tpo, cb = (tile - oy * tpo) * kRows;
-                    const int ubase = tb0 + h * kJobCols - sw - (sbit ? 1 : 0);
+                    const int ubase = tb0 + h * jc - sw - (sbit ? 1 : 0);
                     const int s = ij & 1;
                     PWAIT(0, smem_u32(&bar_add_empty[s]), ((ij >> 1) & 1) ^ 1);
                     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -796,7 +807,7 @@ __global__ void __launch_bounds__(PipeCfg<FUSED>::kWarps * 32, 1) crt_umma_pipe_
                 prev2 = hv2.y;
             }
             const int tb = ij & 1;
-            const int c0 = tb0 + h * kJobCols;
+            const int c0 = tb0 + h * jc;
             const int ncols = job_cols(h);
             // the job's addend words (output word u = c0 + k - sw - (sbit != 0)), loaded before
             // the accumulator wait so their latency is off the carry chain
