@@ -174,6 +174,12 @@ int hg_ct_automorph(hg_ctx* ctx, const hg_key* key, const uint32_t* c0, const ui
 int hg_ct_automorph_batch(hg_ctx* ctx, const hg_key* key, int count, const uint32_t* const* c0s,
                           const uint32_t* const* c1s, int level, int64_t k,
                           uint32_t* const* out0s, uint32_t* const* out1s, void* stream);
+/* As hg_ct_automorph_batch, accumulating: out_i = c_i + phi_k(c_i) key-switched -- one step of
+ * the rotate-and-sum ladders (c += rot(c, 2^j), matrix.py:79-170) in one call, identical to the
+ * rotation followed by the ciphertext add. */
+int hg_ct_rotate_add_batch(hg_ctx* ctx, const hg_key* key, int count, const uint32_t* const* c0s,
+                           const uint32_t* const* c1s, int level, int64_t k, uint32_t* const* out0s,
+                           uint32_t* const* out1s, void* stream);
 
 /* ---- microbenchmarks / measurement ------------------------------------------------ */
 /* Batched forward+inverse negacyclic NTT over `count` length-N rows of residues

@@ -65,6 +65,8 @@ SIGNATURES = {
     "hg_ct_automorph": (_i, [_vp, _vp, _vp, _vp, _i, _i64, _vp, _vp, _vp]),
     "hg_ct_automorph_batch": (_i, [_vp, _vp, _i, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _i, _i64,
                                    ctypes.POINTER(_vp), ctypes.POINTER(_vp), _vp]),
+"hg_ct_rotate_add_batch": (_i, [_vp, _vp, _i, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _i, _i64,
+                                   ctypes.POINTER(_vp), ctypes.POINTER(_vp), _vp]),
     "hg_ct_prepare": (_i, [_vp, _vp, _vp, _i, _vp, ctypes.POINTER(_vp)]),
     "hg_ct_mult_batch": (_i, [_vp, _vp, _i, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp),
                               ctypes.POINTER(_vp), _i, _i, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _vp]),

@@ -1260,10 +1260,29 @@ extern "C" int hg_ct_automorph(hg_ctx* ctx, const hg_key* key, const uint32_t* c
 // launches: one ModUp of the 4 c1 gathers, one forward NTT over [4][P][N] (twiddle loads
 // shared by the rows of a prime), one batched key product fused into the inverse NTT and one
 // 8-output CRT -- instead of 4 separate chains.  Each output is identical to hg_ct_automorph's.
+static int automorph_batch_impl(hg_ctx* ctx, const hg_key* key, int count, const uint32_t* const* c0s,
+                                const uint32_t* const* c1s, int level, int64_t k, uint32_t* const* out0s,
+                                uint32_t* const* out1s, void* stream, bool acc);
+
 extern "C" int hg_ct_automorph_batch(hg_ctx* ctx, const hg_key* key, int count,
                                      const uint32_t* const* c0s, const uint32_t* const* c1s,
                                      int level, int64_t k, uint32_t* const* out0s,
                                      uint32_t* const* out1s, void* stream) {
+    return automorph_batch_impl(ctx, key, count, c0s, c1s, level, k, out0s, out1s, stream, false);
+}
+
+// out_i = c_i + phi_k(c_i) key-switched: one step of the rotate-and-sum ladders (matrix.py
+// rotate_sum: c += rot(c, 2^j)) without a separate ciphertext add per item
+extern "C" int hg_ct_rotate_add_batch(hg_ctx* ctx, const hg_key* key, int count,
+                                      const uint32_t* const* c0s, const uint32_t* const* c1s,
+                                      int level, int64_t k, uint32_t* const* out0s,
+                                      uint32_t* const* out1s, void* stream) {
+    return automorph_batch_impl(ctx, key, count, c0s, c1s, level, k, out0s, out1s, stream, true);
+}
+
+static int automorph_batch_impl(hg_ctx* ctx, const hg_key* key, int count, const uint32_t* const* c0s,
+                                const uint32_t* const* c1s, int level, int64_t k, uint32_t* const* out0s,
+                                uint32_t* const* out1s, void* stream, bool acc) {
     if (!ctx || !key || key->level != level || count < 0 || (count && (!c0s || !c1s || !out0s || !out1s)))
         return hg_fail(HG_EINVAL, "hg_ct_automorph_batch: bad arguments (key must be prepared at the level)");
     cudaStream_t st = (cudaStream_t)stream;
@@ -1279,19 +1298,31 @@ extern "C" int hg_ct_automorph_batch(hg_ctx* ctx, const hg_key* key, int count,
     for (int g0 = 0; g0 < count; g0 += gmax) {
         int G = count - g0 < gmax ? count - g0 : gmax;
         if (G > 8) G = 8;
-        if (G == 1 || !fuse_pointwise()) {
+        if (!acc && (G == 1 || !fuse_pointwise())) {
             for (int g = 0; g < G; ++g)
                 if ((rc = hg_ct_automorph(ctx, key, c0s[g0 + g], c1s[g0 + g], level, k, out0s[g0 + g],
                                           out1s[g0 + g], stream)))
                     return rc;
             continue;
         }
+        if (acc && !fuse_pointwise()) {
+            for (int g = 0; g < G; ++g) {
+                Scratch t2(st);
+                HG_CUDA_TRY(t2.alloc((size_t)2 * W * N * 4));
+                uint32_t* r0 = t2.u32();
+                uint32_t* r1 = r0 + (size_t)W * N;
+                if ((rc = hg_ct_automorph(ctx, key, c0s[g0 + g], c1s[g0 + g], level, k, r0, r1, stream))) return rc;
+                if ((rc = hg_ew_add(ctx, out0s[g0 + g], c0s[g0 + g], r0, level, false, st))) return rc;
+                if ((rc = hg_ew_add(ctx, out1s[g0 + g], c1s[g0 + g], r1, level, false, st))) return rc;
+            }
+            continue;
+        }
         for (int g = 0; g < G; ++g)
-            if (out0s[g0 + g] == c0s[g0 + g] || out0s[g0 + g] == c1s[g0 + g])
+            if (out0s[g0 + g] == c0s[g0 + g] || out0s[g0 + g] == c1s[g0 + g] || out1s[g0 + g] == c1s[g0 + g])
                 return hg_fail(HG_EINVAL, "hg_ct_automorph_batch: outputs must not alias inputs");
         Scratch res(st), buf(st);
         HG_CUDA_TRY(res.alloc((size_t)3 * G * P * N * 4));   // x residues [G][P][N], products [G][2][P][N]
-        HG_CUDA_TRY(buf.alloc((size_t)2 * G * W * N * 4));   // automorphed c0 and key-switch e0 per item
+        HG_CUDA_TRY(buf.alloc((size_t)(acc ? 3 : 2) * G * W * N * 4));   // automorphed c0, e0 per item (+ e1 with acc)
         for (int h = 0; h < G; h += 4) {   // ModUp: up to 4 gathered c1 per launch
             const int gh = G - h < 4 ? G - h : 4;
             OperandSet ops{};
@@ -1309,7 +1340,7 @@ extern "C" int hg_ct_automorph_batch(hg_ctx* ctx, const hg_key* key, int count,
             OutSet outs{};
             for (int g = 0; g < gh; ++g) {
                 outs.out[2 * g] = buf.u32() + (size_t)(2 * (h + g) + 1) * W * N;   // e0
-                outs.out[2 * g + 1] = out1s[g0 + h + g];
+                outs.out[2 * g + 1] = acc ? buf.u32() + (size_t)(2 * G + h + g) * W * N : out1s[g0 + h + g];
             }
             if ((rc = launch_crt(ctx, t + (size_t)2 * h * P * N, 2 * gh, P, key->big_l, level, outs, st,
                                  nullptr, key->prescaled)))
@@ -1318,7 +1349,15 @@ extern "C" int hg_ct_automorph_batch(hg_ctx* ctx, const hg_key* key, int count,
         for (int g = 0; g < G; ++g) {
             uint32_t* a0 = buf.u32() + (size_t)(2 * g) * W * N;
             if ((rc = hg_ew_automorphism(ctx, a0, c0s[g0 + g], level, k, st))) return rc;
-            if ((rc = hg_ew_add(ctx, out0s[g0 + g], a0, a0 + (size_t)W * N, level, false, st))) return rc;
+            if (acc) {   // out0 = c0 + (phi(c0) + e0), out1 = c1 + e1 (exact mod 2^level)
+                if ((rc = hg_ew_add(ctx, a0, a0, a0 + (size_t)W * N, level, false, st))) return rc;
+                if ((rc = hg_ew_add(ctx, out0s[g0 + g], c0s[g0 + g], a0, level, false, st))) return rc;
+                if ((rc = hg_ew_add(ctx, out1s[g0 + g], c1s[g0 + g], buf.u32() + (size_t)(2 * G + g) * W * N,
+                                    level, false, st)))
+                    return rc;
+            } else if ((rc = hg_ew_add(ctx, out0s[g0 + g], a0, a0 + (size_t)W * N, level, false, st))) {
+                return rc;
+            }
         }
     }
     return HG_OK;

@@ -101,6 +101,35 @@ def test_mult_many_identical_to_one_by_one(log_n, level):
         assert (one.level_bits, one.scale_bits, one.depth_ct) == (m.level_bits, m.scale_bits, m.depth_ct)
 
 
+@pytest.mark.parametrize("log_n,count,step", [(12, 5, 4), (17, 1, 64), (17, 6, 1)])
+def test_rotate_add_many_identical_to_rotate_then_add(log_n, count, step):
+    """hg_ct_rotate_add_batch (one rotate-and-sum ladder step, the add fused into the batched
+    key switch) writes exactly add(ct, rotate(ct, step)) for each ciphertext, with the same
+    metadata and op counts."""
+    import torch
+
+    import paper_1902_04303_b200 as hg
+
+    params = hg.CkksParams(log_n=log_n, log_l=1700, log_p=45, log_p_small=30)
+    sk, pk, evk, rot = hg.keygen(params, 9, device_rng=True)
+    eng = hg.HeEngine(params, evk, rot)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(3)
+    vals = np.random.default_rng(2).uniform(-1, 1, params.slot_count)
+    cts = [hg.mod_down(hg.encrypt_values(vals, params.log_p, pk, params, gen), 1400) for _ in range(count)]
+    with hg.track_ops() as fused_ops:
+        fused = eng.rotate_add_many(cts, step)
+    with hg.track_ops() as one_ops:
+        ones = [eng.add(c, eng.rotate(c, step)) for c in cts]
+    assert fused_ops.rotation_amounts == one_ops.rotation_amounts
+    assert fused_ops.keyswitches == one_ops.keyswitches == count
+    for one, f in zip(ones, fused):
+        assert torch.equal(one.c0.words, f.c0.words) and torch.equal(one.c1.words, f.c1.words)
+        assert (one.level_bits, one.scale_bits, one.depth_ct) == (f.level_bits, f.scale_bits, f.depth_ct)
+    got = hg.decrypt_values(fused[0], sk)
+    assert np.max(np.abs(got - (vals + np.roll(vals, step)))) < 1e-4
+
+
 def test_batched_products_rescan_with_addends():
     """Four prepared products in one group whose relinearisation lands in the CRT's ambiguous
     carry band (d2 = 1 and evk coefficients at 2^(L-1) - 1, 2^(L-1), ...): the exact rescan of
