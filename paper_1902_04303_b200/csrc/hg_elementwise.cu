@@ -184,6 +184,49 @@ __global__ void __launch_bounds__(kThreads) automorphism_kernel(uint32_t* __rest
     }
 }
 
+// The CRT-finish addends of a batched rotation (hg_rns.cu automorph_batch_impl), item g =
+// blockIdx.y: dst[2g] = phi(c0_g) (+ c0_g with acc), dst[2g+1] = c1_g with acc, else 0 -- so the
+// key switch's epilogue writes phi(c0) + e0 (+ c0) and e1 (+ c1) straight to the outputs
+struct AutoItems {
+    const uint32_t* c0[4];
+    const uint32_t* c1[4];
+};
+__global__ void __launch_bounds__(kThreads) automorph_addend_kernel(uint32_t* __restrict__ dst, AutoItems it,
+                                                                    int acc, int W, int bits, int N,
+                                                                    int64_t kinv) {
+    const int i = blockIdx.x * kThreads + threadIdx.x;
+    if (i >= N) return;
+    const int g = blockIdx.y;
+    const uint32_t* __restrict__ a = it.c0[g];
+    const uint32_t* __restrict__ c1 = it.c1[g];
+    uint32_t* __restrict__ d0 = dst + (size_t)(2 * g) * W * N;
+    uint32_t* __restrict__ d1 = d0 + (size_t)W * N;
+    int64_t j = ((int64_t)i * kinv) & (2ll * N - 1);
+    const bool neg = j >= N;
+    const int src = (int)(neg ? j - N : j);
+    uint32_t ncarry = 1u;   // -x = ~x + 1
+    uint64_t carry = 0;
+    for (int w = 0; w < W; ++w) {
+        const size_t o = (size_t)w * N;
+        uint32_t x = a[o + src];
+        if (neg) {
+            uint64_t s = (uint64_t)(~x) + ncarry;
+            x = (uint32_t)s;
+            ncarry = (uint32_t)(s >> 32);
+        }
+        uint64_t s = carry + x + (acc ? a[o + i] : 0u);
+        uint32_t r = (uint32_t)s;
+        carry = s >> 32;
+        uint32_t r1 = acc ? c1[o + i] : 0u;
+        if (w == W - 1) {
+            r &= mask_for(bits);
+            r1 &= mask_for(bits);
+        }
+        d0[o + i] = r;
+        d1[o + i] = r1;
+    }
+}
+
 // out (+)= sum of up to kSumTerms polys: one thread per coefficient, 64-bit column sums with
 // the carry taken word to word; the loads of one word over all terms are independent
 constexpr int kSumTerms = 64;
@@ -248,6 +291,26 @@ int hg_ew_automorphism(hg_ctx* ctx, uint32_t* out, const uint32_t* a, int bits, 
     HgTimed tm(ctx, st, HG_K_ELEMENTWISE, (double)ctx->N);
     automorphism_kernel<<<grid_for(ctx->N), kThreads, 0, st>>>(out, a, words_for_bits(bits), bits,
                                                                ctx->N, inv_mod_pow2(kk, n2));
+    HG_LAUNCH_CHECK(ctx);
+    return HG_OK;
+}
+
+int hg_ew_automorph_addends(hg_ctx* ctx, uint32_t* dst, const uint32_t* const* c0s,
+                            const uint32_t* const* c1s, int G, int bits, int64_t k, bool acc,
+                            cudaStream_t st) {
+    int64_t n2 = 2ll * ctx->N;
+    int64_t kk = ((k % n2) + n2) % n2;
+    if ((kk & 1) == 0 || G < 1 || G > 4) return hg_fail(HG_EINVAL, "automorph addends: bad arguments");
+    AutoItems it{};
+    for (int g = 0; g < G; ++g) {
+        it.c0[g] = c0s[g];
+        it.c1[g] = c1s[g];
+    }
+    HgTimed tm(ctx, st, HG_K_ELEMENTWISE, (double)ctx->N * G);
+    dim3 grid = grid_for(ctx->N);
+    grid.y = G;
+    automorph_addend_kernel<<<grid, kThreads, 0, st>>>(dst, it, acc ? 1 : 0, words_for_bits(bits), bits,
+                                                       ctx->N, inv_mod_pow2(kk, n2));
     HG_LAUNCH_CHECK(ctx);
     return HG_OK;
 }

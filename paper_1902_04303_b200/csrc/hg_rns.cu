@@ -19,6 +19,9 @@ int hg_ew_add(hg_ctx* ctx, uint32_t* out, const uint32_t* a, const uint32_t* b, 
               bool subtract, cudaStream_t stream);
 int hg_ew_divide_round(hg_ctx* ctx, uint32_t* out, int out_bits, const uint32_t* a,
                        int in_bits, int shift, cudaStream_t stream);
+int hg_ew_automorph_addends(hg_ctx* ctx, uint32_t* dst, const uint32_t* const* c0s,
+                            const uint32_t* const* c1s, int G, int bits, int64_t k, bool acc,
+                            cudaStream_t st);
 int hg_ew_automorphism(hg_ctx* ctx, uint32_t* out, const uint32_t* a, int bits, int64_t k,
                        cudaStream_t stream);
 int hg_intt_fused(hg_ctx* ctx, int pre, uint32_t* out, const uint32_t* i0, const uint32_t* i1,
@@ -1295,6 +1298,7 @@ static int automorph_batch_impl(hg_ctx* ctx, const hg_key* key, int count, const
     const int64_t kinv = kk == 1 ? 0 : inverse_mod_2n(kk, n2);
     int rc;
     static const int gmax = getenv("HG_ROT_G") ? atoi(getenv("HG_ROT_G")) : 4;   // 8: no gain measured
+    const bool fin_ok = crt_finish_ok(ctx, P, key->big_l, level) && !getenv("HG_ROT_NO_FINISH");
     for (int g0 = 0; g0 < count; g0 += gmax) {
         int G = count - g0 < gmax ? count - g0 : gmax;
         if (G > 8) G = 8;
@@ -1318,7 +1322,8 @@ static int automorph_batch_impl(hg_ctx* ctx, const hg_key* key, int count, const
             continue;
         }
         for (int g = 0; g < G; ++g)
-            if (out0s[g0 + g] == c0s[g0 + g] || out0s[g0 + g] == c1s[g0 + g] || out1s[g0 + g] == c1s[g0 + g])
+            if (out0s[g0 + g] == c0s[g0 + g] || out0s[g0 + g] == c1s[g0 + g] || out1s[g0 + g] == c1s[g0 + g] ||
+                out1s[g0 + g] == c0s[g0 + g])
                 return hg_fail(HG_EINVAL, "hg_ct_automorph_batch: outputs must not alias inputs");
         Scratch res(st), buf(st);
         HG_CUDA_TRY(res.alloc((size_t)3 * G * P * N * 4));   // x residues [G][P][N], products [G][2][P][N]
@@ -1335,6 +1340,25 @@ static int automorph_batch_impl(hg_ctx* ctx, const hg_key* key, int count, const
         uint32_t* t = res.u32() + (size_t)G * P * N;
         rc = hg_intt_fused(ctx, 1, t, res.u32(), key->d_kb, key->d_ka, nullptr, P, st, G);
         if (rc) return rc < 0 ? hg_fail(HG_EINVAL, "batched key product not available") : rc;
+        if (fin_ok) {   // (phi(c0) [+ c0], [c1]) added in the CRT epilogue, written to the outputs
+            for (int h = 0; h < G; h += 4) {
+                const int gh = G - h < 4 ? G - h : 4;
+                uint32_t* ad = buf.u32() + (size_t)2 * h * W * N;
+                if ((rc = hg_ew_automorph_addends(ctx, ad, c0s + g0 + h, c1s + g0 + h, gh, level, k, acc, st)))
+                    return rc;
+                CrtFinish fin;
+                for (int q = 0; q < 2 * gh; ++q) fin.add[q] = ad + (size_t)q * W * N;
+                OutSet outs{};
+                for (int g = 0; g < gh; ++g) {
+                    outs.out[2 * g] = out0s[g0 + h + g];
+                    outs.out[2 * g + 1] = out1s[g0 + h + g];
+                }
+                if ((rc = launch_crt(ctx, t + (size_t)2 * h * P * N, 2 * gh, P, key->big_l, level, outs, st,
+                                     &fin, key->prescaled)))
+                    return rc;
+            }
+            continue;
+        }
         for (int h = 0; h < G; h += 4) {   // CRT: up to 8 outputs (4 items) per launch
             const int gh = G - h < 4 ? G - h : 4;
             OutSet outs{};

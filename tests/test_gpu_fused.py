@@ -130,6 +130,27 @@ def test_rotate_add_many_identical_to_rotate_then_add(log_n, count, step):
     assert np.max(np.abs(got - (vals + np.roll(vals, step)))) < 1e-4
 
 
+@pytest.mark.parametrize("log_n,count,step", [(12, 6, 3), (17, 5, 32)])
+def test_rotate_many_identical_to_one_by_one(log_n, count, step):
+    """hg_ct_automorph_batch (phi(c0) handed to the key switch's CRT epilogue as an addend)
+    writes exactly what hg_ct_automorph writes for each rotation."""
+    import torch
+
+    import paper_1902_04303_b200 as hg
+
+    params = hg.CkksParams(log_n=log_n, log_l=1700, log_p=45, log_p_small=30)
+    sk, pk, evk, rot = hg.keygen(params, 10, device_rng=True)
+    eng = hg.HeEngine(params, evk, rot)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(4)
+    vals = np.random.default_rng(3).uniform(-1, 1, params.slot_count)
+    cts = [hg.mod_down(hg.encrypt_values(vals, params.log_p, pk, params, gen), 1500) for _ in range(count)]
+    many = eng.rotate_many(cts, step)
+    for c, m in zip(cts, many):
+        one = eng.rotate(c, step)
+        assert torch.equal(one.c0.words, m.c0.words) and torch.equal(one.c1.words, m.c1.words)
+
+
 def test_batched_products_rescan_with_addends():
     """Four prepared products in one group whose relinearisation lands in the CRT's ambiguous
     carry band (d2 = 1 and evk coefficients at 2^(L-1) - 1, 2^(L-1), ...): the exact rescan of
