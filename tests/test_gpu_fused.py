@@ -151,6 +151,31 @@ def test_rotate_many_identical_to_one_by_one(log_n, count, step):
         assert torch.equal(one.c0.words, m.c0.words) and torch.equal(one.c1.words, m.c1.words)
 
 
+def test_rotate_left_each_identical_to_one_by_one():
+    """HeEngine.rotate_left_each (the ccp_to_cp rotations batched per amount bit) equals
+    rotate_left one by one, bit for bit, with the same recorded rotation amounts."""
+    import torch
+
+    import paper_1902_04303_b200 as hg
+
+    params = hg.CkksParams(log_n=12, log_l=1700, log_p=45, log_p_small=30)
+    sk, pk, evk, rot = hg.keygen(params, 12, device_rng=True)
+    eng = hg.HeEngine(params, evk, rot)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(8)
+    vals = np.random.default_rng(5).uniform(-1, 1, params.slot_count)
+    amounts = [8, 16, 24, 0, 1000, 7, 2047]
+    cts = [hg.mod_down(hg.encrypt_values(vals, params.log_p, pk, params, gen), 1450) for _ in amounts]
+    with hg.track_ops() as each_ops:
+        each = eng.rotate_left_each(cts, amounts)
+    with hg.track_ops() as one_ops:
+        ones = [eng.rotate_left(c, r) for c, r in zip(cts, amounts)]
+    assert each_ops.rotation_amounts == one_ops.rotation_amounts
+    assert each_ops.keyswitches == one_ops.keyswitches
+    for one, e in zip(ones, each):
+        assert torch.equal(one.c0.words, e.c0.words) and torch.equal(one.c1.words, e.c1.words)
+
+
 def test_batched_products_rescan_with_addends():
     """Four prepared products in one group whose relinearisation lands in the CRT's ambiguous
     carry band (d2 = 1 and evk coefficients at 2^(L-1) - 1, 2^(L-1), ...): the exact rescan of
