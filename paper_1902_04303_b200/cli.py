@@ -23,6 +23,7 @@ from __future__ import annotations
 
 import argparse
 import sys
+import contextvars
 import threading
 import time
 from concurrent.futures import ThreadPoolExecutor
@@ -121,7 +122,10 @@ class _BatchReader:
         with self.lock:
             for nb in range(b, min(b + 1 + self.depth, len(self.names))):
                 if nb not in self.pending:
-                    self.pending[nb] = self.pool.submit(self._read, nb)
+                    # the io audit is a ContextVar: run the worker's read in the caller's
+                    # context so every prefetched batch file lands in the audit log
+                    ctx = contextvars.copy_context()
+                    self.pending[nb] = self.pool.submit(ctx.run, self._read, nb)
             fut = self.pending.pop(b)
         return fut.result()
 

@@ -74,6 +74,7 @@ extern "C" int hg_ctx_create(int log_n, int device, hg_ctx** out) {
     ctx->log_n = log_n;
     ctx->N = 1 << log_n;
     ctx->device = device;
+    HG_CUDA_TRY(cudaDeviceGetAttribute(&ctx->nsm, cudaDevAttrMultiProcessorCount, device));
     // primes p = k * 2^18 + 1 < 2^30, descending
     for (uint64_t k = ((1ull << 30) - 2) >> HG_PRIME_SHIFT; k >= 1 && ctx->primes.size() < HG_MAX_PRIMES; --k) {
         uint64_t p = (k << HG_PRIME_SHIFT) + 1;

@@ -302,11 +302,9 @@ int hg_crt_mma_launch(hg_ctx* ctx, const CrtTable* tab, const uint32_t* res, int
     rs_words += (4 - rs_words) & 31;
     const size_t smem = (size_t)kCoefs * 4 * rs_words * 4 + (size_t)kWarps * 8 * kColBlock * 4 * 8 +
                         kCoefs * 4 + 4 * kCoefs * 8 + (size_t)4 * (P32 / 32) * 32 * 8;
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<uint64_t> attr_set{0};
+    if (hg_first_on_device(attr_set, ctx->device))
         cudaFuncSetAttribute(crt_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        attr = true;
-    }
     Outs4 o{};
     for (int k = 0; k < nouts; ++k) o.out[k] = outs_in[k];
     const int N = ctx->N;

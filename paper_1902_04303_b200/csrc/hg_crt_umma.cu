@@ -942,8 +942,9 @@ bool hg_crt_umma_pipe_ok(const CrtTable* tab, int N, int shift, int out_bits, in
 int hg_crt_umma_pipe_launch(hg_ctx* ctx, const CrtTable* tab, const uint32_t* res, int nouts, int P,
                             int shift, int out_bits, int tb0, uint32_t* const* outs_in,
                             cudaStream_t st, const CrtFinish* finish, bool prescaled) {
-    static int nsm = 0;
-    if (!nsm) {
+    static std::atomic<uint64_t> attr_set{0};
+    const int nsm = ctx->nsm;
+    if (hg_first_on_device(attr_set, ctx->device)) {
         HG_CUDA_TRY(cudaFuncSetAttribute(crt_umma_pipe_kernel<false, false>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pipe_smem<false>()));
         HG_CUDA_TRY(cudaFuncSetAttribute(crt_umma_pipe_kernel<false, true>,
@@ -952,7 +953,6 @@ int hg_crt_umma_pipe_launch(hg_ctx* ctx, const CrtTable* tab, const uint32_t* re
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pipe_smem<true>()));
         HG_CUDA_TRY(cudaFuncSetAttribute(crt_umma_pipe_kernel<true, true>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pipe_smem<true>()));
-        HG_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device));
     }
     UOuts o{};
     for (int k = 0; k < nouts; ++k) o.out[k] = outs_in[k];
@@ -1018,12 +1018,11 @@ size_t hg_crt_umma_smem(int P32) { return (size_t)kRows * 4 * P32 + 2 * (size_t)
 int hg_crt_umma_launch(hg_ctx* ctx, const CrtTable* tab, const uint32_t* res, int nouts, int P,
                        int shift, int out_bits, int tb0, uint32_t* const* outs_in, cudaStream_t st) {
     const size_t smem = hg_crt_umma_smem(tab->P32);
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<uint64_t> attr_set{0};
+    if (hg_first_on_device(attr_set, ctx->device)) {
         // 227 KB per block includes the kernel's static shared variables
         HG_CUDA_TRY(cudaFuncSetAttribute(crt_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          220 * 1024));
-        attr = true;
     }
     UOuts o{};
     for (int k = 0; k < nouts; ++k) o.out[k] = outs_in[k];

@@ -80,6 +80,7 @@ struct hg_ctx {
     int log_n = 0;
     int N = 0;
     int device = 0;
+    int nsm = 0;          // SM count of `device`
     int nprimes = 0;
     std::vector<uint32_t> primes;       // descending
     std::vector<double> prefix_bits;    // prefix_bits[P] = sum_{j<P} log2 p_j
@@ -157,6 +158,20 @@ int hg_fail(int code, const std::string& msg);
     } while (0)
 
 static inline int words_for_bits(int bits) { return (bits + 31) >> 5; }
+
+// Function attributes (dynamic shared memory limits) are per device: a process driving two
+// GPUs must set them once on each.  True the first time `dev` is seen for this flag set.
+static inline bool hg_first_on_device(std::atomic<uint64_t>& seen, int dev) {
+    const uint64_t bit = 1ull << (dev & 63);
+    return !(seen.fetch_or(bit) & bit);
+}
+// Clamp a group-size override from the environment (unset, 0 or negative -> default).
+static inline int hg_env_group(const char* name, int dflt, int lo, int hi) {
+    const char* s = getenv(name);
+    int v = s ? atoi(s) : dflt;
+    if (v <= 0) v = dflt;
+    return v < lo ? lo : (v > hi ? hi : v);
+}
 
 // ---- host-side helpers (hg_context.cu) ----------------------------------------------
 // 2-D uint32 tensor map (row pitch = inner * 4 bytes) for cp.async.bulk.tensor boxes

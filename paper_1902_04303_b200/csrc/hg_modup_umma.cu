@@ -347,15 +347,14 @@ int hg_modup_umma_launch(hg_ctx* ctx, const uint32_t* const* words, const int* b
     if (ctx->N < kRows || maxw > kWMax || maxw < 1 || nops > 4) return 0;
     int rc = hg_modup_build_umma(ctx);
     if (rc) return -rc;
-    static int nsm = 0;
-    if (!nsm) {
+    static std::atomic<uint64_t> attr_set{0};
+    const int nsm = ctx->nsm;
+    if (hg_first_on_device(attr_set, ctx->device)) {
         if (cudaFuncSetAttribute(modup_umma_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem) != cudaSuccess ||
             cudaFuncSetAttribute(modup_umma_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem) != cudaSuccess ||
             cudaFuncSetAttribute(modup_umma_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem) != cudaSuccess ||
             cudaFuncSetAttribute(modup_umma_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem) != cudaSuccess)
             return -hg_fail(HG_ECUDA, "modup_umma smem attribute");
-        if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device) != cudaSuccess)
-            return -hg_fail(HG_ECUDA, "device attribute");
     }
     MOps o{};
     for (int k = 0; k < nops; ++k) {

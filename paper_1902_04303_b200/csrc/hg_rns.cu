@@ -398,11 +398,10 @@ int launch_modup(hg_ctx* ctx, const OperandSet& ops, int nops, int P, uint32_t* 
             return hg_fail(HG_EINVAL, "operand width out of range");
     }
     size_t smem = (size_t)maxw * kModupThreads * 4;
-    static bool attr_set = false;
-    if (!attr_set) {
+    static std::atomic<uint64_t> attr_set{0};
+    if (hg_first_on_device(attr_set, ctx->device)) {
         cudaFuncSetAttribute(modup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         cudaFuncSetAttribute(crt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        attr_set = true;
     }
     const int N = ctx->N;
     int threads = N < kModupThreads ? N : kModupThreads;
@@ -950,7 +949,7 @@ extern "C" int hg_ct_mult_prepared_batch(hg_ctx* ctx, const hg_key* evk, int cou
     const int W = words_for_bits(level);
     const int Pk = evk->P;
     const bool fused = fuse_pointwise() && crt_finish_ok(ctx, Pk, evk->big_l, level);
-    static const int gmax = getenv("HG_BATCH_G") ? atoi(getenv("HG_BATCH_G")) : 4;
+    static const int gmax = hg_env_group("HG_BATCH_G", 4, 1, 4);
     int rc;
     for (int g0 = 0; g0 < count;) {
         int G = count - g0 < gmax ? count - g0 : gmax;
@@ -1297,7 +1296,7 @@ static int automorph_batch_impl(hg_ctx* ctx, const hg_key* key, int count, const
     if ((kk & 1) == 0) return hg_fail(HG_EINVAL, "automorphism exponent must be odd");
     const int64_t kinv = kk == 1 ? 0 : inverse_mod_2n(kk, n2);
     int rc;
-    static const int gmax = getenv("HG_ROT_G") ? atoi(getenv("HG_ROT_G")) : 4;   // 8: no gain measured
+    static const int gmax = hg_env_group("HG_ROT_G", 4, 1, 8);   // 8: no gain measured
     const bool fin_ok = crt_finish_ok(ctx, P, key->big_l, level) && !getenv("HG_ROT_NO_FINISH");
     for (int g0 = 0; g0 < count; g0 += gmax) {
         int G = count - g0 < gmax ? count - g0 : gmax;

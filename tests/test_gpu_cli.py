@@ -37,6 +37,12 @@ def test_compute_results_byte_identical_to_reference(computed):
         assert ours[key] == ref[key], key
     assert ours["secret_key_accessed"] is False
     assert not any(p.endswith("sk.bin") for p in ours["file_access_audit"])
+
+    # the audited file set (relative to the phase directories) is the reference's: every
+    # prefetched SNP batch file read on the reader thread is logged too
+    def rel(paths):
+        return sorted("/".join(p.split("/")[-2:]) for p in paths)
+    assert rel(ours["file_access_audit"]) == rel(ref["file_access_audit"])
     for entry in ref["results"]["batches"]:
         for name in entry.values():
             assert filecmp.cmp(computed / "computed" / name, os.path.join(GOLD, "computed", name),
