@@ -186,15 +186,19 @@ def run_ours(args, world, rank, local):
         encrypt_gwas_inputs,
     )
 
+    from paper_1902_04303_b200.parallel import compute_setup_sharded, shard_batches
+
     params = hg.CkksParams(log_n=args.log_n, log_l=args.log_l, log_p=45, log_p_small=30)
     t_wall0 = time.time()
-    sk, pk, evk, rot = hg.keygen(params, 1000 + rank, device_rng=True)
+    # every rank holds the same keys and setup inputs: the column-split setup combines their
+    # ciphertexts (parallel.compute_setup_sharded)
+    sk, pk, evk, rot = hg.keygen(params, 1000, device_rng=True)
     engine = hg.HeEngine(params, evk, rot)
     ctx = _lib.get_context(params.log_n)
     gen = torch.Generator(device="cuda")
-    gen.manual_seed(7 + rank)
+    gen.manual_seed(7)
     tau = 2 * params.slot_count // 256
-    ds = synth_gwas_dataset(N_SAMPLES, N_COV, tau, seed=rank)
+    ds = synth_gwas_dataset(N_SAMPLES, N_COV, tau, seed=0)
     config = GwasConfig(n=N_SAMPLES, d=N_COV, k=K_PAPER).resolve(params)
     inputs = encrypt_gwas_inputs(ds, GwasConfig(n=N_SAMPLES, d=N_COV, k=tau), params, pk, gen,
                                  lazy_batches=True)
@@ -223,27 +227,33 @@ def run_ours(args, world, rank, local):
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e_setup = torch.cuda.Event(enable_timing=True)
     nb = math.ceil(K_PAPER / tau)
+    my_batches = len(shard_batches(nb, rank, world))   # round-robin SNP batches of this rank
+    barrier(world)
+    torch.cuda.synchronize()
     s.record()
-    beta, p_prev, inter, m_dup = compute_setup(engine, inputs)
+    if world > 1:   # column-split setup + NCCL all-gathers of z' partials and M_dup
+        beta, p_prev, inter, m_dup = compute_setup_sharded(engine, inputs, rank, world, gather_m=False)
+    else:
+        beta, p_prev, inter, m_dup = compute_setup(engine, inputs)
     e_setup.record()
     job_keep = []
     marks = []
     if hbatch is not None:
-        for b in SnpBatchStream([hbatch] * nb, params):
+        for b in SnpBatchStream([hbatch] * my_batches, params):
             read_back(compute_batch(engine, inputs, inter, m_dup, b), job_keep)
             if os.environ.get("HG_BENCH_DEBUG"):
                 marks.append(torch.cuda.Event(enable_timing=True))
                 marks[-1].record()
     e.record()
     torch.cuda.synchronize()
-    t_setup = s.elapsed_time(e_setup) / 1e3
+    t_setup = max_over_ranks(s.elapsed_time(e_setup) / 1e3, world)
     if marks:
         prev, per = e_setup, []
         for m in marks:
             per.append(round(prev.elapsed_time(m), 1))
             prev = m
         print(f"[bench] whole-job batch ms: {per}", file=sys.stderr, flush=True)
-    t_whole = s.elapsed_time(e) / 1e3 if hbatch is not None else None
+    t_whole = max_over_ranks(s.elapsed_time(e) / 1e3, world) if hbatch is not None else None
     del job_keep
 
     def step_resident():
@@ -430,75 +440,167 @@ def ncu_traffic(dom: str):
 
 
 # ---------------------------------------------------------------------------------------------
-def cpu_mult_sample(log_n: int, level: int, big_l: int, log_p: int, seed: int = 0):
-    """Time one HeEngine.mult at (N, level) with the CPU oracle port (gmp-backed exact
-    products) -- the reference algorithm restated, single thread."""
+# CPU baseline: the reference evaluator's time is >= 99.7% big Kronecker products (hegwas
+# ring.py:46-58, the multiply at :55), so one batch step's CPU cost is the sum over its
+# products, each timed at its exact operand widths through oracle/ (the reference algorithm
+# restated, libgmp's mpz_mul for the big multiply).
+
+def batch_step_products(big_l: int = 1700, log_p: int = 45, log_p_small: int = 30) -> dict:
+    """{(a_bits, b_bits): count} of the big products in one config-3 batch step at P17, from the
+    reference's own op sequence (gwas.py:197-229, 325-331; ckks.py:166-194, 256-279):
+    a ct-mult at level l = 4 tensor products l x l + 2 key-switch products l x (l + L); a rotation
+    or conjugation = 2 key-switch products; a plaintext mult = 2 products l x l (the mask is held
+    mod 2^l).  Levels: M at 1700-150, S' = M S at 1505, w 545, z' 185 (SURVEY §8 level table)."""
+    lm = big_l - 150
+    s1 = lm - log_p                                  # S' = M S_i
+    lw, lz = 545, 185
+    wz = min(lw, lz) - log_p                         # w z' (aligned at z')
+    num = wz - log_p                                 # dup(w z') S'
+    wm = lw - log_p_small                            # w (.) 0.5-mask
+    ws = wm - log_p                                  # dup(w_m) S'
+    den = ws - log_p                                 # ws S', ws conj(S')
+    prods: dict = {}
+
+    def add(a, b, k):
+        prods[(a, b)] = prods.get((a, b), 0) + k
+
+    def mult(level, k=1):
+        add(level, level, 4 * k)
+        add(level, level + big_l, 2 * k)
+
+    def rot(level, k=1):
+        add(level, level + big_l, 2 * k)
+
+    mult(lm, 245)                                    # orthogonalize_snps: 245 ct-mults
+    mult(lz)                                         # w z'
+    rot(wz, 8)                                       # duplicate(w z', 256)
+    mult(wz)                                         # num terms
+    rot(num, 8 + 9)                                  # col_sum: 8 ladder steps + rotate_left(255)
+    add(lw, lw, 2)                                   # mult_plain(w, range-value mask)
+    rot(wm, 8)                                       # duplicate(w_m)
+    mult(wm)                                         # ws
+    mult(ws, 2)                                      # wss, wsc
+    rot(s1)                                          # conjugate(S')
+    rot(den, 2 * 17)                                 # two col_sums
+    return prods
+
+
+def cpu_product_sample(log_n: int, a_bits: int, b_bits: int, seed: int = 0) -> float:
+    """Seconds for one exact negacyclic product of uniform a_bits x b_bits operands through
+    oracle/ (ring.py:46-58 restated; gmp multiply), single thread."""
     import random
 
-    from oracle import ckks_oracle as C
+    from oracle import ring_oracle as R
 
     n = 1 << log_n
     rng = random.Random(seed)
-    a0, a1, b0, b1 = ([rng.getrandbits(level) for _ in range(n)] for _ in range(4))
-    kb = [rng.getrandbits(2 * big_l) for _ in range(n)]
-    ka = [rng.getrandbits(2 * big_l) for _ in range(n)]
+    a = [rng.getrandbits(a_bits) for _ in range(n)]
+    b = [rng.getrandbits(b_bits) for _ in range(n)]
     t = time.perf_counter()
-    C.engine_mult(a0, a1, b0, b1, level, kb, ka, big_l, log_p, n)
+    R.negacyclic_mul(a, b, n, a_bits, b_bits)
     return time.perf_counter() - t
 
 
-def cpu_snp_rate(t_mult: float, tau: int, n_mults: int = N_SAMPLES + 5) -> float:
-    """SNP/s of the CPU port on one batch: op-count extrapolation from the dominant op
-    (the batch's ct-mults at level ~1550; rotations and the rest are left out, so this is
-    an upper bound on CPU throughput)."""
-    return tau / (n_mults * t_mult)
+def cpu_step_seconds(prods: dict, times: dict) -> float:
+    """CPU-seconds of one batch step: every product class at its timed cost; a class without its
+    own sample takes the nearest timed class's cost scaled by operand width (a + b)."""
+    total = 0.0
+    for (a, b), k in prods.items():
+        if (a, b) in times:
+            t = times[(a, b)]
+        else:
+            ref = min(times, key=lambda c: abs(c[0] + c[1] - a - b))
+            t = times[ref] * (a + b) / (ref[0] + ref[1])
+        total += k * t
+    return total
+
+
+def cpu_baseline_sample(log_n: int, big_l: int) -> dict:
+    """Rank 0, N=1: the batch step's four costliest product classes timed once each on one core
+    (~15-20 s at P17), the step's CPU time summed over its exact product list."""
+    prods = batch_step_products(big_l)
+    ranked = sorted(prods, key=lambda c: -prods[c] * (c[0] + c[1]))[:4]
+    times = {c: cpu_product_sample(log_n, c[0], c[1], i) for i, c in enumerate(ranked)}
+    sec = cpu_step_seconds(prods, times)
+    return {"step_cpu_s": sec, "classes_timed": {f"{a}x{b}": round(t, 2) for (a, b), t in times.items()},
+            "products": sum(prods.values())}
 
 
 def run_reference(args, world, rank):
     """--impl reference: the reference algorithm (CPU oracle port; the reference is pure
-    Python and cannot travel) on all host cores, bounded samples of the same step."""
+    Python and cannot travel) on all host cores.  Each timed step runs `cores` concurrent exact
+    products of the batch step's product classes (cycled, so every class is sampled); the step's
+    CPU time is the exact product list x the per-class median; value = SNP/s with all cores."""
     if rank != 0:
         return None
     from concurrent.futures import ProcessPoolExecutor
 
     cores = os.cpu_count() or 1
-    level = args.log_l - 150
     tau = 2 * (1 << (args.log_n - 1)) // 256
-    times = []
-    total_w = args.warmup + args.steps
+    prods = batch_step_products(args.log_l)
+    classes = sorted(prods, key=lambda c: -prods[c] * (c[0] + c[1]))
+    samples: dict = {c: [] for c in classes}
+    walls = []
     with ProcessPoolExecutor(max_workers=cores) as ex:
-        # each step: one batch-sized sample = `cores` concurrent mults at level 1550
-        for i in range(total_w):
-            # warm-up steps load gmp and fork the workers on a small ring (N=2^13, same level);
-            # timed steps run the full-size sample
-            log_n = args.log_n if i >= args.warmup else min(args.log_n, 13)
+        for i in range(args.warmup + args.steps):
+            timed = i >= args.warmup
+            # warm-up steps load gmp and fork the workers on a small ring; timed steps sample
+            # the full-size classes
+            log_n = args.log_n if timed else min(args.log_n, 12)
+            k0 = (i - args.warmup) * cores if timed else 0
+            picks = [classes[(k0 + c) % len(classes)] for c in range(cores)]
             t = time.perf_counter()
-            list(ex.map(cpu_mult_sample, [log_n] * cores, [level] * cores,
-                        [args.log_l] * cores, [45] * cores, range(cores)))
+            res = list(ex.map(cpu_product_sample, [log_n] * cores, [c[0] for c in picks],
+                              [c[1] for c in picks], range(cores)))
             dt = time.perf_counter() - t
-            if i >= args.warmup:
-                times.append(dt)
-    per_mult = statistics.median(times) / cores  # throughput-equivalent seconds per mult
-    value = cpu_snp_rate(per_mult, tau)
+            if timed:
+                walls.append(dt)
+                for c, r in zip(picks, res):
+                    samples[c].append(r)
+    times = {c: statistics.median(v) for c, v in samples.items() if v}
+    step_cpu = cpu_step_seconds(prods, times)
+    value = tau * cores / step_cpu
     line = {
         "impl": "reference", "metric": "encrypted semi-parallel GWAS SNPs/s", "value": value,
         "unit": "SNP/s", "higher_is_better": True, "n_gpus": 0, "steps": args.steps,
         "warmup": args.warmup, "dtype": "u32", "data": "synthetic",
-        "ms_per_step": round(1e3 * statistics.median(times), 1),
+        "ms_per_step": round(1e3 * statistics.median(walls), 1),
         "config": {"workload": f"config3 per-batch step, P17 (N=2^{args.log_n}, log_l={args.log_l}), "
                                f"{tau} SNPs/batch, n=245", "scaling": "n/a"},
         "cpu_baseline": {"value": value, "unit": "SNP/s", "cores": cores, "kind": "port",
-                         "sample": f"{cores} concurrent HeEngine.mult at level {level} per step via "
-                                   "oracle/ (gmp Kronecker products); SNP/s = tau / (250 x t_mult), "
-                                   "rotations excluded (upper bound)"},
+                         "sample": f"each step: {cores} concurrent exact negacyclic products (oracle/, gmp) "
+                                   f"cycling over the batch step's {len(classes)} product classes; step CPU "
+                                   f"time = its {sum(prods.values())} products (245 ct-mults at 1550 + the "
+                                   f"statistics' 5 ct-mults, 1 pt-mult, 67 rotations, 1 conjugation) x the "
+                                   f"per-class medians = {step_cpu:.0f} core-s",
+                         "classes_s": {f"{a}x{b}": round(t, 2) for (a, b), t in times.items()}},
         "e2e": {"value": value, "unit": "SNP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     return line
 
 
 # ---------------------------------------------------------------------------------------------
+def relaunch_under_torchrun(args) -> int:
+    """`bench.py --gpus N` (N > 1) started as a plain process: re-run it under torchrun with one
+    rank per GPU (127.0.0.1 rendezvous, a free port); returns torchrun's exit code."""
+    import socket
+
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is None and args.gpus > 1:
+        sys.exit(relaunch_under_torchrun(args))
+    if env_world is not None and int(env_world) != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={env_world}; launch one rank per GPU")
     world, rank, local = dist_setup() if args.impl == "ours" else (
         int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0)
     if args.impl == "reference":
@@ -514,7 +616,7 @@ def main():
     value = tau * steps * world / r["t_steps"]
     ms_step = 1e3 * r["t_steps"] / steps
     nb = math.ceil(K_PAPER / tau)
-    whole = K_PAPER / (r["t_setup"] + nb * r["t_steps"] / steps)
+    whole = K_PAPER / (r["t_setup"] + math.ceil(nb / world) * r["t_steps"] / steps)
     whole_e2e = K_PAPER / r["t_whole"] if r.get("t_whole") else None
     ks = r["kstats"]
     # roofline of the dominant kernel class (integer pipe: CRT reconstruction MACs)
@@ -549,10 +651,12 @@ def main():
     roofline["i8_peak_tops"] = round(i8_tops, 1)
     cpu = None
     if not args.no_cpu_baseline and world == 1:   # the contract: rank 0 at N=1 only
-        t_cpu = cpu_mult_sample(params.log_n, params.log_l - 150, params.log_l, params.log_p)
-        cpu = {"value": round(cpu_snp_rate(t_cpu, tau), 6), "unit": "SNP/s", "cores": 1, "kind": "port",
-               "sample": f"one HeEngine.mult at N=2^{params.log_n}, level {params.log_l - 150} via oracle/ "
-                         f"({t_cpu:.1f}s, gmp Kronecker); SNP/s = {tau} / (250 x t_mult), rotations excluded"}
+        cb = cpu_baseline_sample(params.log_n, params.log_l)
+        cpu = {"value": round(tau / cb["step_cpu_s"], 6), "unit": "SNP/s", "cores": 1, "kind": "port",
+               "sample": f"the batch step's {cb['products']} exact products (ring.py:55 Kronecker multiplies: "
+                         f"250 ct-mults, 1 pt-mult, 67 rotations, 1 conjugation) costed from one timed product "
+                         f"per dominant class via oracle/ (gmp) at N=2^{params.log_n}: {cb['classes_timed']} s; "
+                         f"{cb['step_cpu_s']:.0f} core-s per step"}
     line = {
         "metric": "encrypted semi-parallel GWAS SNPs/s", "value": round(value, 3), "unit": "SNP/s",
         "n_gpus": world, "steps": steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 2),

@@ -50,3 +50,25 @@ class Golden:
 
 def words_hash(arr) -> str:
     return hashlib.sha256(np.ascontiguousarray(np.asarray(arr, dtype=np.uint32)).tobytes()).hexdigest()
+
+
+def random_words(seed, bits: int, n: int) -> np.ndarray:
+    """Uniform residues mod 2^bits as limb-major [W][N] uint32 words from a seeded numpy
+    generator (seed: an int or a tuple of ints) -- the inputs of the scale goldens
+    (tools/make_scale_golden.py), rebuilt identically by the GPU tests."""
+    seq = list(seed) if isinstance(seed, (tuple, list)) else [seed]
+    rng = np.random.default_rng(seq)
+    w = (bits + 31) // 32
+    arr = rng.integers(0, 1 << 32, size=(w, n), dtype=np.uint64).astype(np.uint32)
+    top = bits - 32 * (w - 1)
+    if top < 32:
+        arr[w - 1] &= np.uint32((1 << top) - 1)
+    return arr
+
+
+def ints_to_words(coeffs, bits: int) -> np.ndarray:
+    """Coefficients mod 2^bits -> limb-major [W][N] uint32 words (inverse of words_to_ints)."""
+    w = (bits + 31) // 32
+    mask = (1 << bits) - 1
+    buf = b"".join((c & mask).to_bytes(4 * w, "little") for c in coeffs)
+    return np.ascontiguousarray(np.frombuffer(buf, dtype="<u4").reshape(len(coeffs), w).T)

@@ -158,3 +158,40 @@ def test_cleartext_oracles_restate_reference_definitions():
     assert np.allclose(a[0], b[0]) and np.allclose(a[1], b[1])
     rep_acc = accuracy([0.0, 1.0, 2.0], [0.0, 1.02, 2.2])
     assert rep_acc["above"] == {"0.1": 1, "0.01": 2, "0.005": 2}
+
+
+@pytest.mark.parametrize("case", ["n13_l240", "n13_l1440"])
+def test_oracle_against_reference_hashes_at_n8192(case):
+    """The oracle at N=2^13 against the reference-run hashes of tests/golden/scale_hashes.json
+    (tools/make_scale_golden.py): rescale and mult_plain + rescale of the seeded inputs."""
+    import hashlib
+    import json
+    import os
+
+    from paper_1902_04303_b200.encoding import encode_coefficients, mask_vector
+    from paper_1902_04303_b200.params import CkksParams
+    from tests.golden_io import HERE, random_words, words_to_ints
+
+    g = json.load(open(os.path.join(HERE, "golden", "scale_hashes.json")))[case]
+    params = CkksParams(log_n=g["log_n"], log_l=g["log_l"], log_p=g["log_p"],
+                        log_p_small=g["log_p_small"], h=g["h"])
+    n, lv, seed = params.n, g["level"], g["seed"]
+    a0 = words_to_ints(random_words((seed, lv, 0, 0), lv, n))
+    a1 = words_to_ints(random_words((seed, lv, 0, 1), lv, n))
+
+    def sha(*polys_bits):
+        from tests.golden_io import ints_to_words
+
+        h = hashlib.sha256()
+        for coeffs, bits in polys_bits:
+            h.update(ints_to_words(coeffs, bits).tobytes())
+        return h.hexdigest()
+
+    r0, r1 = C.rescale(a0, a1, 30, lv)
+    assert sha((r0, lv - 30), (r1, lv - 30)) == g["outputs"]["rescale30_a"]["sha256"]
+    mask = [c % (1 << params.log_l) for c in
+            encode_coefficients(mask_vector(("range", 0, 256), params.slot_count), params.log_p_small, params)]
+    m0, m1 = C.mult_plain(a0, a1, mask, params.log_l, lv, n)
+    p0, p1 = C.rescale(m0, m1, params.log_p_small, lv)
+    out_bits = lv - params.log_p_small
+    assert sha((p0, out_bits), (p1, out_bits)) == g["outputs"]["mult_plain_range_a"]["sha256"]
