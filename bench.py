@@ -236,6 +236,14 @@ def run_ours(args, world, rank, local):
     else:
         beta, p_prev, inter, m_dup = compute_setup(engine, inputs)
     e_setup.record()
+    if os.environ.get("HG_BENCH_DEBUG"):
+        from paper_1902_04303_b200.ckks import KEY_CACHE
+
+        free, total = torch.cuda.mem_get_info()
+        print(f"[bench] after setup: free {free / 1e9:.1f} GB, torch reserved "
+              f"{torch.cuda.memory_reserved() / 1e9:.1f} / allocated {torch.cuda.memory_allocated() / 1e9:.1f} GB, "
+              f"library pool {ctx.pool_bytes() / 1e9:.1f} / in use {ctx.pool_bytes(True) / 1e9:.1f} GB, "
+              f"key cache {KEY_CACHE.bytes / 1e9:.1f} GB", file=sys.stderr, flush=True)
     job_keep = []
     marks = []
     if hbatch is not None:

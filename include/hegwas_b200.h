@@ -181,6 +181,32 @@ int hg_ct_rotate_add_batch(hg_ctx* ctx, const hg_key* key, int count, const uint
                            const uint32_t* const* c1s, int level, int64_t k, uint32_t* const* out0s,
                            uint32_t* const* out1s, void* stream);
 
+/* ---- plaintext products and batched ciphertext ops (arrays of device pointers in host
+ * arrays; outputs must not alias inputs) --------------------------------------------------
+ * HeEngine.mult_plain = mult_plain then rescale by the plaintext's scale (hegwas ckks.py:147-163,
+ * 197-224, 315-317) with the rescale fused into the CRT window.
+ * hg_ct_mult_plain_many: ONE ciphertext (c0, c1 at `level`) times `count` plaintexts ms[i]
+ *   (replicate's masks, matrix.py:79-96; ccp_to_cp's column ranges, :196-209) -> (out0s[i], out1s[i]).
+ * hg_ct_mult_plain_batch: `count` ciphertexts times ONE plaintext m. */
+int hg_ct_mult_plain_many(hg_ctx* ctx, const uint32_t* c0, const uint32_t* c1, int level, int count,
+                          const hg_operand* ms, int rescale_bits, uint32_t* const* out0s,
+                          uint32_t* const* out1s, void* stream);
+int hg_ct_mult_plain_batch(hg_ctx* ctx, int count, const uint32_t* const* c0s, const uint32_t* const* c1s,
+                           int level, hg_operand m, int rescale_bits, uint32_t* const* out0s,
+                           uint32_t* const* out1s, void* stream);
+/* rescale (ckks.py:197-224) of `count` ciphertexts at `level` by `bits`: outputs at level - bits. */
+int hg_ct_rescale_batch(hg_ctx* ctx, int count, const uint32_t* const* c0s, const uint32_t* const* c1s,
+                        int level, int bits, uint32_t* const* out0s, uint32_t* const* out1s, void* stream);
+/* add / sub (ckks.py:108-125) of `count` aligned ciphertext pairs (subtract != 0: a - b). */
+int hg_ct_add_batch(hg_ctx* ctx, int count, const uint32_t* const* a0s, const uint32_t* const* a1s,
+                    const uint32_t* const* b0s, const uint32_t* const* b1s, int bits, int subtract,
+                    uint32_t* const* out0s, uint32_t* const* out1s, void* stream);
+/* HeEngine.mult_const (ckks.py:351-356): times the constant plaintext k (|k| < 2^32, the single
+ * coefficient of encode_constant, encoding.py:82-90), then rescale by `shift`, in one pass. */
+int hg_ct_mult_const_rescale_batch(hg_ctx* ctx, int count, const uint32_t* const* c0s,
+                                   const uint32_t* const* c1s, int level, int64_t k, int shift,
+                                   uint32_t* const* out0s, uint32_t* const* out1s, void* stream);
+
 /* ---- microbenchmarks / measurement ------------------------------------------------ */
 /* Batched forward+inverse negacyclic NTT over `count` length-N rows of residues
  * (prime i % num_primes for row i); data is [count][N] uint32 on device.            */

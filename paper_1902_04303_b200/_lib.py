@@ -78,6 +78,16 @@ SIGNATURES = {
     "hg_ctprep_destroy": (_i, [_vp]),
     "hg_ctprep_device_bytes": (ctypes.c_size_t, [_vp]),
     "hg_ct_mult_prepared": (_i, [_vp, _vp, _vp, _vp, _vp, _i, _i, _vp, _vp, _vp]),
+    "hg_ct_mult_plain_many": (_i, [_vp, _vp, _vp, _i, _i, ctypes.POINTER(Operand), _i, ctypes.POINTER(_vp),
+                                   ctypes.POINTER(_vp), _vp]),
+    "hg_ct_mult_plain_batch": (_i, [_vp, _i, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _i, Operand, _i,
+                                    ctypes.POINTER(_vp), ctypes.POINTER(_vp), _vp]),
+    "hg_ct_rescale_batch": (_i, [_vp, _i, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _i, _i,
+                                 ctypes.POINTER(_vp), ctypes.POINTER(_vp), _vp]),
+    "hg_ct_add_batch": (_i, [_vp, _i, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp),
+                             ctypes.POINTER(_vp), _i, _i, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _vp]),
+    "hg_ct_mult_const_rescale_batch": (_i, [_vp, _i, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _i, _i64, _i,
+                                            ctypes.POINTER(_vp), ctypes.POINTER(_vp), _vp]),
     "hg_ntt_forward": (_i, [_vp, _vp, _i, _i, _vp]),
     "hg_ntt_inverse": (_i, [_vp, _vp, _i, _i, _vp]),
     "hg_bench_modmul": (_i, [_vp, _i, _vp, ctypes.POINTER(ctypes.c_double), _vp]),
@@ -142,6 +152,24 @@ def check_alloc(call, evict=None):
             evict()
             torch.cuda.synchronize()
             rc = call()
+    check(rc)
+
+
+def _is_oom(rc: int) -> bool:
+    if rc == HG_ENOMEM:
+        return True
+    return rc == HG_ECUDA and b"out of memory" in load_library().hg_last_error()
+
+
+def call(fn, *args):
+    """check(fn(*args)) for a product entry point whose scratch comes from the library's
+    stream-ordered pool: on out-of-memory the caches torch and the library hold are handed
+    back and the call is repeated once (the entry points never write their inputs, so a
+    repeat recomputes every output from unchanged operands)."""
+    rc = fn(*args)
+    if rc != HG_OK and _is_oom(rc):
+        release_device_memory()
+        rc = fn(*args)
     check(rc)
 
 

@@ -534,7 +534,7 @@ int hg_get_crt(hg_ctx* ctx, int P, const CrtTable** out) {
         std::vector<uint32_t> Mp((size_t)W * t.P32p, 0u);
         std::copy(M.begin(), M.begin() + (size_t)W * P, Mp.begin());
         std::copy(negQ.begin(), negQ.end(), Mp.begin() + (size_t)W * P);
-        hg_crt_build_conv(t, P + 1, t.P32p, conv, Mp);
+        hg_crt_build_pack4(t, P + 1, t.P32p, conv, Mp);
         HG_CUDA_TRY(cudaMalloc(&t.d_Bpipe, conv.size()));
         if (int rc = hg_upload(ctx, t.d_Bpipe, conv.data(), conv.size())) return rc;
     }

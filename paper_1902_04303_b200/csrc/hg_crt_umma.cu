@@ -345,18 +345,19 @@ __global__ void __launch_bounds__(2 * kRows) crt_umma_kernel(
 constexpr int kConvWarp0 = 3, kEpiWarp0 = 11, kAddWarp = 19;
 template <bool FUSED> struct PipeCfg {
     static constexpr int kWarps = FUSED ? 20 : 19;
-    static constexpr int kRA = 4;
+    static constexpr int kRR = FUSED ? 2 : 3;
+    static constexpr int kRA = FUSED ? 3 : 4;
     static constexpr int kRB = FUSED ? 2 : 3;
 };
-constexpr int kRR = 3;
-constexpr int kJobCols = 32;                     // output words per job (N = 256)
+constexpr int kJobCols = 64;                     // output words per job (4 columns each: N = 256)
 constexpr int kResStage = 32 * kRows * 4;        // 16 KB: 32 prime rows of 128 residues
 constexpr int kAStage = kRows * kKChunk;         // 16 KB
-constexpr int kBStagePipe = kJobCols * 8 * kKChunk;   // 32 KB
-constexpr int kAddStage = kJobCols * kRows * 4;  // 16 KB: 32 addend words of 128 coefficients
+constexpr int kBStagePipe = kJobCols * 4 * kKChunk;   // 32 KB
+constexpr int kBGran = 4096;                     // B image bytes per (K chunk, 8-word group)
+constexpr int kAddStage = kJobCols * kRows * 4;  // 32 KB: 64 addend words of 128 coefficients
 template <bool FUSED>
 constexpr size_t pipe_smem() {
-    return (size_t)kRR * kResStage + (size_t)PipeCfg<FUSED>::kRA * kAStage + (size_t)PipeCfg<FUSED>::kRB * kBStagePipe +
+    return (size_t)PipeCfg<FUSED>::kRR * kResStage + (size_t)PipeCfg<FUSED>::kRA * kAStage + (size_t)PipeCfg<FUSED>::kRB * kBStagePipe +
            (FUSED ? 2 * (size_t)kAddStage : 0);
 }
 
@@ -512,6 +513,7 @@ __global__ void __launch_bounds__(PipeCfg<FUSED>::kWarps * 32, 1) crt_umma_pipe_
     const uint32_t* __restrict__ Mtab, int W, const uint32_t* __restrict__ negQ,
     const uint32_t* __restrict__ cinv, const uint32_t* __restrict__ cinv_sh,
     const double* __restrict__ invp, int shift, int out_bits, int tb0, UOuts outs, CrtFinish fin) {
+    constexpr int kRR = PipeCfg<FUSED>::kRR;
     constexpr int kRA = PipeCfg<FUSED>::kRA;
     constexpr int kRB = PipeCfg<FUSED>::kRB;
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -583,11 +585,12 @@ __global__ void __launch_bounds__(PipeCfg<FUSED>::kWarps * 32, 1) crt_umma_pipe_
     }();
     const int ntiles = nouts * tpo;
     const int nkc = P32p / 32;
-    // columns of job block h: [tb0 + 32h, min(T, tb0 + 32h + 32)), padded to an even count
+    // columns of job block h: [tb0 + jc h, min(T, tb0 + jc (h + 1))), padded to a multiple of
+    // 4 words (UMMA N = 4 x words must be a multiple of 16)
     auto job_cols = [&](int h) {
         const int c0 = tb0 + h * jc;
         const int c = h == jpt - 1 ? T - c0 : (T - c0 < jc ? T - c0 : jc);
-        return (c + 1) & ~1;
+        return (c + 3) & ~3;
     };
 
     if (warp == 0) {
@@ -619,13 +622,13 @@ __global__ void __launch_bounds__(PipeCfg<FUSED>::kWarps * 32, 1) crt_umma_pipe_
             int it = 0;
             for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
               for (int h = 0; h < jpt; ++h) {
-                const uint32_t bytes = (uint32_t)((job_cols(h) + 7) >> 3) * 8192u;
-                const uint8_t* bsrc = Bpipe + (size_t)((tb0 >> 3) + h * (jc / 8)) * 8192;
+                const uint32_t bytes = (uint32_t)((job_cols(h) + 7) >> 3) * kBGran;
+                const uint8_t* bsrc = Bpipe + (size_t)((tb0 >> 3) + h * (jc / 8)) * kBGran;
                 for (int kc = 0; kc < nkc; ++kc, ++it) {
                     const int s = it % kRB;
                     PWAIT(0, smem_u32(&bar_b_empty[s]), ((it / kRB) & 1) ^ 1);
                     mbar_expect_tx(smem_u32(&bar_b_full[s]), bytes);
-                    bulk_g2s(smem_u32(s_b + s * kBStagePipe), bsrc + (size_t)kc * (W >> 3) * 8192, bytes,
+                    bulk_g2s(smem_u32(s_b + s * kBStagePipe), bsrc + (size_t)kc * (W >> 3) * kBGran, bytes,
                              smem_u32(&bar_b_full[s]));
                 }
             }
@@ -637,7 +640,7 @@ __global__ void __launch_bounds__(PipeCfg<FUSED>::kWarps * 32, 1) crt_umma_pipe_
             int ia = 0, ib = 0, ij = 0;
             for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
               for (int h = 0; h < jpt; ++h, ++ij) {
-                const uint32_t Nn = 8u * (uint32_t)job_cols(h);
+                const uint32_t Nn = 4u * (uint32_t)job_cols(h);
                 const uint32_t idesc = (2u << 4) | ((Nn >> 3) << 17) | ((uint32_t)(kRows >> 4) << 24);
                 const int tb = ij & 1;
                 PWAIT(0, smem_u32(&bar_tm_empty[tb]), ((ij >> 1) & 1) ^ 1);
@@ -819,7 +822,7 @@ __global__ void __launch_bounds__(PipeCfg<FUSED>::kWarps * 32, 1) crt_umma_pipe_
 #ifdef HG_CRT_PROF
             const long long t_loop = clock64();
 #endif
-            for (int tl = 0; tl < ncols; tl += 4) {
+            for (int tl = 0; tl < ncols; tl += 8) {
                 uint32_t e[32];
 #ifdef HG_CRT_PROF
                 const long long t_ld = clock64();
@@ -832,32 +835,32 @@ __global__ void __launch_bounds__(PipeCfg<FUSED>::kWarps * 32, 1) crt_umma_pipe_
                                "=r"(e[18]), "=r"(e[19]), "=r"(e[20]), "=r"(e[21]), "=r"(e[22]), "=r"(e[23]),
                                "=r"(e[24]), "=r"(e[25]), "=r"(e[26]), "=r"(e[27]), "=r"(e[28]), "=r"(e[29]),
                                "=r"(e[30]), "=r"(e[31])
-                             : "r"(lane_addr + (uint32_t)(tl * 8)));
+                             : "r"(lane_addr + (uint32_t)(tl * 4)));
                 asm volatile("tcgen05.wait::ld.sync.aligned;\n");
 #ifdef HG_CRT_PROF
                 prof[4] += (unsigned long long)(clock64() - t_ld);
 #endif
-                // the four columns' digit sums first (independent of the carry), then the short
-                // carry chain, then emission: column value = lo + hi * 2^32 (digit 7 is zero);
-                // columns past T (padding of the last batch) only disturb the dead carry
-                uint64_t lo[4], hi[4];
+                // the eight words' digit sums first (independent of the carry), then the short
+                // carry chain, then emission: word value = D0 + D1 2^8 + D2 2^16 + D3 2^24 < 2^51
+                // (the packed layout already carries the previous word's high digits);
+                // columns past T (padding of the last job) only disturb the dead carry
+                uint64_t val[8];
 #pragma unroll
-                for (int hh = 0; hh < 4; ++hh) {
-                    const uint32_t* E = e + 8 * hh;
-                    lo[hh] = madw(E[3], 1u << 24, madw(E[2], 1u << 16, madw(E[1], 256u, (uint64_t)E[0])));
-                    hi[hh] = madw(E[6], 1u << 16, madw(E[5], 256u, (uint64_t)E[4]));
+                for (int hh = 0; hh < 8; ++hh) {
+                    const uint32_t* E = e + 4 * hh;
+                    val[hh] = madw(E[3], 1u << 24, madw(E[2], 1u << 16, madw(E[1], 256u, (uint64_t)E[0])));
                 }
-                uint32_t wv[4];
+                uint32_t wv[8];
 #pragma unroll
-                for (int hh = 0; hh < 4; ++hh) {
-                    const uint64_t x = lo[hh] + carry + (c0 + tl + hh == round_col ? round_bit : 0u);
+                for (int hh = 0; hh < 8; ++hh) {
+                    const uint64_t x = val[hh] + carry + (c0 + tl + hh == round_col ? round_bit : 0u);
                     wv[hh] = (uint32_t)x;
-                    carry = (x >> 32) + hi[hh];
+                    carry = x >> 32;
                 }
                 // emission, predicated rather than branched (every condition is warp-uniform):
                 // window word u = t - sw - (sbit != 0) is valid for 0 <= u < out_w (so t < T)
 #pragma unroll
-                for (int hh = 0; hh < 4; ++hh) {
+                for (int hh = 0; hh < 8; ++hh) {
                     const int t = c0 + tl + hh;
                     const uint32_t word = wv[hh];
                     if (t < sw) {   // below the window: the truncated-column ambiguity flag
@@ -1010,6 +1013,41 @@ int hg_crt_build_conv(const CrtTable& t, int P, int P32, std::vector<uint8_t>& o
                                 out[off] = val;
                             }
             }
+    return HG_OK;
+}
+
+// B in the PACKED digit layout of the pipelined kernel: 4 TMEM columns per output word.  Byte
+// q of y_j times byte r of word t of M_j lands at bit 32t + 8(q + r): digit q + r of word t when
+// q + r < 4, else digit q + r - 4 of word t + 1.  So column (word T, digit s) gathers
+//     B[(j, q), (T, s)] = byte (s - q) of M[j][T]          (s >= q)
+//                         byte (s - q + 4) of M[j][T - 1]  (s <  q)
+// -- every (K row, column) entry is live (the 8-column layout above is half zeros), and the
+// epilogue folds 4 digits (< 2^27 each) per word instead of 7.  Image: [K chunk kc][8-word group
+// tg][row group rg (8 N-rows = words 2rg, 2rg+1 x digits 0-3)][16-byte K chunk c][row][16 bytes];
+// 4096 bytes per (kc, tg).
+int hg_crt_build_pack4(const CrtTable& t, int P, int P32, std::vector<uint8_t>& out,
+                       const std::vector<uint32_t>& M) {
+    const int W = t.W, nkc = P32 / 32, ntg = W / 8;
+    out.assign((size_t)nkc * ntg * 4096, 0);
+    for (int kc = 0; kc < nkc; ++kc)
+        for (int tg = 0; tg < ntg; ++tg)
+            for (int rg = 0; rg < 4; ++rg)
+                for (int c = 0; c < 8; ++c)
+                    for (int rr = 0; rr < 8; ++rr) {
+                        const int T = tg * 8 + rg * 2 + (rr >> 2), sd = rr & 3;
+                        for (int jj = 0; jj < 4; ++jj)
+                            for (int q = 0; q < 4; ++q) {
+                                const int j = kc * 32 + c * 4 + jj;
+                                const int word = sd >= q ? T : T - 1;
+                                const int byte = sd >= q ? sd - q : sd - q + 4;
+                                uint8_t val = 0;
+                                if (j < P && word >= 0)
+                                    val = (uint8_t)(M[(size_t)j * W + word] >> (8 * byte));
+                                const size_t off = ((size_t)kc * ntg + tg) * 4096 +
+                                                   ((size_t)(rg * 8 + c) * 8 + rr) * 16 + jj * 4 + q;
+                                out[off] = val;
+                            }
+                    }
     return HG_OK;
 }
 

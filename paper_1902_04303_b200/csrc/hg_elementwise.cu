@@ -259,6 +259,122 @@ int64_t inv_mod_pow2(int64_t k, int64_t n2) {
     return (int64_t)(inv & (uint64_t)(n2 - 1));
 }
 
+// ---- batched ciphertext-level kernels: grid.y walks up to kPolys polys per launch -------------
+constexpr int kPolys = 16;
+struct PolyPtrs {
+    const uint32_t* a[kPolys];
+    const uint32_t* b[kPolys];
+    uint32_t* out[kPolys];
+};
+template <typename T>
+__device__ __forceinline__ T sel16(const T (&v)[kPolys], int k) {
+    T r = v[0];
+#pragma unroll
+    for (int q = 1; q < kPolys; ++q) r = k == q ? v[q] : r;   // select, not a dynamic index
+    return r;
+}
+
+// divide_round over a batch of polys                 rescale  ckks.py:197-224
+__device__ __forceinline__ void divide_round_one(uint32_t* __restrict__ out, int out_bits,
+                                                 const uint32_t* __restrict__ a, int in_bits,
+                                                 int shift, int N, int i) {
+    const int Wi = (in_bits + 31) >> 5, Wo = (out_bits + 31) >> 5;
+    const int sw = shift >> 5, sb = shift & 31;
+    const int rc = shift > 0 ? (shift - 1) >> 5 : -1;
+    const uint32_t rbit = shift > 0 ? 1u << ((shift - 1) & 31) : 0u;
+    uint32_t carry = 0, prev = 0;
+    const int T = sw + Wo + 1;
+    for (int t = 0; t < T; ++t) {
+        uint32_t x = 0;
+        if (t < Wi) {
+            x = a[(size_t)t * N + i];
+            if (t == Wi - 1) x &= mask_for(in_bits);
+        }
+        const uint64_t s = (uint64_t)x + carry + (t == rc ? rbit : 0u);
+        const uint32_t word = (uint32_t)s;
+        carry = (uint32_t)(s >> 32);
+        const int u = sb ? t - sw - 1 : t - sw;
+        if (u >= 0 && u < Wo) {
+            uint32_t o = sb ? __funnelshift_r(prev, word, sb) : word;
+            if (u == Wo - 1) o &= mask_for(out_bits);
+            out[(size_t)u * N + i] = o;
+        }
+        prev = word;
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) rescale_batch_kernel(PolyPtrs p, int out_bits, int in_bits,
+                                                                 int shift, int N) {
+    const int i = blockIdx.x * kThreads + threadIdx.x;
+    if (i >= N) return;
+    divide_round_one(sel16(p.out, blockIdx.y), out_bits, sel16(p.a, blockIdx.y), in_bits, shift, N, i);
+}
+
+// a +/- b over a batch of poly pairs                  add / sub  ckks.py:108-125
+template <bool SUB>
+__global__ void __launch_bounds__(kThreads) add_batch_kernel(PolyPtrs p, int W, int bits, int N) {
+    const int i = blockIdx.x * kThreads + threadIdx.x;
+    if (i >= N) return;
+    const uint32_t* a = sel16(p.a, blockIdx.y);
+    const uint32_t* b = sel16(p.b, blockIdx.y);
+    uint32_t* out = sel16(p.out, blockIdx.y);
+    uint32_t carry = SUB ? 1u : 0u;
+    for (int w = 0; w < W; ++w) {
+        uint32_t y = b[(size_t)w * N + i];
+        if (SUB) y = ~y;
+        const uint64_t s = (uint64_t)a[(size_t)w * N + i] + y + carry;
+        uint32_t r = (uint32_t)s;
+        carry = (uint32_t)(s >> 32);
+        if (w == W - 1) r &= mask_for(bits);
+        out[(size_t)w * N + i] = r;
+    }
+}
+
+// HeEngine.mult_const (an encode_constant plaintext: a single coefficient k, ckks.py:351-356
+// with encoding.py:82-90) followed by its rescale, in one pass: the words of (c * k mod 2^level)
+// -- |k| < 2^32, negatives as the two's-complement negation of c * |k| -- stream straight into
+// divide_round by `shift`
+__global__ void __launch_bounds__(kThreads) mult_const_rescale_kernel(PolyPtrs p, int level, int shift,
+                                                                      uint32_t kabs, int negative, int N) {
+    const int i = blockIdx.x * kThreads + threadIdx.x;
+    if (i >= N) return;
+    const uint32_t* a = sel16(p.a, blockIdx.y);
+    uint32_t* out = sel16(p.out, blockIdx.y);
+    const int out_bits = level - shift;
+    const int Wi = (level + 31) >> 5, Wo = (out_bits + 31) >> 5;
+    const int sw = shift >> 5, sb = shift & 31;
+    const int rc = shift > 0 ? (shift - 1) >> 5 : -1;
+    const uint32_t rbit = shift > 0 ? 1u << ((shift - 1) & 31) : 0u;
+    uint64_t pc = 0;                      // product column carry (< 2^32)
+    uint32_t nc = negative ? 1u : 0u;     // negation carry: -x = ~x + 1
+    uint32_t carry = 0, prev = 0;
+    const int T = sw + Wo + 1;
+    for (int t = 0; t < T; ++t) {
+        uint32_t x = 0;
+        if (t < Wi) {
+            const uint64_t pr = (uint64_t)a[(size_t)t * N + i] * kabs + pc;
+            pc = pr >> 32;
+            x = (uint32_t)pr;
+            if (negative) {
+                const uint64_t ns = (uint64_t)(~x) + nc;
+                x = (uint32_t)ns;
+                nc = (uint32_t)(ns >> 32);
+            }
+            if (t == Wi - 1) x &= mask_for(level);
+        }
+        const uint64_t s = (uint64_t)x + carry + (t == rc ? rbit : 0u);
+        const uint32_t word = (uint32_t)s;
+        carry = (uint32_t)(s >> 32);
+        const int u = sb ? t - sw - 1 : t - sw;
+        if (u >= 0 && u < Wo) {
+            uint32_t o = sb ? __funnelshift_r(prev, word, sb) : word;
+            if (u == Wo - 1) o &= mask_for(out_bits);
+            out[(size_t)u * N + i] = o;
+        }
+        prev = word;
+    }
+}
+
 }  // namespace
 
 // ---- internal entry points (used by the fused drivers in hg_rns.cu) --------------------------
@@ -415,4 +531,85 @@ extern "C" int hg_poly_automorphism(hg_ctx* ctx, uint32_t* out, const uint32_t* 
                                     int64_t k, void* stream) {
     HG_CHECK_ARGS(ctx && out && a && bits >= 1 && out != a, "hg_poly_automorphism: bad arguments");
     return hg_ew_automorphism(ctx, out, a, bits, k, (cudaStream_t)stream);
+}
+
+// ---- batched ciphertext-level entry points (arrays of device pointers, host arrays) ---------------
+// Each takes `count` ciphertexts as (c0, c1) pointer arrays and writes (out0, out1); polys go
+// kPolys per launch.  Outputs may not alias inputs.
+namespace {
+template <typename Launch>
+int over_polys(int count, const uint32_t* const* a0, const uint32_t* const* a1, const uint32_t* const* b0,
+               const uint32_t* const* b1, uint32_t* const* o0, uint32_t* const* o1, Launch launch) {
+    const int polys = 2 * count;
+    for (int k0 = 0; k0 < polys; k0 += kPolys) {
+        PolyPtrs p{};
+        const int c = polys - k0 < kPolys ? polys - k0 : kPolys;
+        for (int k = 0; k < c; ++k) {
+            const int q = (k0 + k) >> 1, h = (k0 + k) & 1;
+            p.a[k] = h ? a1[q] : a0[q];
+            p.b[k] = b0 ? (h ? b1[q] : b0[q]) : nullptr;
+            p.out[k] = h ? o1[q] : o0[q];
+            if (!p.a[k] || !p.out[k] || (b0 && !p.b[k])) return hg_fail(HG_EINVAL, "null ciphertext pointer");
+        }
+        if (int rc = launch(p, c)) return rc;
+    }
+    return HG_OK;
+}
+}  // namespace
+
+/* rescale (ckks.py:197-224) of `count` ciphertexts at `level` by `bits`. */
+extern "C" int hg_ct_rescale_batch(hg_ctx* ctx, int count, const uint32_t* const* c0s,
+                                   const uint32_t* const* c1s, int level, int bits,
+                                   uint32_t* const* out0s, uint32_t* const* out1s, void* stream) {
+    HG_CHECK_ARGS(ctx && count >= 0 && (!count || (c0s && c1s && out0s && out1s)) && bits >= 1 &&
+                  bits < level, "hg_ct_rescale_batch: bad arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    HgTimed tm(ctx, st, HG_K_ELEMENTWISE, (double)ctx->N * 2 * count);
+    return over_polys(count, c0s, c1s, nullptr, nullptr, out0s, out1s, [&](const PolyPtrs& p, int c) {
+        dim3 grid = grid_for(ctx->N);
+        grid.y = c;
+        rescale_batch_kernel<<<grid, kThreads, 0, st>>>(p, level - bits, level, bits, ctx->N);
+        HG_LAUNCH_CHECK(ctx);
+        return HG_OK;
+    });
+}
+
+/* add / sub (ckks.py:108-125) of `count` aligned ciphertext pairs at `bits`. */
+extern "C" int hg_ct_add_batch(hg_ctx* ctx, int count, const uint32_t* const* a0s, const uint32_t* const* a1s,
+                               const uint32_t* const* b0s, const uint32_t* const* b1s, int bits, int subtract,
+                               uint32_t* const* out0s, uint32_t* const* out1s, void* stream) {
+    HG_CHECK_ARGS(ctx && count >= 0 && (!count || (a0s && a1s && b0s && b1s && out0s && out1s)) && bits >= 1,
+                  "hg_ct_add_batch: bad arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int W = words_for_bits(bits);
+    HgTimed tm(ctx, st, HG_K_ELEMENTWISE, (double)ctx->N * 2 * count);
+    return over_polys(count, a0s, a1s, b0s, b1s, out0s, out1s, [&](const PolyPtrs& p, int c) {
+        dim3 grid = grid_for(ctx->N);
+        grid.y = c;
+        if (subtract) add_batch_kernel<true><<<grid, kThreads, 0, st>>>(p, W, bits, ctx->N);
+        else add_batch_kernel<false><<<grid, kThreads, 0, st>>>(p, W, bits, ctx->N);
+        HG_LAUNCH_CHECK(ctx);
+        return HG_OK;
+    });
+}
+
+/* HeEngine.mult_const: product with the integer constant k (|k| < 2^32), then rescale by
+   `shift` (the constant's scale), for `count` ciphertexts at `level`; one pass per poly. */
+extern "C" int hg_ct_mult_const_rescale_batch(hg_ctx* ctx, int count, const uint32_t* const* c0s,
+                                              const uint32_t* const* c1s, int level, int64_t k,
+                                              int shift, uint32_t* const* out0s, uint32_t* const* out1s,
+                                              void* stream) {
+    HG_CHECK_ARGS(ctx && count >= 0 && (!count || (c0s && c1s && out0s && out1s)) && shift >= 1 &&
+                  shift < level && k > -(1ll << 32) && k < (1ll << 32),
+                  "hg_ct_mult_const_rescale_batch: bad arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    const uint32_t kabs = (uint32_t)(k < 0 ? -k : k);
+    HgTimed tm(ctx, st, HG_K_ELEMENTWISE, (double)ctx->N * 2 * count);
+    return over_polys(count, c0s, c1s, nullptr, nullptr, out0s, out1s, [&](const PolyPtrs& p, int c) {
+        dim3 grid = grid_for(ctx->N);
+        grid.y = c;
+        mult_const_rescale_kernel<<<grid, kThreads, 0, st>>>(p, level, shift, kabs, k < 0 ? 1 : 0, ctx->N);
+        HG_LAUNCH_CHECK(ctx);
+        return HG_OK;
+    });
 }

@@ -191,6 +191,8 @@ int hg_crt_mma_launch(hg_ctx* ctx, const CrtTable* tab, const uint32_t* res, int
                       int shift, int out_bits, int tb0, uint32_t* const* outs, cudaStream_t st);
 int hg_crt_build_conv(const CrtTable& t, int P, int P32, std::vector<uint8_t>& out,
                       const std::vector<uint32_t>& M);
+int hg_crt_build_pack4(const CrtTable& t, int P, int P32, std::vector<uint8_t>& out,
+                       const std::vector<uint32_t>& M);
 int hg_crt_umma_launch(hg_ctx* ctx, const CrtTable* tab, const uint32_t* res, int nouts, int P,
                        int shift, int out_bits, int tb0, uint32_t* const* outs, cudaStream_t st);
 size_t hg_crt_umma_smem(int P32);

@@ -331,13 +331,15 @@ __global__ void __launch_bounds__(256, HG_HI_MINB) ntt_hi8_kernel(uint32_t* __re
 //   PRE 1 (key switch):  out rows (x*kb, x*ka)           in0 = x [0,4p), in1 = kb, in2 = ka [0,p)
 //   PRE 2 (tensor):      out rows (a0b0, a0b1+a1b0, a1b1) in0..in3 = a0, a1, b0, b1 [0,4p)
 //   PRE 3 (product):     out row  a*b                    in0, in1 [0,4p)
+//   PRE 5 (shared factor): out row x*b                   in0 = x [0,4p), in1 = b [0,p)
 // Inputs and outputs are [rows][P][N]; a block reads its chunk of every input row before its
 // last round writes, so the outputs may alias the inputs chunk-for-chunk (in-place use).
 template <int PRE>
-struct PreRows { static constexpr int value = PRE == 1 ? 2 : (PRE == 2 ? 3 : 1); };
+struct PreRows { static constexpr int value = PRE == 1 ? 2 : (PRE == 2 ? 3 : 1); };   // PRE 3, 5: 1
 
 // blockIdx.y selects one of a batch of independent products sharing in1..in3 (PRE 1: several
-// key switches with one key): in0 advances by bstride_in words, out by bstride_out
+// key switches with one key, or one ciphertext times several plaintexts; PRE 5: several
+// polynomials times one plaintext): in0 advances by bstride_in words, out by bstride_out
 template <int K2, int PRE>
 __global__ void __launch_bounds__(256, HG_FUSED_MINB) intt_lo8_fused_kernel(
     uint32_t* out, const uint32_t* in0, const uint32_t* in1, const uint32_t* in2,
@@ -363,7 +365,7 @@ __global__ void __launch_bounds__(256, HG_FUSED_MINB) intt_lo8_fused_kernel(
         uint32_t u0[8], u1[8], u2[8], u3[8];
         load8<0>(u0, in0 + roff, base);
         load8<0>(u1, in1 + roff, base);
-        if (PRE != 3) load8<0>(u2, in2 + roff, base);
+        if (PRE != 3 && PRE != 5) load8<0>(u2, in2 + roff, base);
         if (PRE == 2) load8<0>(u3, in3 + roff, base);
 #pragma unroll
         for (int m = 0; m < 8; ++m) {
@@ -379,6 +381,8 @@ __global__ void __launch_bounds__(256, HG_FUSED_MINB) intt_lo8_fused_kernel(
                 const uint32_t d1 = mont_mul(a, b1, p, pi.pinv_neg) + mont_mul(a1, b0, p, pi.pinv_neg);
                 x[RB > 1 ? 1 : 0][m] = min(d1, d1 - p2);
                 x[RB - 1][m] = mont_mul(a1, b1, p, pi.pinv_neg);
+            } else if (PRE == 5) {
+                x[0][m] = mont_mul(a, u1[m], p, pi.pinv_neg);
             } else {
                 x[0][m] = mont_mul(a, min(u1[m], u1[m] - p2), p, pi.pinv_neg);
             }
@@ -525,13 +529,14 @@ int hg_intt_fused(hg_ctx* ctx, int pre, uint32_t* out, const uint32_t* i0, const
     const int k1 = log_n <= 11 ? 0 : (log_n <= 14 ? 3 : 6);
     const int k2 = log_n - k1;
     const int rb = pre == 1 ? 2 : (pre == 2 ? 3 : 1);
-    if (batch < 1 || (batch > 1 && pre != 1) || batch > 65535) return -1;
+    if (batch < 1 || (batch > 1 && pre != 1 && pre != 5) || batch > 65535) return -1;
     HgTimed tm(ctx, st, HG_K_NTT, (double)batch * rb * P * (N / 2) * log_n);
     // batch > 1 (key switch only): input g's x rows at i0 + g P N, its two outputs at out + g 2 P N
     const dim3 g(N >> k2, batch, P);
     const size_t bsi = (size_t)P * N, bso = (size_t)rb * P * N;
     if (pre == 1) launch_fused_lo8<1>(k2, g, st, out, i0, i1, i2, i3, log_n, P, ctx->d_pinfo, ctx->d_tw_inv, bsi, bso);
     else if (pre == 2) launch_fused_lo8<2>(k2, g, st, out, i0, i1, i2, i3, log_n, P, ctx->d_pinfo, ctx->d_tw_inv);
+    else if (pre == 5) launch_fused_lo8<5>(k2, g, st, out, i0, i1, i2, i3, log_n, P, ctx->d_pinfo, ctx->d_tw_inv, bsi, bso);
     else launch_fused_lo8<3>(k2, g, st, out, i0, i1, i2, i3, log_n, P, ctx->d_pinfo, ctx->d_tw_inv);
     HG_LAUNCH_CHECK(ctx);
     if (k1) return ntt_pass<false>(ctx, true, k1, k2, out, batch * rb, P, 0, ctx->d_tw_inv, st);

@@ -1385,3 +1385,128 @@ static int automorph_batch_impl(hg_ctx* ctx, const hg_key* key, int count, const
     }
     return HG_OK;
 }
+
+// ---- plaintext products with the rescale fused into the CRT window -------------------------------
+// HeEngine.mult_plain = mult_plain then rescale by the plaintext scale (ckks.py:147-163, 197-224,
+// 315-317): out = divide_round(c * m mod 2^level, bits) = bits [bits, level) of (c*m + 2^(bits-1))
+// (reducing mod 2^level first does not change those bits).  The ciphertext polys are read as
+// centered level-bit values, the plaintext through its caller-chosen (compact) operand.
+namespace {
+int plain_primes(hg_ctx* ctx, int level, const hg_operand* ms, int count) {
+    int mb = 1;
+    for (int i = 0; i < count; ++i) mb = std::max(mb, magnitude_bits(ms[i]));
+    return primes_for_product(ctx, (double)(level - 1) + mb, level);
+}
+bool plain_args_ok(int level, int rescale_bits) { return level >= 1 && rescale_bits >= 1 && rescale_bits < level; }
+}  // namespace
+
+// One ciphertext times `count` plaintexts (replicate's one-hot masks, ccp_to_cp's column
+// ranges: matrix.py:79-96, 196-209): c's ModUp and forward NTT run once for all of them; each
+// group of up to 4 plaintexts is one ModUp, one NTT, one fused pointwise/inverse pass and one CRT.
+extern "C" int hg_ct_mult_plain_many(hg_ctx* ctx, const uint32_t* c0, const uint32_t* c1, int level,
+                                     int count, const hg_operand* ms, int rescale_bits,
+                                     uint32_t* const* out0s, uint32_t* const* out1s, void* stream) {
+    if (!ctx || !c0 || !c1 || count < 0 || (count && (!ms || !out0s || !out1s)) ||
+        !plain_args_ok(level, rescale_bits))
+        return hg_fail(HG_EINVAL, "hg_ct_mult_plain_many: bad arguments");
+    if (count == 0) return HG_OK;
+    for (int i = 0; i < count; ++i)
+        if (!ms[i].words || ms[i].bits < 1 || !out0s[i] || !out1s[i])
+            return hg_fail(HG_EINVAL, "hg_ct_mult_plain_many: bad plaintext or output");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int N = ctx->N;
+    const int P = plain_primes(ctx, level, ms, count);
+    if (P < 0) return hg_fail(HG_ERANGE, "plaintext product exceeds the NTT prime basis");
+    if (!fuse_pointwise()) return hg_fail(HG_EINVAL, "hg_ct_mult_plain_many needs the fused inverse NTT");
+    const size_t plane = (size_t)P * N;
+    const int G = count < 4 ? count : 4;
+    Scratch cres(st), mres(st), prod(st);
+    HG_CUDA_TRY(cres.alloc(2 * plane * 4));
+    HG_CUDA_TRY(mres.alloc((size_t)G * plane * 4));
+    HG_CUDA_TRY(prod.alloc((size_t)2 * G * plane * 4));
+    OperandSet cops{};
+    cops.words[0] = c0; cops.bits[0] = level; cops.is_signed[0] = 1;
+    cops.words[1] = c1; cops.bits[1] = level; cops.is_signed[1] = 1;
+    int rc = launch_modup(ctx, cops, 2, P, cres.u32(), 0, st);
+    if (!rc) rc = hg_ntt_launch(ctx, cres.u32(), 2 * P, P, 0, true, st);
+    if (rc) return rc;
+    // the shared factor enters the Montgomery products reduced to [0, p)
+    reduce_rows_kernel<<<pw_grid(N, P), 256, 0, st>>>(cres.u32(), N, ctx->d_pinfo);
+    ctx->launches++;
+    reduce_rows_kernel<<<pw_grid(N, P), 256, 0, st>>>(cres.u32() + plane, N, ctx->d_pinfo);
+    HG_LAUNCH_CHECK(ctx);
+    for (int g0 = 0; g0 < count; g0 += G) {
+        const int gh = count - g0 < G ? count - g0 : G;
+        OperandSet mops{};
+        for (int g = 0; g < gh; ++g) {
+            mops.words[g] = ms[g0 + g].words; mops.bits[g] = ms[g0 + g].bits;
+            mops.is_signed[g] = ms[g0 + g].signed_rep;
+        }
+        if ((rc = launch_modup(ctx, mops, gh, P, mres.u32(), 0, st))) return rc;
+        if ((rc = hg_ntt_launch(ctx, mres.u32(), gh * P, P, 0, true, st))) return rc;
+        // out rows per plaintext: (m c0, m c1), the key-switch form with c as the shared "key"
+        rc = hg_intt_fused(ctx, 1, prod.u32(), mres.u32(), cres.u32(), cres.u32() + plane, nullptr, P, st, gh);
+        if (rc) return rc < 0 ? hg_fail(HG_EINVAL, "fused plaintext product not available") : rc;
+        OutSet outs{};
+        for (int g = 0; g < gh; ++g) {
+            outs.out[2 * g] = out0s[g0 + g];
+            outs.out[2 * g + 1] = out1s[g0 + g];
+        }
+        if ((rc = launch_crt(ctx, prod.u32(), 2 * gh, P, rescale_bits, level - rescale_bits, outs, st)))
+            return rc;
+    }
+    return HG_OK;
+}
+
+// `count` ciphertexts times one plaintext: m's ModUp and NTT run once; up to 2 ciphertexts (4
+// polys) per ModUp launch, 4 (8 outputs) per fused pass and CRT.
+extern "C" int hg_ct_mult_plain_batch(hg_ctx* ctx, int count, const uint32_t* const* c0s,
+                                      const uint32_t* const* c1s, int level, hg_operand m,
+                                      int rescale_bits, uint32_t* const* out0s,
+                                      uint32_t* const* out1s, void* stream) {
+    if (!ctx || count < 0 || (count && (!c0s || !c1s || !out0s || !out1s)) || !m.words || m.bits < 1 ||
+        !plain_args_ok(level, rescale_bits))
+        return hg_fail(HG_EINVAL, "hg_ct_mult_plain_batch: bad arguments");
+    if (count == 0) return HG_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int N = ctx->N;
+    const int P = plain_primes(ctx, level, &m, 1);
+    if (P < 0) return hg_fail(HG_ERANGE, "plaintext product exceeds the NTT prime basis");
+    if (!fuse_pointwise()) return hg_fail(HG_EINVAL, "hg_ct_mult_plain_batch needs the fused inverse NTT");
+    const size_t plane = (size_t)P * N;
+    const int G = count < 4 ? count : 4;
+    Scratch mres(st), cres(st);
+    HG_CUDA_TRY(mres.alloc(plane * 4));
+    HG_CUDA_TRY(cres.alloc((size_t)2 * G * plane * 4));
+    OperandSet mops{};
+    mops.words[0] = m.words; mops.bits[0] = m.bits; mops.is_signed[0] = m.signed_rep;
+    int rc = launch_modup(ctx, mops, 1, P, mres.u32(), 0, st);
+    if (!rc) rc = hg_ntt_launch(ctx, mres.u32(), P, P, 0, true, st);
+    if (rc) return rc;
+    reduce_rows_kernel<<<pw_grid(N, P), 256, 0, st>>>(mres.u32(), N, ctx->d_pinfo);
+    HG_LAUNCH_CHECK(ctx);
+    for (int g0 = 0; g0 < count; g0 += G) {
+        const int gh = count - g0 < G ? count - g0 : G;
+        for (int h = 0; h < gh; h += 2) {
+            const int k = gh - h < 2 ? gh - h : 2;
+            OperandSet ops{};
+            for (int q = 0; q < k; ++q) {
+                ops.words[2 * q] = c0s[g0 + h + q]; ops.bits[2 * q] = level; ops.is_signed[2 * q] = 1;
+                ops.words[2 * q + 1] = c1s[g0 + h + q]; ops.bits[2 * q + 1] = level; ops.is_signed[2 * q + 1] = 1;
+            }
+            if ((rc = launch_modup(ctx, ops, 2 * k, P, cres.u32() + (size_t)2 * h * plane, 0, st))) return rc;
+        }
+        if ((rc = hg_ntt_launch(ctx, cres.u32(), 2 * gh * P, P, 0, true, st))) return rc;
+        // every poly times the shared plaintext, in place (each block reads its chunk first)
+        rc = hg_intt_fused(ctx, 5, cres.u32(), cres.u32(), mres.u32(), nullptr, nullptr, P, st, 2 * gh);
+        if (rc) return rc < 0 ? hg_fail(HG_EINVAL, "fused plaintext product not available") : rc;
+        OutSet outs{};
+        for (int g = 0; g < gh; ++g) {
+            outs.out[2 * g] = out0s[g0 + g];
+            outs.out[2 * g + 1] = out1s[g0 + g];
+        }
+        if ((rc = launch_crt(ctx, cres.u32(), 2 * gh, P, rescale_bits, level - rescale_bits, outs, st)))
+            return rc;
+    }
+    return HG_OK;
+}

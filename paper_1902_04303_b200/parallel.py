@@ -178,7 +178,7 @@ def compute_setup_sharded(engine, inputs, rank: int, world: int, group=None, gat
     del dup_own
     if gather_m:
         m = CPMatrix(cols=all_gather_ciphertexts(dict(zip(own, m_own.cols)), n, world, group),
-                     rows=m_own.rows, cols_logical=m_own.cols_logical)
+                     rows=m_own.rows, cols_logical=n)
     else:
         m = m_own
     inter = gwas.GwasIntermediate(w=w, w_inv=w_inv, z=z, M=m, z_prime=z_prime)

@@ -27,7 +27,6 @@ pytestmark = pytest.mark.gpu
 GOLD = json.load(open(os.path.join(HERE, "golden", "scale_hashes.json")))
 CASES = sorted(GOLD, key=lambda c: (GOLD[c]["log_n"], GOLD[c]["log_l"], GOLD[c]["level"]))
 
-_STATE: dict = {}
 
 
 def _ct_sha(ct) -> str:
@@ -47,38 +46,37 @@ def _check(case, name, ct):
     assert _ct_sha(ct) == want["sha256"], f"{case}/{name}: ciphertext words differ from the reference"
 
 
-def _state(case):
-    """Keys (own keygen, same seed), engine and the four input ciphertexts of a case."""
-    if _STATE.get("case") != case:
-        _STATE.clear()
-        import gc
+@pytest.fixture(scope="module", params=CASES)
+def st(request):
+    """Keys (own keygen, same seed), engine and the four input ciphertexts of a case (module
+    scope: pytest runs every test of one case before building the next)."""
+    import gc
 
-        gc.collect()
-        import paper_1902_04303_b200 as hg
-        from paper_1902_04303_b200.ring import RingElement, upload_words
+    import paper_1902_04303_b200 as hg
+    from paper_1902_04303_b200.ring import RingElement, upload_words
 
-        g = GOLD[case]
-        params = hg.CkksParams(log_n=g["log_n"], log_l=g["log_l"], log_p=g["log_p"],
-                               log_p_small=g["log_p_small"], h=g["h"])
-        keys = hg.keygen(params, g["seed"])
-        n, level, seed = params.n, g["level"], g["seed"]
+    gc.collect()
+    case = request.param
+    g = GOLD[case]
+    params = hg.CkksParams(log_n=g["log_n"], log_l=g["log_l"], log_p=g["log_p"],
+                           log_p_small=g["log_p_small"], h=g["h"])
+    keys = hg.keygen(params, g["seed"])
+    n, level, seed = params.n, g["level"], g["seed"]
 
-        def ct(tag):
-            c0 = RingElement(n, level, words=upload_words(random_words((seed, level, tag, 0), level, n)))
-            c1 = RingElement(n, level, words=upload_words(random_words((seed, level, tag, 1), level, n)))
-            return hg.Ciphertext(c0=c0, c1=c1, level_bits=level, scale_bits=params.log_p,
-                                 slots=params.slot_count, params=params)
+    def ct(tag):
+        c0 = RingElement(n, level, words=upload_words(random_words((seed, level, tag, 0), level, n)))
+        c1 = RingElement(n, level, words=upload_words(random_words((seed, level, tag, 1), level, n)))
+        return hg.Ciphertext(c0=c0, c1=c1, level_bits=level, scale_bits=params.log_p,
+                             slots=params.slot_count, params=params)
 
-        _STATE.update(case=case, params=params, keys=keys, engine=hg.HeEngine(params, keys[2], keys[3]),
-                      cts=[ct(i) for i in range(4)])
-    return _STATE
+    yield dict(case=case, params=params, keys=keys, engine=hg.HeEngine(params, keys[2], keys[3]),
+               cts=[ct(i) for i in range(4)])
 
 
-@pytest.mark.parametrize("case", CASES)
-def test_keygen_hashes(case):
+def test_keygen_hashes(st):
     from tests.gpu_helpers import ring_hash
 
-    st = _state(case)
+    case = st["case"]
     sk, pk, evk, rot = st["keys"]
     got = {"sk.s": ring_hash(sk.s), "pk.b": ring_hash(pk.b), "pk.a": ring_hash(pk.a),
            "evk.b": ring_hash(evk.b), "evk.a": ring_hash(evk.a),
@@ -89,11 +87,10 @@ def test_keygen_hashes(case):
     assert got == GOLD[case]["keys"]
 
 
-@pytest.mark.parametrize("case", CASES)
-def test_scheme_ops(case):
+def test_scheme_ops(st):
     from paper_1902_04303_b200 import ckks
 
-    st = _state(case)
+    case = st["case"]
     eng, (a, b, a2, b2), params = st["engine"], st["cts"], st["params"]
     slots = params.slot_count
     _check(case, "mult_ab", eng.mult(a, b))
@@ -115,9 +112,8 @@ def test_scheme_ops(case):
     _check(case, "mult_const_a", eng.mult_const(a, 0.125))
 
 
-@pytest.mark.parametrize("case", CASES)
-def test_batched_entry_points(case):
-    st = _state(case)
+def test_batched_entry_points(st):
+    case = st["case"]
     eng, (a, b, a2, b2), params = st["engine"], st["cts"], st["params"]
     slots = params.slot_count
     m1, m2 = eng.mult_many([a, a2], [b, b2])

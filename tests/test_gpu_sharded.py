@@ -70,8 +70,15 @@ def _worker(rank, world, port, q):
         dist.barrier()
         dist.destroy_process_group()
         q.put((rank, "ok"))
+        q.close()
+        q.join_thread()
+        os._exit(0)   # skip the interpreter's CUDA / gloo teardown (slow in spawned ranks)
     except Exception:
         q.put((rank, traceback.format_exc()))
+        # a failed rank may leave its peer blocked in a collective: leave without teardown
+        q.close()
+        q.join_thread()
+        os._exit(1)
 
 
 def test_two_ranks_split_setup_and_batches_bit_exact():
@@ -81,8 +88,14 @@ def test_two_ranks_split_setup_and_batches_bit_exact():
     procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    res = dict(q.get(timeout=600) for _ in procs)
-    for p in procs:
-        p.join(timeout=120)
+    try:
+        res = dict(q.get(timeout=600) for _ in procs)
+        for p in procs:
+            p.join(timeout=60)
+    finally:
+        for p in procs:   # never leave a rank behind (pytest would wait for it at exit)
+            if p.is_alive():
+                p.kill()
+                p.join(timeout=30)
     assert res == {0: "ok", 1: "ok"}, res
     assert all(p.exitcode == 0 for p in procs)
