@@ -168,9 +168,14 @@ def call(fn, *args):
     repeat recomputes every output from unchanged operands)."""
     rc = fn(*args)
     if rc != HG_OK and _is_oom(rc):
+        global OOM_RETRIES
+        OOM_RETRIES += 1
         release_device_memory()
         rc = fn(*args)
     check(rc)
+
+
+OOM_RETRIES = 0   # library-scratch out-of-memory retries so far (diagnostics)
 
 
 def operand(words, bits: int, signed: bool) -> Operand:

@@ -183,7 +183,7 @@ def compute_setup_sharded(engine, inputs, rank: int, world: int, group=None, gat
         m = m_own
     inter = gwas.GwasIntermediate(w=w, w_inv=w_inv, z=z, M=m, z_prime=z_prime)
     if prepare_left and hasattr(engine, "prepare"):
-        m_dup = [engine.prepare(ct) for ct in m_dup]
+        m_dup = [engine.prepare(ct, keep_words=False) for ct in m_dup]
     return beta, p_prev, inter, m_dup
 
 

@@ -126,12 +126,33 @@ def test_toy_pipeline_streamed_batches_bit_exact(toy):
     g, params, (sk, pk, evk, rot), ds, config, seed = toy
     enc = _golden_inputs(g, params, config)
     host = [HostSnpBatch.from_device(b) for b in enc.batches]
-    # three passes over the batches so both device slots are reused while the next one loads
-    stream = SnpBatchStream(host * 3, params)
-    out = compute_gwas_encrypted(hg.HeEngine(params, evk, rot), enc, cache=stream)
-    assert len(out.batch_outputs) == 3 * len(host)
-    for bo in out.batch_outputs:
+    # three passes over the batches so both device slots are reused while the next one loads;
+    # then the rows streamed only at the projector's level (mod_down on upload)
+    m_level = g.meta("out.M0")["level_bits"]
+    for level in (None, m_level):
+        stream = SnpBatchStream(host * 3, params, level=level)
+        out = compute_gwas_encrypted(hg.HeEngine(params, evk, rot), enc, cache=stream)
+        assert len(out.batch_outputs) == 3 * len(host)
+        for bo in out.batch_outputs:
+            assert_ct_equal(bo.num_ct, g, f"out.b{bo.index}.num")
+            assert_ct_equal(bo.den_even_ct, g, f"out.b{bo.index}.den_even")
+            if config.complex_packing:
+                assert_ct_equal(bo.den_odd_ct, g, f"out.b{bo.index}.den_odd")
+
+
+def test_batch_keys_prepared_by_the_setup(toy):
+    """gwas.batch_key_plan names every (switching key, level) the batch loop uses: after the
+    setup (which prepares them) a batch makes no further key preparation."""
+    import paper_1902_04303_b200 as hg
+    from paper_1902_04303_b200.ckks import KEY_CACHE
+    from paper_1902_04303_b200.gwas import compute_batch, compute_setup
+
+    g, params, (sk, pk, evk, rot), ds, config, seed = toy
+    enc = _golden_inputs(g, params, config)
+    engine = hg.HeEngine(params, evk, rot)
+    beta, p_prev, inter, m_dup = compute_setup(engine, enc)
+    misses = KEY_CACHE.misses
+    for batch in enc.batches:
+        bo = compute_batch(engine, enc, inter, m_dup, batch)
         assert_ct_equal(bo.num_ct, g, f"out.b{bo.index}.num")
-        assert_ct_equal(bo.den_even_ct, g, f"out.b{bo.index}.den_even")
-        if config.complex_packing:
-            assert_ct_equal(bo.den_odd_ct, g, f"out.b{bo.index}.den_odd")
+    assert KEY_CACHE.misses == misses
