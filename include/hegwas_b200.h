@@ -109,6 +109,9 @@ int hg_poly_tensor(hg_ctx* ctx, uint32_t* d0, uint32_t* d1, uint32_t* d2, int ou
 int hg_key_prepare(hg_ctx* ctx, const uint32_t* kb, const uint32_t* ka, int key_bits,
                    int level, int big_l, void* stream, hg_key** out);
 int hg_key_destroy(hg_key* key);
+/* Stream-ordered destroy: the key's device memory is reused only after the work queued on
+ * `stream` so far has completed (no host synchronisation, unlike hg_key_destroy). */
+int hg_key_release(hg_key* key, void* stream);
 size_t hg_key_device_bytes(const hg_key* key);
 /* (out0, out1) = (round(x*kb / 2^L), round(x*ka / 2^L)) mod 2^level, x canonical
  * (level bits).  If automorph_k != 1, x is first mapped by x -> x(X^k) (fused
@@ -158,6 +161,7 @@ int hg_ct_inner_prepared(hg_ctx* ctx, const hg_key* evk, int nq, int nb, const h
                          const uint32_t* const* b0s, const uint32_t* const* b1s, int level,
                          int rescale_bits, uint32_t* const* out0s, uint32_t* const* out1s, void* stream);
 int hg_ctprep_destroy(hg_ctprep* prep);
+int hg_ctprep_release(hg_ctprep* prep, void* stream);   /* stream-ordered, as hg_key_release */
 size_t hg_ctprep_device_bytes(const hg_ctprep* prep);
 /* hg_ct_mult with the left operand prepared (same output, bit for bit). */
 int hg_ct_mult_prepared(hg_ctx* ctx, const hg_key* evk, const hg_ctprep* a, const uint32_t* b0,

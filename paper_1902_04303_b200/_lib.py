@@ -59,6 +59,8 @@ SIGNATURES = {
     "hg_poly_tensor": (_i, [_vp, _vp, _vp, _vp, _i, Operand, Operand, Operand, Operand, _vp]),
     "hg_key_prepare": (_i, [_vp, _vp, _vp, _i, _i, _i, _vp, ctypes.POINTER(_vp)]),
     "hg_key_destroy": (_i, [_vp]),
+    "hg_key_release": (_i, [_vp, _vp]),
+    "hg_ctprep_release": (_i, [_vp, _vp]),
     "hg_key_device_bytes": (ctypes.c_size_t, [_vp]),
     "hg_keyswitch": (_i, [_vp, _vp, _vp, _i64, _vp, _vp, _vp]),
     "hg_ct_mult": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _vp, _vp, _vp]),
@@ -202,6 +204,13 @@ class Context:
         import torch
 
         return ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def compute_stream(self):
+        """The device's default torch stream, where this package issues its compute (the side
+        streams only copy): stream-ordered frees are ordered after it."""
+        import torch
+
+        return ctypes.c_void_p(torch.cuda.default_stream(self.device).cuda_stream)
 
     def primes(self) -> list[int]:
         n = self.lib.hg_ctx_num_primes(self.handle)

@@ -174,12 +174,55 @@ static void* arena_take(DeviceArena& a, size_t bytes) {
     return nullptr;
 }
 
+static void arena_free_locked(DeviceArena& a, void* ptr);
+
+// return deferred frees whose events have completed (block: wait for all of them)
+static void arena_reclaim_locked(DeviceArena& a, bool block) {
+    size_t k = 0;
+    for (auto& d : a.deferred) {
+        const cudaError_t q = block ? cudaEventSynchronize(d.second) : cudaEventQuery(d.second);
+        if (q == cudaSuccess) {
+            arena_free_locked(a, d.first);
+            a.spare_events.push_back(d.second);
+        } else {
+            if (q != cudaErrorNotReady) cudaGetLastError();
+            a.deferred[k++] = d;
+        }
+    }
+    a.deferred.resize(k);
+}
+
+int hg_arena_free_after(hg_ctx* ctx, void* ptr, cudaStream_t stream) {
+    if (!ptr) return HG_OK;
+    std::lock_guard<std::mutex> g(ctx->arena.mu);
+    DeviceArena& a = ctx->arena;
+    cudaEvent_t ev;
+    if (!a.spare_events.empty()) {
+        ev = a.spare_events.back();
+        a.spare_events.pop_back();
+    } else if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        cudaStreamSynchronize(stream);   // no event: order the free the slow way
+        arena_free_locked(a, ptr);
+        return HG_OK;
+    }
+    cudaEventRecord(ev, stream);
+    a.deferred.emplace_back(ptr, ev);
+    arena_reclaim_locked(a, false);
+    return HG_OK;
+}
+
 void* hg_arena_alloc(hg_ctx* ctx, size_t bytes) {
     if (!bytes) bytes = 1;
     bytes = (bytes + kArenaAlign - 1) & ~(kArenaAlign - 1);
     {
         std::lock_guard<std::mutex> g(ctx->arena.mu);
+        arena_reclaim_locked(ctx->arena, false);
         if (void* p = arena_take(ctx->arena, bytes)) return p;
+        if (!ctx->arena.deferred.empty()) {   // before growing: wait for pending frees
+            arena_reclaim_locked(ctx->arena, true);
+            if (void* p = arena_take(ctx->arena, bytes)) return p;
+        }
     }
     // grow by a default slab (or exactly the request when the device is nearly full)
     if (hg_arena_grow(ctx, bytes > kArenaSlab ? bytes : kArenaSlab) != HG_OK &&
@@ -192,7 +235,10 @@ void* hg_arena_alloc(hg_ctx* ctx, size_t bytes) {
 void hg_arena_free(hg_ctx* ctx, void* ptr) {
     if (!ptr) return;
     std::lock_guard<std::mutex> g(ctx->arena.mu);
-    DeviceArena& a = ctx->arena;
+    arena_free_locked(ctx->arena, ptr);
+}
+
+static void arena_free_locked(DeviceArena& a, void* ptr) {
     auto it = a.live.find((char*)ptr);
     if (it == a.live.end()) return;
     const int si = it->second.first;
@@ -226,6 +272,7 @@ extern "C" size_t hg_pool_trim(hg_ctx* ctx) {
     if (!ctx) return 0;
     std::lock_guard<std::mutex> g(ctx->arena.mu);
     DeviceArena& a = ctx->arena;
+    arena_reclaim_locked(a, true);
     size_t released = 0;
     std::vector<DeviceArena::Slab> keep;
     std::vector<int> remap(a.slabs.size(), -1);

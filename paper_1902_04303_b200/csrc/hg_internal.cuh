@@ -68,12 +68,18 @@ struct DeviceArena {
     };
     std::vector<Slab> slabs;
     std::map<char*, std::pair<int, size_t>> live;   // ptr -> (slab, length)
+    // stream-ordered frees: (object, event recorded on the stream that last used it); the
+    // memory returns to the free lists once the event has completed
+    std::vector<std::pair<void*, cudaEvent_t>> deferred;
+    std::vector<cudaEvent_t> spare_events;
     std::mutex mu;
     size_t reserved = 0;
     size_t in_use = 0;
 };
 void* hg_arena_alloc(hg_ctx* ctx, size_t bytes);   // nullptr when the device is out of memory
 void hg_arena_free(hg_ctx* ctx, void* p);
+// free `p` once the work queued on `stream` so far has finished (no host synchronisation)
+int hg_arena_free_after(hg_ctx* ctx, void* p, cudaStream_t stream);
 int hg_arena_grow(hg_ctx* ctx, size_t bytes);        // one more slab of exactly `bytes`
 
 struct hg_ctx {

@@ -59,6 +59,12 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar) : "memory");
 }
+// a * b + c, 32 x 32 -> 64-bit multiply-add (one IMAD.WIDE)
+__device__ __forceinline__ uint64_t madw(uint32_t a, uint32_t b, uint64_t c) {
+    uint64_t d;
+    asm("mad.wide.u32 %0, %1, %2, %3;\n" : "=l"(d) : "r"(a), "r"(b), "l"(c));
+    return d;
+}
 template <typename T>
 __device__ __forceinline__ T pick(const T (&a)[4], int k) {
     return k == 0 ? a[0] : k == 1 ? a[1] : k == 2 ? a[2] : a[3];
@@ -80,17 +86,25 @@ __global__ void __launch_bounds__(kWarps * 32, 1) modup_umma_kernel(
     __shared__ uint32_t s_fl[2][kRows];            // bit0 sign, bit1 negate, bit2 any-nonzero
     // per prime: p, 2^30 mod p (+ Shoup); per operand and prime: the sign correction
     // p - 2^bits mod p and the negation base (p for signed, p + 2^bits mod p for unsigned)
-    __shared__ uint4 s_pc[HG_MAX_PRIMES];
-    __shared__ uint2 s_corr[4][HG_MAX_PRIMES];
+    // padded by a prime chunk so the epilogue indexes base + constant without clamping
+    __shared__ uint4 s_pc[HG_MAX_PRIMES + kPrimesChunk];
+    __shared__ uint2 s_corr[4][HG_MAX_PRIMES + kPrimesChunk];
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    for (int j = tid; j < P; j += blockDim.x) {
+    for (int j = tid; j < P + kPrimesChunk; j += blockDim.x) {
+        if (j >= P) {
+            s_pc[j] = make_uint4(1u, 0u, 0u, 0u);
+            for (int k = 0; k < 4; ++k) s_corr[k][j] = make_uint2(0u, 0u);
+            continue;
+        }
         const PrimeInfo pi = pinfo[j];
         s_pc[j] = make_uint4(pi.p, pi.c30, pi.c30_sh, 0u);
         for (int k = 0; k < nops; ++k) {
             const int bits = pick(ops.bits, k);
             const uint32_t pw = reduce_u64((uint64_t)modup_tab[(size_t)j * HG_MODUP_WMAX + (bits >> 5)] << (bits & 31), pi);
-            s_corr[k][j] = make_uint2(pw ? pi.p - pw : 0u, pick(ops.is_signed, k) ? pi.p : pi.p + pw);
+            // sign correction (- 2^bits mod p) and the negation base for a value in [0, 3p):
+            // 3p (signed: -x) or 3p + (2^bits mod p) (unsigned: 2^bits - x)
+            s_corr[k][j] = make_uint2(pw ? pi.p - pw : 0u, pick(ops.is_signed, k) ? 3u * pi.p : 3u * pi.p + pw);
         }
     }
     if (warp == 1) {
@@ -252,6 +266,11 @@ __global__ void __launch_bounds__(kWarps * 32, 1) modup_umma_kernel(
                 const int jbase = ch * kPrimesChunk + h * kEpiPrimes;
                 const uint32_t lane_addr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ts * 256) +
                                            (uint32_t)(h * kEpiPrimes * 4);
+                // outputs are left lazily reduced in [0, 4p): every ModUp result feeds the forward
+                // NTT, whose butterflies take [0, 4p) inputs (fwd_bfly)
+                uint32_t* orow = outp + (size_t)jbase * N;
+                const uint4* pcb = s_pc + jbase;
+                const uint2* crb = corr + jbase;
 #pragma unroll 1
                 for (int jj = 0; jj < kEpiPrimes && jbase + jj < P; jj += 8) {
                     uint32_t d[32];
@@ -265,31 +284,24 @@ __global__ void __launch_bounds__(kWarps * 32, 1) modup_umma_kernel(
                                    "=r"(d[30]), "=r"(d[31])
                                  : "r"(lane_addr + (uint32_t)(jj * 4)));
                     asm volatile("tcgen05.wait::ld.sync.aligned;\n");
+                    const int nv = P - (jbase + jj);   // primes of this group that exist (warp-uniform)
 #pragma unroll
                     for (int e = 0; e < 8; ++e) {
                         // branch-free: the 8 primes are independent chains the scheduler interleaves
-                        const int j = jbase + jj + e;
-                        const int jc = j < P ? j : P - 1;
-                        const uint4 pc = s_pc[jc];
-                        const uint2 cr = corr[jc];
+                        const uint4 pc = pcb[jj + e];
                         const uint32_t p = pc.x;
                         // digits < 2^24 (K <= 256 bytes): v < 2^49, one 2^30 fold reaches [0, 4p)
-                        const uint64_t v = (uint64_t)d[4 * e] + ((uint64_t)d[4 * e + 1] << 8) +
-                                           ((uint64_t)d[4 * e + 2] << 16) + ((uint64_t)d[4 * e + 3] << 24);
+                        const uint32_t t = d[4 * e + 3] * 256u + d[4 * e + 2];   // < 2^31 (byte 3 < 64)
+                        const uint64_t v = madw(t, 1u << 16, madw(d[4 * e + 1], 256u, (uint64_t)d[4 * e]));
                         uint32_t r = mul_shoup_lazy((uint32_t)(v >> 30), pc.y, pc.z, p) +
                                      ((uint32_t)v & 0x3fffffffu);
-                        r = min(r, r - 2 * p);
-                        r = min(r, r - p);
-                        // two's-complement sign: subtract 2^bits; automorphism sign: negate
-                        if (SIGNED) {
-                            r += sgn ? cr.x : 0u;
-                            r = min(r, r - p);
+                        if (SIGNED || AUTOMORPH) {
+                            const uint2 cr = crb[jj + e];
+                            r = min(r, r - 2 * p);              // [0, 2p)
+                            if (SIGNED) r += sgn ? cr.x : 0u;   // two's-complement sign: -2^bits, [0, 3p)
+                            if (AUTOMORPH) r = ng ? cr.y - r : r;   // automorphism sign, (0, 4p)
                         }
-                        if (AUTOMORPH) {
-                            r = ng ? cr.y - r : r;   // < 2p
-                            r = min(r, r - p);
-                        }
-                        if (j < P) outp[(size_t)j * N] = r;
+                        if (e < nv) orow[(size_t)(jj + e) * N] = r;
                     }
                 }
                 asm volatile("tcgen05.fence::before_thread_sync;\n");

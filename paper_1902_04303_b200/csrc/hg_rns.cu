@@ -710,6 +710,15 @@ extern "C" int hg_key_destroy(hg_key* key) {
     return HG_OK;
 }
 
+// stream-ordered destruction: the key's memory returns to the arena once the work queued on
+// `stream` (the stream its readers were issued on) has finished -- no host synchronisation
+extern "C" int hg_key_release(hg_key* key, void* stream) {
+    if (!key) return HG_OK;
+    int rc = hg_arena_free_after(key->ctx, key->d_kb, (cudaStream_t)stream);
+    delete key;
+    return rc;
+}
+
 extern "C" size_t hg_key_device_bytes(const hg_key* key) { return key ? key->bytes : 0; }
 
 static int64_t inverse_mod_2n(int64_t k, int64_t n2) {
@@ -883,6 +892,14 @@ extern "C" int hg_ctprep_destroy(hg_ctprep* pr) {
     hg_arena_free(pr->ctx, pr->d_res);
     delete pr;
     return HG_OK;
+}
+
+/* As hg_key_release for a prepared operand. */
+extern "C" int hg_ctprep_release(hg_ctprep* pr, void* stream) {
+    if (!pr) return HG_OK;
+    int rc = hg_arena_free_after(pr->ctx, pr->d_res, (cudaStream_t)stream);
+    delete pr;
+    return rc;
 }
 
 extern "C" size_t hg_ctprep_device_bytes(const hg_ctprep* pr) { return pr ? pr->bytes : 0; }
