@@ -92,6 +92,7 @@ SIGNATURES = {
                                             ctypes.POINTER(_vp), ctypes.POINTER(_vp), _vp]),
     "hg_ntt_forward": (_i, [_vp, _vp, _i, _i, _vp]),
     "hg_ntt_inverse": (_i, [_vp, _vp, _i, _i, _vp]),
+    "hg_set_ntt_variant": (_i, [_vp, _i]),
     "hg_bench_modmul": (_i, [_vp, _i, _vp, ctypes.POINTER(ctypes.c_double), _vp]),
     "hg_bench_mac": (_i, [_vp, _i, _vp, ctypes.POINTER(ctypes.c_double), _vp]),
     "hg_launch_count": (ctypes.c_longlong, [_vp]),

@@ -132,6 +132,7 @@ extern "C" int hg_ctx_create(int log_n, int device, hg_ctx** out) {
         hg_ctx_destroy(ctx);
         return hg_fail(HG_ECUDA, std::string("context upload: ") + cudaGetErrorString(e));
     }
+    if (const char* v = getenv("HG_NTT_CLUSTER")) ctx->ntt_cluster = v[0] == '1';
     *out = ctx;
     return HG_OK;
 }
@@ -305,6 +306,8 @@ extern "C" int hg_ctx_destroy(hg_ctx* ctx) {
     cudaFree(ctx->d_modup);
     cudaFree(ctx->d_tw_fwd);
     cudaFree(ctx->d_tw_inv);
+    cudaFree(ctx->d_twc_fwd);
+    cudaFree(ctx->d_twc_inv);
     cudaFree(ctx->d_modup_frag);
     cudaFree(ctx->d_modup_umma);
     for (auto& sl : ctx->arena.slabs) cudaFree(sl.base);

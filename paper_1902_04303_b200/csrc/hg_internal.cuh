@@ -97,6 +97,10 @@ struct hg_ctx {
     uint2* d_tw_fwd = nullptr;
     uint2* d_tw_inv = nullptr;
     int tw_ready = 0;
+    // log_n = 17 cluster NTT: lane-transposed round-B twiddles (hg_ntt_cluster.cu), lazily built
+    uint2* d_twc_fwd = nullptr;
+    uint2* d_twc_inv = nullptr;
+    int ntt_cluster = 0;   // use the cluster kernels where they apply (hg_set_ntt_variant; env HG_NTT_CLUSTER=1)
     uint32_t* d_modup_frag = nullptr;   // ModUp-on-tensor-cores B fragments (hg_modup_mma.cu)
     uint8_t* d_modup_umma = nullptr;    // ModUp tcgen05 B smem images (hg_modup_umma.cu)
     int modup_frag_ks = 0;
@@ -184,6 +188,12 @@ static inline int hg_env_group(const char* name, int dflt, int lo, int hi) {
 int hg_tmap_2d_u32(CUtensorMap* tm, const void* base, uint64_t inner, uint64_t outer,
                    uint32_t box_inner, uint32_t box_outer);
 int hg_ensure_twiddles(hg_ctx* ctx, int P);
+// one-round-trip length-2^17 transforms on 8-CTA clusters (hg_ntt_cluster.cu)
+bool hg_ntt_cluster_ok(const hg_ctx* ctx, int P);
+int hg_ntt_cluster(hg_ctx* ctx, uint32_t* data, int rows, int P, int prime_offset, bool forward,
+                   cudaStream_t st);
+int hg_intt_fused_cluster(hg_ctx* ctx, int pre, uint32_t* out, const uint32_t* i0, const uint32_t* i1,
+                          const uint32_t* i2, const uint32_t* i3, int P, cudaStream_t st, int batch);
 int hg_get_crt(hg_ctx* ctx, int P, const CrtTable** out);
 // host -> device copy of a lazily built table on the context's private non-blocking stream: a
 // plain cudaMemcpy would synchronise with the legacy default stream and so wait for every

@@ -476,6 +476,8 @@ int hg_ntt_launch(hg_ctx* ctx, uint32_t* data, int rows, int P, int prime_offset
     if (rc) return rc;
     const int log_n = ctx->log_n, N = ctx->N;
     const uint2* tw = forward ? ctx->d_tw_fwd : ctx->d_tw_inv;
+    if (rows % P == 0 && rows / P <= 65535 && hg_ntt_cluster_ok(ctx, P))
+        return hg_ntt_cluster(ctx, data, rows, P, prime_offset, forward, stream);
     HgTimed tm(ctx, stream, HG_K_NTT, (double)rows * (N / 2) * log_n);
     if (log_n >= 3 && rows % P == 0 && P <= 65535) {
         const int k1 = log_n <= 11 ? 0 : (log_n <= 14 ? 3 : 6);
@@ -530,6 +532,7 @@ int hg_intt_fused(hg_ctx* ctx, int pre, uint32_t* out, const uint32_t* i0, const
     const int k2 = log_n - k1;
     const int rb = pre == 1 ? 2 : (pre == 2 ? 3 : 1);
     if (batch < 1 || (batch > 1 && pre != 1 && pre != 5) || batch > 65535) return -1;
+    if (hg_ntt_cluster_ok(ctx, P)) return hg_intt_fused_cluster(ctx, pre, out, i0, i1, i2, i3, P, st, batch);
     HgTimed tm(ctx, st, HG_K_NTT, (double)batch * rb * P * (N / 2) * log_n);
     // batch > 1 (key switch only): input g's x rows at i0 + g P N, its two outputs at out + g 2 P N
     const dim3 g(N >> k2, batch, P);
