@@ -819,6 +819,27 @@ __global__ void __launch_bounds__(PipeCfg<FUSED>::kWarps * 32, 1) crt_umma_pipe_
             PWAIT(2, smem_u32(&bar_tm_full[tb]), (ij >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;\n");
             const uint32_t lane_addr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(tb * 256);
+            // steps [fast_lo, fast_hi] (first column of an 8-word step) take the interior path:
+            // window words u = t - sw - ush in [max(0, rw2 + 1), out_w - 2] (no top-word mask, no
+            // rescale rounding bit), past the key switch's rounding column, and fused output
+            // words v = u - rw - vsh in [0, out2_w - 2]
+            int fast_lo = sw + ush + (rw2 + 1 > 0 ? rw2 + 1 : 0);
+            if (shift > 0 && fast_lo <= round_col) fast_lo = round_col + 1;
+            int fast_hi = out_w - 2 + sw + ush - 7;
+            if (FUSED) {
+                if (fast_lo < sw + ush + rw + vsh) fast_lo = sw + ush + rw + vsh;
+                const int hi2 = out2_w - 2 + rw + vsh + sw + ush - 7;
+                if (fast_hi > hi2) fast_hi = hi2;
+            }
+            const int fast_v0 = sw + ush + rw + vsh;   // column of output word v = 0 (fused)
+#ifdef HG_CRT_WIDE_FOLD
+            // digit weights the compiler cannot see through: one IMAD.WIDE per digit instead of
+            // the shift / high-shift / add-with-carry sequence (N < 2^31, so the term is 0)
+            const uint32_t kz = (uint32_t)(N >> 31);
+            const uint32_t k8 = 256u + kz, k16 = (1u << 16) + kz, k24 = (1u << 24) + kz;
+#else
+            constexpr uint32_t k8 = 256u, k16 = 1u << 16, k24 = 1u << 24;
+#endif
 #ifdef HG_CRT_PROF
             const long long t_loop = clock64();
 #endif
@@ -848,9 +869,54 @@ __global__ void __launch_bounds__(PipeCfg<FUSED>::kWarps * 32, 1) crt_umma_pipe_
 #pragma unroll
                 for (int hh = 0; hh < 8; ++hh) {
                     const uint32_t* E = e + 4 * hh;
-                    val[hh] = madw(E[3], 1u << 24, madw(E[2], 1u << 16, madw(E[1], 256u, (uint64_t)E[0])));
+                    val[hh] = madw(E[3], k24, madw(E[2], k16, madw(E[1], k8, (uint64_t)E[0])));
                 }
                 uint32_t wv[8];
+                const int t0 = c0 + tl;
+                if (t0 >= fast_lo && t0 <= fast_hi) {
+                    // interior step: every word is a full (unmasked) window word past the rounding
+                    // column and, fused, a full output word past the rescale's rounding bit --
+                    // no per-word predicates, pointer-stepped stores
+#pragma unroll
+                    for (int hh = 0; hh < 8; ++hh) {
+                        const uint64_t x = val[hh] + carry;
+                        wv[hh] = (uint32_t)x;
+                        carry = x >> 32;
+                    }
+                    if (FUSED) {
+                        uint32_t* op = outi + (size_t)(t0 - fast_v0) * N;
+                        const uint32_t* ap = av + tl * kRows;
+#pragma unroll
+                        for (int hh = 0; hh < 8; ++hh) {
+                            const uint32_t o = sbit ? __funnelshift_r(prev, wv[hh], sbit) : wv[hh];
+                            prev = wv[hh];
+                            const uint64_t sum = (uint64_t)o + ap[hh * kRows] + c2;
+                            const uint32_t w = (uint32_t)sum;
+                            c2 = (uint32_t)(sum >> 32);
+                            *op = rb ? __funnelshift_r(prev2, w, rb) : w;
+                            prev2 = w;
+                            op += N;
+                        }
+                    } else {
+                        uint32_t* op = outi + (size_t)(t0 - sw - ush) * N;
+                        if (sbit) {
+#pragma unroll
+                            for (int hh = 0; hh < 8; ++hh) {
+                                *op = __funnelshift_r(prev, wv[hh], sbit);
+                                prev = wv[hh];
+                                op += N;
+                            }
+                        } else {
+#pragma unroll
+                            for (int hh = 0; hh < 8; ++hh) {
+                                *op = wv[hh];
+                                op += N;
+                            }
+                            prev = wv[7];
+                        }
+                    }
+                    continue;
+                }
 #pragma unroll
                 for (int hh = 0; hh < 8; ++hh) {
                     const uint64_t x = val[hh] + carry + (c0 + tl + hh == round_col ? round_bit : 0u);

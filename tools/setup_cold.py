@@ -18,6 +18,7 @@ from paper_1902_04303_b200 import _lib, ckks, gwas, matrix  # noqa: E402
 from paper_1902_04303_b200.data import synth_gwas_dataset  # noqa: E402
 from paper_1902_04303_b200.logreg import hom_logreg  # noqa: E402
 
+BUSY = False
 ACC = {"key_s": 0.0, "key_n": 0, "mask_s": 0.0, "mask_n": 0}
 
 
@@ -56,6 +57,8 @@ class T:
 
     def __enter__(self):
         torch.cuda.synchronize()
+        if BUSY:
+            _lib.get_context(17).set_kernel_timing(True)
         self.acc = dict(ACC)
         self.ms = torch.cuda.memory_stats()
         self.t = time.perf_counter()
@@ -66,18 +69,28 @@ class T:
         dt = time.perf_counter() - self.t
         ms = torch.cuda.memory_stats()
         d = {k: ACC[k] - self.acc[k] for k in ACC}
+        busy = ""
+        if BUSY:
+            ctx = _lib.get_context(17)
+            st = {k: ctx.kernel_stats(k) for k in ("crt", "modup", "ntt", "pointwise", "elementwise")}
+            ctx.set_kernel_timing(False)
+            busy = "  device " + " ".join(f"{k} {v['ms']:.0f}ms/{v['launches']}" for k, v in st.items()) + \
+                f" = {sum(v['ms'] for v in st.values()) / 1e3:.2f}s"
         print(f"{self.name:16s} wall {dt:6.2f}s (host issue {th:5.2f}s)  key-prep {d['key_n']:4d} "
               f"{d['key_s']:5.2f}s  masks {d['mask_n']:4d} {d['mask_s']:5.2f}s  "
               f"cudaMalloc {ms['num_device_alloc'] - self.ms.get('num_device_alloc', 0):5d} "
               f"retries {ms['num_alloc_retries'] - self.ms.get('num_alloc_retries', 0)} "
-              f"reserved {ms['reserved_bytes.all.current'] / 1e9:5.1f} GB", flush=True)
+              f"reserved {ms['reserved_bytes.all.current'] / 1e9:5.1f} GB{busy}", flush=True)
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=245)
     ap.add_argument("--no-plan", action="store_true")
+    ap.add_argument("--busy", action="store_true", help="per-stage device busy time by kernel class")
     args = ap.parse_args()
+    global BUSY
+    BUSY = args.busy
     _wrap_key_get()
     _wrap_mask()
     params = hg.CkksParams(log_n=17, log_l=1700, log_p=45, log_p_small=30)
