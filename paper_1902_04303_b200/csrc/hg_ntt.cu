@@ -270,15 +270,18 @@ __global__ void __launch_bounds__(256, HG_LO_MINB) ntt_lo8_kernel(uint32_t* __re
 
 // Strided stages [0, K1), K1 in {3, 6}: tile of 2^K1 rows (stride 2^k2) x (2048 >> K1)
 // columns; thread = (column c, row group g) holding 8 rows.  K1 = 3 needs no shared memory.
-template <bool FWD, int K1, int RB>
+// K2 = log_n - K1 as a template parameter: every row / column offset is a compile-time
+// immediate (fewer address instructions per butterfly in this memory-heavy pass)
+template <bool FWD, int K1, int RB, int K2>
 __global__ void __launch_bounds__(256, HG_HI_MINB) ntt_hi8_kernel(uint32_t* __restrict__ data, int log_n,
                                                       int P, int bb0, int prime_offset,
                                                       const PrimeInfo* __restrict__ pinfo,
                                                       const uint2* __restrict__ tw) {
     __shared__ uint32_t sm[K1 > 3 ? RB * kTile : 1];
     constexpr int TC = kTile >> K1;
-    const int N = 1 << log_n;
-    const int k2 = log_n - K1;
+    constexpr int N = 1 << (K1 + K2);
+    constexpr int k2 = K2;
+    (void)log_n;
     const int jp = blockIdx.z, bb = bb0 + blockIdx.y * RB;
     const int prime = prime_offset + jp;
     const uint32_t p = pinfo[prime].p;
@@ -303,10 +306,17 @@ __global__ void __launch_bounds__(256, HG_HI_MINB) ntt_hi8_kernel(uint32_t* __re
         constexpr int BB = FWD ? 0 : 3;
         const int ra = BA ? g : 8 * g;
         const int rb = BB ? g : 8 * g;
+        uint32_t* pa[RB];
+        uint32_t* pb[RB];
+#pragma unroll
+        for (int r = 0; r < RB; ++r) {
+            pa[r] = colp + r * rstride + ((size_t)ra << k2);
+            pb[r] = colp + r * rstride + ((size_t)rb << k2);
+        }
 #pragma unroll
         for (int r = 0; r < RB; ++r)
 #pragma unroll
-            for (int m = 0; m < 8; ++m) x[r][m] = colp[r * rstride + ((size_t)(ra + (m << BA)) << k2)];
+            for (int m = 0; m < 8; ++m) x[r][m] = pa[r][(m << BA) << k2];
         round8<FWD, 3, BA, (FWD ? 0 : 3), RB>(x, 1, ra, twp, p);
 #pragma unroll
         for (int r = 0; r < RB; ++r)
@@ -321,7 +331,7 @@ __global__ void __launch_bounds__(256, HG_HI_MINB) ntt_hi8_kernel(uint32_t* __re
 #pragma unroll
         for (int r = 0; r < RB; ++r)
 #pragma unroll
-            for (int m = 0; m < 8; ++m) colp[r * rstride + ((size_t)(rb + (m << BB)) << k2)] = x[r][m];
+            for (int m = 0; m < 8; ++m) pb[r][(m << BB) << k2] = x[r][m];
     }
 }
 
@@ -431,9 +441,17 @@ int launch_lo8(int k2, dim3 grid, cudaStream_t st, uint32_t* data, int log_n, in
 template <bool FWD, int RB>
 int launch_hi8(int k1, dim3 grid, cudaStream_t st, uint32_t* data, int log_n, int P, int bb0,
                int off, const PrimeInfo* pinfo, const uint2* tw) {
-    if (k1 == 3) ntt_hi8_kernel<FWD, 3, RB><<<grid, 256, 0, st>>>(data, log_n, P, bb0, off, pinfo, tw);
-    else if (k1 == 6) ntt_hi8_kernel<FWD, 6, RB><<<grid, 256, 0, st>>>(data, log_n, P, bb0, off, pinfo, tw);
-    return 0;
+    // k1 = 3 for log_n 12..14, 6 for 15..17 (hg_ntt_launch)
+    switch (log_n) {
+#define HG_HI(LN, K1)                                                                              \
+    case LN:                                                                                       \
+        ntt_hi8_kernel<FWD, K1, RB, LN - K1><<<grid, 256, 0, st>>>(data, log_n, P, bb0, off, pinfo, tw); \
+        return 0;
+        HG_HI(12, 3) HG_HI(13, 3) HG_HI(14, 3) HG_HI(15, 6) HG_HI(16, 6) HG_HI(17, 6)
+#undef HG_HI
+    }
+    (void)k1;
+    return -1;
 }
 
 // one pass over all rows: groups of 2 batch rows per block (3 for an odd count), 1 if B == 1
