@@ -345,11 +345,20 @@ __global__ void __launch_bounds__(2 * kRows) crt_umma_kernel(
 constexpr int kConvWarp0 = 3, kEpiWarp0 = 11, kAddWarp = 19;
 template <bool FUSED> struct PipeCfg {
     static constexpr int kWarps = FUSED ? 20 : 19;
-    static constexpr int kRR = FUSED ? 2 : 3;
+#ifndef HG_CRT_RR_FUSED
+#define HG_CRT_RR_FUSED 2
+#endif
+#ifndef HG_CRT_RR_PLAIN
+#define HG_CRT_RR_PLAIN 3
+#endif
+    static constexpr int kRR = FUSED ? HG_CRT_RR_FUSED : HG_CRT_RR_PLAIN;
     static constexpr int kRA = FUSED ? 3 : 4;
     static constexpr int kRB = FUSED ? 2 : 3;
 };
-constexpr int kJobCols = 64;                     // output words per job (4 columns each: N = 256)
+#ifndef HG_CRT_JOBCOLS
+#define HG_CRT_JOBCOLS 64
+#endif
+constexpr int kJobCols = HG_CRT_JOBCOLS;          // output words per job (4 columns each: N <= 256)
 constexpr int kResStage = 32 * kRows * 4;        // 16 KB: 32 prime rows of 128 residues
 constexpr int kAStage = kRows * kKChunk;         // 16 KB
 constexpr int kBStagePipe = kJobCols * 4 * kKChunk;   // 32 KB
