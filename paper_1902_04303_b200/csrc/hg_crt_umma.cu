@@ -346,17 +346,17 @@ constexpr int kConvWarp0 = 3, kEpiWarp0 = 11, kAddWarp = 19;
 template <bool FUSED> struct PipeCfg {
     static constexpr int kWarps = FUSED ? 20 : 19;
 #ifndef HG_CRT_RR_FUSED
-#define HG_CRT_RR_FUSED 2
+#define HG_CRT_RR_FUSED 3
 #endif
 #ifndef HG_CRT_RR_PLAIN
-#define HG_CRT_RR_PLAIN 3
+#define HG_CRT_RR_PLAIN 4
 #endif
     static constexpr int kRR = FUSED ? HG_CRT_RR_FUSED : HG_CRT_RR_PLAIN;
     static constexpr int kRA = FUSED ? 3 : 4;
     static constexpr int kRB = FUSED ? 2 : 3;
 };
 #ifndef HG_CRT_JOBCOLS
-#define HG_CRT_JOBCOLS 64
+#define HG_CRT_JOBCOLS 56   // 49-52-word windows are one job; 56 frees smem for a third / fourth residue stage
 #endif
 constexpr int kJobCols = HG_CRT_JOBCOLS;          // output words per job (4 columns each: N <= 256)
 constexpr int kResStage = 32 * kRows * 4;        // 16 KB: 32 prime rows of 128 residues

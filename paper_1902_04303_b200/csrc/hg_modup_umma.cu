@@ -59,12 +59,14 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar) : "memory");
 }
+#ifdef HG_MODUP_FOLD30
 // a * b + c, 32 x 32 -> 64-bit multiply-add (one IMAD.WIDE)
 __device__ __forceinline__ uint64_t madw(uint32_t a, uint32_t b, uint64_t c) {
     uint64_t d;
     asm("mad.wide.u32 %0, %1, %2, %3;\n" : "=l"(d) : "r"(a), "r"(b), "l"(c));
     return d;
 }
+#endif
 template <typename T>
 __device__ __forceinline__ T pick(const T (&a)[4], int k) {
     return k == 0 ? a[0] : k == 1 ? a[1] : k == 2 ? a[2] : a[3];
@@ -98,7 +100,12 @@ __global__ void __launch_bounds__(kWarps * 32, 1) modup_umma_kernel(
             continue;
         }
         const PrimeInfo pi = pinfo[j];
+#ifdef HG_MODUP_FOLD30
         s_pc[j] = make_uint4(pi.p, pi.c30, pi.c30_sh, 0u);
+#else
+        // 2^16 mod p = 2^16 (p > 2^16): its Shoup companion floor(2^48 / p)
+        s_pc[j] = make_uint4(pi.p, 1u << 16, (uint32_t)((1ull << 48) / pi.p), 0u);
+#endif
         for (int k = 0; k < nops; ++k) {
             const int bits = pick(ops.bits, k);
             const uint32_t pw = reduce_u64((uint64_t)modup_tab[(size_t)j * HG_MODUP_WMAX + (bits >> 5)] << (bits & 31), pi);
@@ -290,11 +297,22 @@ __global__ void __launch_bounds__(kWarps * 32, 1) modup_umma_kernel(
                         // branch-free: the 8 primes are independent chains the scheduler interleaves
                         const uint4 pc = pcb[jj + e];
                         const uint32_t p = pc.x;
+#ifdef HG_MODUP_FOLD30
                         // digits < 2^24 (K <= 256 bytes): v < 2^49, one 2^30 fold reaches [0, 4p)
                         const uint32_t t = d[4 * e + 3] * 256u + d[4 * e + 2];   // < 2^31 (byte 3 < 64)
                         const uint64_t v = madw(t, 1u << 16, madw(d[4 * e + 1], 256u, (uint64_t)d[4 * e]));
                         uint32_t r = mul_shoup_lazy((uint32_t)(v >> 30), pc.y, pc.z, p) +
                                      ((uint32_t)v & 0x3fffffffu);
+#else
+                        // v = D0 + D1 2^8 + D2 2^16 + D3 2^24 (digits <= 256 * 255^2 < 2^24, D3 < 2^22)
+                        //   = T' 2^16 + (U mod 2^16),  U = D1 2^8 + D0 < 2^32,  T' = D3 2^8 + D2 + (U >> 16) < 2^31
+                        // so one Shoup product by 2^16 (a shift and one multiply-high) and a 16-bit add
+                        // land in [0, 2p + 2^16) within [0, 3p), all in 32-bit arithmetic
+                        const uint32_t u = d[4 * e + 1] * 256u + d[4 * e];
+                        const uint32_t tt = d[4 * e + 3] * 256u + d[4 * e + 2] + (u >> 16);
+                        const uint32_t q = __umulhi(tt, pc.z);
+                        uint32_t r = (tt << 16) - q * p + (u & 0xffffu);
+#endif
                         if (SIGNED || AUTOMORPH) {
                             const uint2 cr = crb[jj + e];
                             r = min(r, r - 2 * p);              // [0, 2p)
