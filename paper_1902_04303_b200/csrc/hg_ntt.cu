@@ -139,7 +139,8 @@ __device__ __forceinline__ void round8(uint32_t (&x)[RB][8], int G, int base,
         const int d = 1 << (R - 1 - k);
         // the 8 >> (R-k) twiddles of this stage are contiguous and aligned to their count:
         // 16-byte loads
-        const uint2* tg = twp + (G << (LS0 + k)) + (base >> (B + R - k));
+        // unsigned 32-bit index: one shift-add into the block's table pointer (no sign extension)
+        const uint2* tg = twp + (((uint32_t)G << (LS0 + k)) + ((uint32_t)base >> (B + R - k)));
         uint2 w[4];
         const int nt = 8 >> (R - k);
         if (nt == 1) {
@@ -164,12 +165,9 @@ __device__ __forceinline__ void round8(uint32_t (&x)[RB][8], int G, int base,
     }
 }
 
-// bank-conflict swizzle (a bijection on [0, 2048)): bits 2-4 ^= bits 5-7
-__device__ __forceinline__ int swz(int i) { return i ^ (((i >> 5) & 7) << 2); }
-
 template <int B>
 __device__ __forceinline__ void load8(uint32_t (&x)[8], const uint32_t* src, int base) {
-    if (B == 0) {   // contiguous (the smem swizzle keeps 4-word groups): 16-byte accesses
+    if (B == 0) {   // contiguous: 16-byte accesses
         const uint4 a = *reinterpret_cast<const uint4*>(src + base);
         const uint4 b = *reinterpret_cast<const uint4*>(src + base + 4);
         x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
@@ -188,29 +186,44 @@ __device__ __forceinline__ void store8(const uint32_t (&x)[8], uint32_t* dst, in
         for (int m = 0; m < 8; ++m) dst[base + (m << B)] = x[m];
     }
 }
+
+// Shared-memory rows are padded: word i of a 2048-word row sits at pad(i) = i + 4 (i >> 5) (four
+// spare words after every 32), which keeps every round's access pattern free of bank conflicts
+// and -- unlike an XOR swizzle -- lets a thread's 8 words be one base address plus compile-time
+// offsets: for B >= 5 the 8 words lie in different 32-word blocks (offset m 2^B + m 2^(B-3)),
+// for B <= 2 in the thread's own block (base mod 32 + 7 2^B < 32: offset m 2^B)
+__device__ __forceinline__ int pad(int i) { return i + ((i >> 5) << 2); }
+template <int B>
+__device__ __forceinline__ int pad_off(int pb, int base, int m) {
+    if constexpr (B >= 5) return pb + (m << B) + (m << (B - 3));
+    else if constexpr (B <= 2) return pb + (m << B);
+    else return pad(base + (m << B));
+}
 template <int B>
 __device__ __forceinline__ void sload8(uint32_t (&x)[8], const uint32_t* s, int base) {
-    if (B == 0) {
-        const uint4 a = *reinterpret_cast<const uint4*>(s + swz(base));
-        const uint4 b = *reinterpret_cast<const uint4*>(s + swz(base + 4));
+    const int pb = pad(base);
+    if (B == 0) {   // 8 words inside one 32-word block: 16-byte accesses
+        const uint4 a = *reinterpret_cast<const uint4*>(s + pb);
+        const uint4 b = *reinterpret_cast<const uint4*>(s + pb + 4);
         x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
     } else {
 #pragma unroll
-        for (int m = 0; m < 8; ++m) x[m] = s[swz(base + (m << B))];
+        for (int m = 0; m < 8; ++m) x[m] = s[pad_off<B>(pb, base, m)];
     }
 }
 template <int B>
 __device__ __forceinline__ void sstore8(const uint32_t (&x)[8], uint32_t* s, int base) {
+    const int pb = pad(base);
     if (B == 0) {
-        *reinterpret_cast<uint4*>(s + swz(base)) = make_uint4(x[0], x[1], x[2], x[3]);
-        *reinterpret_cast<uint4*>(s + swz(base + 4)) = make_uint4(x[4], x[5], x[6], x[7]);
+        *reinterpret_cast<uint4*>(s + pb) = make_uint4(x[0], x[1], x[2], x[3]);
+        *reinterpret_cast<uint4*>(s + pb + 4) = make_uint4(x[4], x[5], x[6], x[7]);
     } else {
 #pragma unroll
-        for (int m = 0; m < 8; ++m) s[swz(base + (m << B))] = x[m];
+        for (int m = 0; m < 8; ++m) s[pad_off<B>(pb, base, m)] = x[m];
     }
 }
 
-constexpr int kSmRow = kTile;   // the swizzle stays inside the row: no padding
+constexpr int kSmRow = kTile + kTile / 8;   // padded row (2304 words)
 
 template <bool FWD, int K2, int ROUND, int RB, bool PRELOADED = false>
 __device__ __forceinline__ void lo_round(uint32_t (&x)[RB][8], uint32_t* __restrict__ rowp,
@@ -227,16 +240,19 @@ __device__ __forceinline__ void lo_round(uint32_t (&x)[RB][8], uint32_t* __restr
         if (ROUND == 0) {
             if (!PRELOADED) load8<B>(x[r], rowp + r * rstride, base);
         } else {
-            sload8<B>(x[r], sm + (((ROUND - 1) & 1) * RB + r) * kSmRow, base);
+            sload8<B>(x[r], sm + r * kSmRow, base);
         }
     }
+    // one buffer, updated in place: a round reads and writes the same words of each row (its
+    // thread -> word map partitions the row), so one barrier per round orders it after the
+    // previous round's writes
     round8<FWD, R, B, LS0, RB>(x, G, base, twp, p);
     if (ROUND == NR - 1) {
 #pragma unroll
         for (int r = 0; r < RB; ++r) store8<B>(x[r], rowp + r * rstride, base);
     } else {
 #pragma unroll
-        for (int r = 0; r < RB; ++r) sstore8<B>(x[r], sm + ((ROUND & 1) * RB + r) * kSmRow, base);
+        for (int r = 0; r < RB; ++r) sstore8<B>(x[r], sm + r * kSmRow, base);
         __syncthreads();
     }
 }
@@ -249,7 +265,7 @@ __global__ void __launch_bounds__(256, HG_LO_MINB) ntt_lo8_kernel(uint32_t* __re
                                                       int P, int bb0, int prime_offset,
                                                       const PrimeInfo* __restrict__ pinfo,
                                                       const uint2* __restrict__ tw) {
-    __shared__ __align__(16) uint32_t sm[2 * RB * kSmRow];
+    __shared__ __align__(16) uint32_t sm[RB * kSmRow];
     const int N = 1 << log_n;
     const int k1 = log_n - K2;
     const int jp = blockIdx.z, bb = bb0 + blockIdx.y * RB;
@@ -358,7 +374,7 @@ __global__ void __launch_bounds__(256, HG_FUSED_MINB) intt_lo8_fused_kernel(
     out += blockIdx.y * bstride_out;
     in0 += blockIdx.y * bstride_in;
     constexpr int RB = PreRows<PRE>::value;
-    __shared__ __align__(16) uint32_t sm[2 * RB * kSmRow];
+    __shared__ __align__(16) uint32_t sm[RB * kSmRow];
     const int N = 1 << log_n;
     const int k1 = log_n - K2;
     const int jp = blockIdx.z;
