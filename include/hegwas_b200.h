@@ -216,10 +216,11 @@ int hg_ct_mult_const_rescale_batch(hg_ctx* ctx, int count, const uint32_t* const
  * (prime i % num_primes for row i); data is [count][N] uint32 on device.            */
 int hg_ntt_forward(hg_ctx* ctx, uint32_t* data, int count, int prime_offset, void* stream);
 int hg_ntt_inverse(hg_ctx* ctx, uint32_t* data, int count, int prime_offset, void* stream);
-/* NTT kernel variant for log_n = 17: 1 = one HBM round trip on 8-CTA clusters exchanging
-   through distributed shared memory, 0 = two passes (default, measured faster).  Same output
-   words. */
-int hg_set_ntt_variant(hg_ctx* ctx, int cluster);
+/* NTT kernel variant: 0 = two passes (strided tiles, contiguous chunks), 1 = log_n 17 on 8-CTA
+   clusters exchanging through distributed shared memory, 2 = log_n 17 both passes in one launch
+   on 8-CTA clusters with the intermediate through L2 (other sizes: two passes).  Same output
+   words; 0 is the default (measured fastest). */
+int hg_set_ntt_variant(hg_ctx* ctx, int variant);
 /* Integer-pipe peak microbenchmark: runs the NTT butterfly modmul sequence register-
  * resident on all SMs; returns butterflies executed (host) for `iters`.              */
 int hg_bench_modmul(hg_ctx* ctx, int iters, uint32_t* sink, double* ops_out, void* stream);

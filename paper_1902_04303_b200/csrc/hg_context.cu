@@ -132,7 +132,7 @@ extern "C" int hg_ctx_create(int log_n, int device, hg_ctx** out) {
         hg_ctx_destroy(ctx);
         return hg_fail(HG_ECUDA, std::string("context upload: ") + cudaGetErrorString(e));
     }
-    if (const char* v = getenv("HG_NTT_CLUSTER")) ctx->ntt_cluster = v[0] == '1';
+    if (const char* v = getenv("HG_NTT_CLUSTER")) ctx->ntt_cluster = (v[0] == '1' || v[0] == '2') ? v[0] - '0' : 0;
     *out = ctx;
     return HG_OK;
 }

@@ -100,7 +100,7 @@ struct hg_ctx {
     // log_n = 17 cluster NTT: lane-transposed round-B twiddles (hg_ntt_cluster.cu), lazily built
     uint2* d_twc_fwd = nullptr;
     uint2* d_twc_inv = nullptr;
-    int ntt_cluster = 0;   // use the cluster kernels where they apply (hg_set_ntt_variant; env HG_NTT_CLUSTER=1)
+    int ntt_cluster = 0;   // NTT kernel variant (hg_set_ntt_variant; env HG_NTT_CLUSTER=0/1/2)
     uint32_t* d_modup_frag = nullptr;   // ModUp-on-tensor-cores B fragments (hg_modup_mma.cu)
     uint8_t* d_modup_umma = nullptr;    // ModUp tcgen05 B smem images (hg_modup_umma.cu)
     int modup_frag_ks = 0;

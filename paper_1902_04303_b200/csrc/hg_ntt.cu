@@ -257,6 +257,23 @@ __device__ __forceinline__ void lo_round(uint32_t (&x)[RB][8], uint32_t* __restr
     }
 }
 
+// Contiguous stages on chunk `chunk` (2^K2 words) of RB rows of one prime; K2/3 rounds, 2^K2 / 8
+// threads.  Leaves sm free (its last shared-memory round is followed by a barrier).
+template <bool FWD, int K2, int RB>
+__device__ __forceinline__ void lo_chunk(uint32_t* __restrict__ rowp0, size_t rstride, int chunk,
+                                         int k1, uint32_t* __restrict__ sm,
+                                         const uint2* __restrict__ twp, uint32_t p) {
+    uint32_t* rowp = rowp0 + ((size_t)chunk << K2);
+    const int G = (1 << k1) + chunk;
+    const int t = threadIdx.x;
+    uint32_t x[RB][8];
+    constexpr int NR = (K2 + 2) / 3;
+    lo_round<FWD, K2, 0, RB>(x, rowp, rstride, sm, G, t, twp, p);
+    if (NR > 1) lo_round<FWD, K2, (NR > 1 ? 1 : 0), RB>(x, rowp, rstride, sm, G, t, twp, p);
+    if (NR > 2) lo_round<FWD, K2, (NR > 2 ? 2 : 0), RB>(x, rowp, rstride, sm, G, t, twp, p);
+    if (NR > 3) lo_round<FWD, K2, (NR > 3 ? 3 : 0), RB>(x, rowp, rstride, sm, G, t, twp, p);
+}
+
 // Contiguous stages: chunk of 2^K2 words, K2/3 rounds; block = 2^K2 / 8 threads.
 // grid = (N >> K2 chunks, batch-row groups of RB, primes): prime-major scheduling keeps the
 // prime's twiddles in L2 while its batch rows pass.
@@ -267,44 +284,25 @@ __global__ void __launch_bounds__(256, HG_LO_MINB) ntt_lo8_kernel(uint32_t* __re
                                                       const uint2* __restrict__ tw) {
     __shared__ __align__(16) uint32_t sm[RB * kSmRow];
     const int N = 1 << log_n;
-    const int k1 = log_n - K2;
     const int jp = blockIdx.z, bb = bb0 + blockIdx.y * RB;
     const int prime = prime_offset + jp;
-    const uint32_t p = pinfo[prime].p;
-    const uint2* twp = tw + (size_t)prime * N;
-    const size_t rstride = (size_t)P * N;
-    uint32_t* rowp = data + ((size_t)bb * P + jp) * N + ((size_t)blockIdx.x << K2);
-    const int G = (1 << k1) + blockIdx.x;
-    const int t = threadIdx.x;
-    uint32_t x[RB][8];
-    constexpr int NR = (K2 + 2) / 3;
-    lo_round<FWD, K2, 0, RB>(x, rowp, rstride, sm, G, t, twp, p);
-    if (NR > 1) lo_round<FWD, K2, (NR > 1 ? 1 : 0), RB>(x, rowp, rstride, sm, G, t, twp, p);
-    if (NR > 2) lo_round<FWD, K2, (NR > 2 ? 2 : 0), RB>(x, rowp, rstride, sm, G, t, twp, p);
-    if (NR > 3) lo_round<FWD, K2, (NR > 3 ? 3 : 0), RB>(x, rowp, rstride, sm, G, t, twp, p);
+    lo_chunk<FWD, K2, RB>(data + ((size_t)bb * P + jp) * N, (size_t)P * N, blockIdx.x, log_n - K2, sm,
+                          tw + (size_t)prime * N, pinfo[prime].p);
 }
 
-// Strided stages [0, K1), K1 in {3, 6}: tile of 2^K1 rows (stride 2^k2) x (2048 >> K1)
-// columns; thread = (column c, row group g) holding 8 rows.  K1 = 3 needs no shared memory.
-// K2 = log_n - K1 as a template parameter: every row / column offset is a compile-time
-// immediate (fewer address instructions per butterfly in this memory-heavy pass)
+// Strided stages [0, K1), K1 in {3, 6}: tile `tile` of 2^K1 rows (stride 2^k2) x (2048 >> K1)
+// columns of RB rows (rows rowp0 + r rstride); thread = (column c, row group g) holding 8 rows.
+// K1 = 3 needs no shared memory.  K2 = log_n - K1 as a template parameter: every row / column
+// offset is a compile-time immediate (fewer address instructions per butterfly in this
+// memory-heavy pass).  Ends with a barrier when it used sm (K1 = 6).
 template <bool FWD, int K1, int RB, int K2>
-__global__ void __launch_bounds__(256, HG_HI_MINB) ntt_hi8_kernel(uint32_t* __restrict__ data, int log_n,
-                                                      int P, int bb0, int prime_offset,
-                                                      const PrimeInfo* __restrict__ pinfo,
-                                                      const uint2* __restrict__ tw) {
-    __shared__ uint32_t sm[K1 > 3 ? RB * kTile : 1];
+__device__ __forceinline__ void hi_tile(uint32_t* __restrict__ rowp0, size_t rstride, int tile,
+                                        uint32_t* __restrict__ sm, const uint2* __restrict__ twp,
+                                        uint32_t p) {
     constexpr int TC = kTile >> K1;
-    constexpr int N = 1 << (K1 + K2);
     constexpr int k2 = K2;
-    (void)log_n;
-    const int jp = blockIdx.z, bb = bb0 + blockIdx.y * RB;
-    const int prime = prime_offset + jp;
-    const uint32_t p = pinfo[prime].p;
-    const uint2* twp = tw + (size_t)prime * N;
-    const size_t rstride = (size_t)P * N;
     const int c = threadIdx.x % TC, g = threadIdx.x / TC;
-    uint32_t* colp = data + ((size_t)bb * P + jp) * N + blockIdx.x * TC + c;
+    uint32_t* colp = rowp0 + tile * TC + c;
     uint32_t x[RB][8];
     if (K1 == 3) {
 #pragma unroll
@@ -348,7 +346,22 @@ __global__ void __launch_bounds__(256, HG_HI_MINB) ntt_hi8_kernel(uint32_t* __re
         for (int r = 0; r < RB; ++r)
 #pragma unroll
             for (int m = 0; m < 8; ++m) pb[r][(m << BB) << k2] = x[r][m];
+        __syncthreads();
     }
+}
+
+template <bool FWD, int K1, int RB, int K2>
+__global__ void __launch_bounds__(256, HG_HI_MINB) ntt_hi8_kernel(uint32_t* __restrict__ data, int log_n,
+                                                      int P, int bb0, int prime_offset,
+                                                      const PrimeInfo* __restrict__ pinfo,
+                                                      const uint2* __restrict__ tw) {
+    __shared__ uint32_t sm[K1 > 3 ? RB * kTile : 1];
+    constexpr int N = 1 << (K1 + K2);
+    (void)log_n;
+    const int jp = blockIdx.z, bb = bb0 + blockIdx.y * RB;
+    const int prime = prime_offset + jp;
+    hi_tile<FWD, K1, RB, K2>(data + ((size_t)bb * P + jp) * N, (size_t)P * N, blockIdx.x, sm,
+                             tw + (size_t)prime * N, pinfo[prime].p);
 }
 
 // Inverse contiguous pass with the NTT-domain product fused into its first round (which is
@@ -367,23 +380,14 @@ struct PreRows { static constexpr int value = PRE == 1 ? 2 : (PRE == 2 ? 3 : 1);
 // key switches with one key, or one ciphertext times several plaintexts; PRE 5: several
 // polynomials times one plaintext): in0 advances by bstride_in words, out by bstride_out
 template <int K2, int PRE>
-__global__ void __launch_bounds__(256, HG_FUSED_MINB) intt_lo8_fused_kernel(
-    uint32_t* out, const uint32_t* in0, const uint32_t* in1, const uint32_t* in2,
-    const uint32_t* in3, int log_n, int P, const PrimeInfo* __restrict__ pinfo,
-    const uint2* __restrict__ tw, size_t bstride_in, size_t bstride_out) {
-    out += blockIdx.y * bstride_out;
-    in0 += blockIdx.y * bstride_in;
+__device__ __forceinline__ void lo_fused_chunk(uint32_t* out, const uint32_t* in0, const uint32_t* in1,
+                                               const uint32_t* in2, const uint32_t* in3, size_t rstride,
+                                               size_t roff0, int chunk, int k1, const PrimeInfo& pi,
+                                               uint32_t* __restrict__ sm, const uint2* __restrict__ twp) {
     constexpr int RB = PreRows<PRE>::value;
-    __shared__ __align__(16) uint32_t sm[RB * kSmRow];
-    const int N = 1 << log_n;
-    const int k1 = log_n - K2;
-    const int jp = blockIdx.z;
-    const PrimeInfo pi = pinfo[jp];
     const uint32_t p = pi.p, p2 = p << 1;
-    const uint2* twp = tw + (size_t)jp * N;
-    const size_t rstride = (size_t)P * N;
-    const size_t roff = (size_t)jp * N + ((size_t)blockIdx.x << K2);
-    const int G = (1 << k1) + blockIdx.x;
+    const size_t roff = roff0 + ((size_t)chunk << K2);
+    const int G = (1 << k1) + chunk;
     const int t = threadIdx.x;
     const int base = t << 3;     // round 0 of the inverse pass has B = 0
     uint32_t x[RB][8];
@@ -420,6 +424,150 @@ __global__ void __launch_bounds__(256, HG_FUSED_MINB) intt_lo8_fused_kernel(
     if (NR > 1) lo_round<false, K2, (NR > 1 ? 1 : 0), RB>(x, rowp, rstride, sm, G, t, twp, p);
     if (NR > 2) lo_round<false, K2, (NR > 2 ? 2 : 0), RB>(x, rowp, rstride, sm, G, t, twp, p);
     if (NR > 3) lo_round<false, K2, (NR > 3 ? 3 : 0), RB>(x, rowp, rstride, sm, G, t, twp, p);
+}
+
+template <int K2, int PRE>
+__global__ void __launch_bounds__(256, HG_FUSED_MINB) intt_lo8_fused_kernel(
+    uint32_t* out, const uint32_t* in0, const uint32_t* in1, const uint32_t* in2,
+    const uint32_t* in3, int log_n, int P, const PrimeInfo* __restrict__ pinfo,
+    const uint2* __restrict__ tw, size_t bstride_in, size_t bstride_out) {
+    out += blockIdx.y * bstride_out;
+    in0 += blockIdx.y * bstride_in;
+    constexpr int RB = PreRows<PRE>::value;
+    __shared__ __align__(16) uint32_t sm[RB * kSmRow];
+    const int N = 1 << log_n;
+    const int jp = blockIdx.z;
+    const PrimeInfo pi = pinfo[jp];
+    lo_fused_chunk<K2, PRE>(out, in0, in1, in2, in3, (size_t)P * N, (size_t)jp * N, blockIdx.x,
+                            log_n - K2, pi, sm, tw + (size_t)jp * N);
+}
+
+// ---- one-launch transforms on 8-CTA clusters, the intermediate through L2 ----------------------
+// The two passes of a transform (strided tiles, contiguous chunks) run in ONE launch: the 8 CTAs
+// of a cluster own RB transforms of one prime; CTA k runs the strided stages of tiles
+// [k T/8, (k+1) T/8) (forward) with the code of the two-pass kernels, one cluster barrier
+// (release / acquire: every CTA's stores are visible to the others, L1 invalidated), then the
+// contiguous stages of chunks [8k, 8k+8) -- the inverse in the opposite order, with the NTT-domain
+// product fused into its first phase.  The intermediate is written and re-read within a few
+// microseconds, so it stays in L2: one HBM round trip per transform instead of two, while every
+// CTA keeps the low register count (and 3 CTAs per SM) of the tile kernels.  Measured slower than
+// the two passes (tools/ntt_bench.py, 656 rows: forward 0.584 vs 0.511 us per row, inverse 0.548
+// vs 0.490; batch step 244 vs 223 ms): the barrier holds each CTA until its cluster's slowest
+// member has finished the first phase.  Opt-in (hg_set_ntt_variant(ctx, 2)), log_n = 17 only
+// (256 threads per 2048-word chunk).
+#ifndef HG_CL_MINB
+#define HG_CL_MINB 3
+#endif
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+template <bool FWD, int RB, int K2>
+__global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(256, HG_CL_MINB)
+ntt_c8l2_kernel(uint32_t* __restrict__ data, int P, int bb0, int prime_offset,
+                const PrimeInfo* __restrict__ pinfo, const uint2* __restrict__ tw) {
+    __shared__ __align__(16) uint32_t sm[RB * kSmRow];
+    constexpr int K1 = 6, N = 1 << (K1 + K2);
+    constexpr int TPC = (N / kTile) / 8;   // strided tiles per CTA
+    constexpr int CPC = (1 << K1) / 8;     // contiguous chunks per CTA
+    const int k = blockIdx.x;
+    const int jp = blockIdx.z, bb = bb0 + blockIdx.y * RB;
+    const int prime = prime_offset + jp;
+    const uint32_t p = pinfo[prime].p;
+    const uint2* twp = tw + (size_t)prime * N;
+    uint32_t* rowp0 = data + ((size_t)bb * P + jp) * N;
+    const size_t rs = (size_t)P * N;
+    if (FWD) {
+#pragma unroll 1
+        for (int i = 0; i < TPC; ++i) hi_tile<true, K1, RB, K2>(rowp0, rs, k * TPC + i, sm, twp, p);
+        cluster_sync_all();
+#pragma unroll 1
+        for (int i = 0; i < CPC; ++i) {
+            lo_chunk<true, K2, RB>(rowp0, rs, k * CPC + i, K1, sm, twp, p);
+            __syncthreads();
+        }
+    } else {
+#pragma unroll 1
+        for (int i = 0; i < CPC; ++i) {
+            lo_chunk<false, K2, RB>(rowp0, rs, k * CPC + i, K1, sm, twp, p);
+            __syncthreads();
+        }
+        cluster_sync_all();
+#pragma unroll 1
+        for (int i = 0; i < TPC; ++i) hi_tile<false, K1, RB, K2>(rowp0, rs, k * TPC + i, sm, twp, p);
+    }
+}
+
+template <int K2, int PRE>
+__global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(256, HG_CL_MINB)
+intt_fused_c8l2_kernel(uint32_t* out, const uint32_t* in0, const uint32_t* in1, const uint32_t* in2,
+                       const uint32_t* in3, int P, const PrimeInfo* __restrict__ pinfo,
+                       const uint2* __restrict__ tw, size_t bstride_in, size_t bstride_out) {
+    constexpr int RB = PreRows<PRE>::value;
+    __shared__ __align__(16) uint32_t sm[RB * kSmRow];
+    constexpr int K1 = 6, N = 1 << (K1 + K2);
+    constexpr int TPC = (N / kTile) / 8;
+    constexpr int CPC = (1 << K1) / 8;
+    out += blockIdx.y * bstride_out;
+    in0 += blockIdx.y * bstride_in;
+    const int k = blockIdx.x, jp = blockIdx.z;
+    const PrimeInfo pi = pinfo[jp];
+    const uint2* twp = tw + (size_t)jp * N;
+    const size_t rs = (size_t)P * N;
+#pragma unroll 1
+    for (int i = 0; i < CPC; ++i) {
+        lo_fused_chunk<K2, PRE>(out, in0, in1, in2, in3, rs, (size_t)jp * N, k * CPC + i, K1, pi, sm, twp);
+        __syncthreads();
+    }
+    cluster_sync_all();
+#pragma unroll 1
+    for (int i = 0; i < TPC; ++i) hi_tile<false, K1, RB, K2>(out + (size_t)jp * N, rs, k * TPC + i, sm, twp, pi.p);
+}
+
+template <bool FWD, int RB>
+int launch_c8l2(int log_n, dim3 grid, cudaStream_t st, uint32_t* data, int P, int bb0, int off,
+                const PrimeInfo* pinfo, const uint2* tw) {
+    switch (log_n) {
+        case 15: ntt_c8l2_kernel<FWD, RB, 9><<<grid, 256, 0, st>>>(data, P, bb0, off, pinfo, tw); return 0;
+        case 16: ntt_c8l2_kernel<FWD, RB, 10><<<grid, 256, 0, st>>>(data, P, bb0, off, pinfo, tw); return 0;
+        case 17: ntt_c8l2_kernel<FWD, RB, 11><<<grid, 256, 0, st>>>(data, P, bb0, off, pinfo, tw); return 0;
+    }
+    return -1;
+}
+
+template <int PRE>
+int launch_fused_c8l2(int log_n, dim3 grid, cudaStream_t st, uint32_t* out, const uint32_t* i0,
+                      const uint32_t* i1, const uint32_t* i2, const uint32_t* i3, int P,
+                      const PrimeInfo* pinfo, const uint2* tw, size_t bsi, size_t bso) {
+    switch (log_n) {
+        case 15: intt_fused_c8l2_kernel<9, PRE><<<grid, 256, 0, st>>>(out, i0, i1, i2, i3, P, pinfo, tw, bsi, bso); return 0;
+        case 16: intt_fused_c8l2_kernel<10, PRE><<<grid, 256, 0, st>>>(out, i0, i1, i2, i3, P, pinfo, tw, bsi, bso); return 0;
+        case 17: intt_fused_c8l2_kernel<11, PRE><<<grid, 256, 0, st>>>(out, i0, i1, i2, i3, P, pinfo, tw, bsi, bso); return 0;
+    }
+    return -1;
+}
+
+// both passes of a transform over all rows in one cluster launch (groups of 2 batch rows, 3 for an
+// odd count, 1 if B == 1), as ntt_pass groups them
+template <bool FWD>
+int ntt_c8l2(hg_ctx* ctx, uint32_t* data, int B, int P, int off, const uint2* tw, cudaStream_t st) {
+    auto run = [&](int rb, int groups, int bb0) {
+        const dim3 g(8, groups, P);
+        int rc = rb == 1 ? launch_c8l2<FWD, 1>(ctx->log_n, g, st, data, P, bb0, off, ctx->d_pinfo, tw)
+               : rb == 2 ? launch_c8l2<FWD, 2>(ctx->log_n, g, st, data, P, bb0, off, ctx->d_pinfo, tw)
+                         : launch_c8l2<FWD, 3>(ctx->log_n, g, st, data, P, bb0, off, ctx->d_pinfo, tw);
+        if (rc) return hg_fail(HG_EINVAL, "cluster NTT: unsupported size");
+        HG_LAUNCH_CHECK(ctx);
+        return HG_OK;
+    };
+    int rc;
+    if (B == 1) return run(1, 1, 0);
+    const int odd = B & 1;
+    const int pairs = (B - 3 * odd) / 2;
+    if (pairs > 0 && (rc = run(2, pairs, 0))) return rc;
+    if (odd && (rc = run(3, 1, 2 * pairs))) return rc;
+    return HG_OK;
 }
 
 template <int PRE>
@@ -517,6 +665,9 @@ int hg_ntt_launch(hg_ctx* ctx, uint32_t* data, int rows, int P, int prime_offset
         const int k1 = log_n <= 11 ? 0 : (log_n <= 14 ? 3 : 6);
         const int k2 = log_n - k1;
         const int B = rows / P;
+        if (ctx->ntt_cluster == 2 && log_n == 17)   // 256 threads per 2048-word chunk and per tile
+            return forward ? ntt_c8l2<true>(ctx, data, B, P, prime_offset, tw, stream)
+                           : ntt_c8l2<false>(ctx, data, B, P, prime_offset, tw, stream);
         if (forward) {
             if (k1 && (rc = ntt_pass<true>(ctx, true, k1, k2, data, B, P, prime_offset, tw, stream))) return rc;
             if ((rc = ntt_pass<true>(ctx, false, k1, k2, data, B, P, prime_offset, tw, stream))) return rc;
@@ -569,8 +720,17 @@ int hg_intt_fused(hg_ctx* ctx, int pre, uint32_t* out, const uint32_t* i0, const
     if (hg_ntt_cluster_ok(ctx, P)) return hg_intt_fused_cluster(ctx, pre, out, i0, i1, i2, i3, P, st, batch);
     HgTimed tm(ctx, st, HG_K_NTT, (double)batch * rb * P * (N / 2) * log_n);
     // batch > 1 (key switch only): input g's x rows at i0 + g P N, its two outputs at out + g 2 P N
-    const dim3 g(N >> k2, batch, P);
     const size_t bsi = (size_t)P * N, bso = (size_t)rb * P * N;
+    if (ctx->ntt_cluster == 2 && log_n == 17) {
+        const dim3 gc(8, batch, P);
+        if (pre == 1) launch_fused_c8l2<1>(log_n, gc, st, out, i0, i1, i2, i3, P, ctx->d_pinfo, ctx->d_tw_inv, bsi, bso);
+        else if (pre == 2) launch_fused_c8l2<2>(log_n, gc, st, out, i0, i1, i2, i3, P, ctx->d_pinfo, ctx->d_tw_inv, bsi, bso);
+        else if (pre == 5) launch_fused_c8l2<5>(log_n, gc, st, out, i0, i1, i2, i3, P, ctx->d_pinfo, ctx->d_tw_inv, bsi, bso);
+        else launch_fused_c8l2<3>(log_n, gc, st, out, i0, i1, i2, i3, P, ctx->d_pinfo, ctx->d_tw_inv, bsi, bso);
+        HG_LAUNCH_CHECK(ctx);
+        return HG_OK;
+    }
+    const dim3 g(N >> k2, batch, P);
     if (pre == 1) launch_fused_lo8<1>(k2, g, st, out, i0, i1, i2, i3, log_n, P, ctx->d_pinfo, ctx->d_tw_inv, bsi, bso);
     else if (pre == 2) launch_fused_lo8<2>(k2, g, st, out, i0, i1, i2, i3, log_n, P, ctx->d_pinfo, ctx->d_tw_inv);
     else if (pre == 5) launch_fused_lo8<5>(k2, g, st, out, i0, i1, i2, i3, log_n, P, ctx->d_pinfo, ctx->d_tw_inv, bsi, bso);

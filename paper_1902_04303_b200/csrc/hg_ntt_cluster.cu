@@ -399,14 +399,16 @@ int ensure_twc(hg_ctx* ctx) {
 }  // namespace
 
 bool hg_ntt_cluster_ok(const hg_ctx* ctx, int P) {
-    return ctx->log_n == 17 && P <= 65535 && ctx->ntt_cluster;
+    return ctx->log_n == 17 && P <= 65535 && ctx->ntt_cluster == 1;
 }
 
-// 1: length-2^17 transforms on 8-CTA clusters; 0: the two-pass kernels of hg_ntt.cu (default:
-// measured faster, see the header).  Both give the same words (same butterflies, same order).
-extern "C" int hg_set_ntt_variant(hg_ctx* ctx, int cluster) {
+// NTT variant: 0 = the two-pass kernels of hg_ntt.cu, 1 = this file's DSMEM cluster kernels
+// (log_n = 17), 2 = hg_ntt.cu's one-launch cluster kernels with the intermediate through L2
+// (log_n = 17).  All give the same words (same butterflies, same order, same lazy ranges).
+extern "C" int hg_set_ntt_variant(hg_ctx* ctx, int variant) {
     if (!ctx) return hg_fail(HG_EINVAL, "hg_set_ntt_variant: null context");
-    ctx->ntt_cluster = cluster ? 1 : 0;
+    if (variant < 0 || variant > 2) return hg_fail(HG_EINVAL, "hg_set_ntt_variant: variant must be 0, 1 or 2");
+    ctx->ntt_cluster = variant;
     return HG_OK;
 }
 

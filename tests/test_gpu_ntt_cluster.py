@@ -1,6 +1,8 @@
-"""The length-2^17 cluster NTT (csrc/hg_ntt_cluster.cu: one HBM round trip per transform, 8-CTA
-clusters exchanging the transform once through distributed shared memory) against the two-pass
-kernels of csrc/hg_ntt.cu, word for word (same butterflies, same order, same lazy ranges):
+"""The cluster NTT variants against the two-pass kernels of csrc/hg_ntt.cu, word for word (same
+butterflies, same order, same lazy ranges): variant 1 (csrc/hg_ntt_cluster.cu, log_n 17: 8-CTA
+clusters exchanging the transform once through distributed shared memory) and variant 2
+(csrc/hg_ntt.cu ntt_c8l2 / intt_fused_c8l2, log_n 17 -- other sizes fall back to the two passes:
+both passes in one cluster launch, the intermediate through L2) --
 raw forward / inverse transforms over [B][P][N] rows with a prime offset, and every fused
 NTT-domain product of the inverse (key switch x.kb / x.ka, tensor, plain product, shared factor;
 batched and in place) through the scheme ops that use them at the parity preset P17 -- whose
@@ -12,10 +14,10 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-def _set(ctx, cluster):
+def _set(ctx, variant):
     from paper_1902_04303_b200 import _lib
 
-    _lib.check(ctx.lib.hg_set_ntt_variant(ctx.handle, 1 if cluster else 0))
+    _lib.check(ctx.lib.hg_set_ntt_variant(ctx.handle, int(variant)))
 
 
 @pytest.fixture(scope="module")
@@ -24,20 +26,21 @@ def ctx17():
 
     ctx = _lib.get_context(17)
     yield ctx
-    _set(ctx, False)
+    _set(ctx, 0)
 
 
+@pytest.mark.parametrize("variant,log_n", [(1, 17), (2, 17), (2, 16)])
 @pytest.mark.parametrize("from_end,rows", [(0, 5), (3, 9), (1, 4)])
-def test_raw_transforms_identical(ctx17, from_end, rows):
+def test_raw_transforms_identical(variant, log_n, from_end, rows):
     import torch
 
     from paper_1902_04303_b200 import _lib
 
-    ctx = ctx17
+    ctx = _lib.get_context(log_n)
     primes = ctx.primes()
     off = len(primes) - from_end if from_end else 0
     P = min(len(primes) - off, rows)
-    n = 1 << 17
+    n = 1 << log_n
     pr = torch.tensor([primes[off + i % P] for i in range(rows)], dtype=torch.int64, device="cuda")[:, None]
     gen = torch.Generator(device="cuda")
     gen.manual_seed(rows)
@@ -45,14 +48,14 @@ def test_raw_transforms_identical(ctx17, from_end, rows):
     src = data.to(torch.int32).contiguous()
     outs = {}
     for cluster in (True, False):
-        _set(ctx, cluster)
+        _set(ctx, variant if cluster else 0)
         buf = src.clone()
         _lib.check(ctx.lib.hg_ntt_forward(ctx.handle, buf.data_ptr(), rows, off, ctx.stream()))
         fwd = buf.clone()
         red = ((buf.to(torch.int64) & 0xFFFFFFFF) % pr).to(torch.int32).contiguous()
         _lib.check(ctx.lib.hg_ntt_inverse(ctx.handle, red.data_ptr(), rows, off, ctx.stream()))
         outs[cluster] = (fwd, red)
-    _set(ctx, False)
+    _set(ctx, 0)
     assert torch.equal(outs[True][0], outs[False][0]), "forward words differ"
     assert torch.equal(outs[True][1], outs[False][1]), "inverse words differ"
     got = (outs[True][1].to(torch.int64) & 0xFFFFFFFF) % pr
@@ -80,7 +83,8 @@ def _words(ct):
     return np.concatenate([ct.c0.numpy_words().ravel(), ct.c1.numpy_words().ravel()])
 
 
-def test_fused_products_identical(ctx17, p17):
+@pytest.mark.parametrize("variant", [1, 2])
+def test_fused_products_identical(ctx17, p17, variant):
     hg, params, eng, (a, b, c, z) = p17
     mask = eng.mask(("range", 0, 4096))
     ops = {
@@ -97,9 +101,9 @@ def test_fused_products_identical(ctx17, p17):
     for name, fn in ops.items():
         got = {}
         for cluster in (True, False):
-            _set(ctx17, cluster)
+            _set(ctx17, variant if cluster else 0)
             got[cluster] = [_words(ct) for ct in fn()]
-        _set(ctx17, False)
+        _set(ctx17, 0)
         assert len(got[True]) == len(got[False])
         for g, w in zip(got[True], got[False]):
             assert np.array_equal(g, w), f"{name}: cluster NTT output differs from the two-pass NTT"

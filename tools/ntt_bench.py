@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--primes", type=int, default=164)
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--ncu", action="store_true")
+    ap.add_argument("--variants", type=int, nargs="+", default=[0, 2, 0, 2])
     a = ap.parse_args()
     ctx = _lib.get_context(17)
     primes = ctx.primes()
@@ -30,13 +31,13 @@ def main():
     buf = (torch.randint(0, 1 << 62, (rows, n), dtype=torch.int64, device="cuda") % pr).to(torch.int32)
     st = ctx.stream()
     if a.ncu:
-        for v in (1, 0):
+        for v in sorted(set(a.variants)):
             _lib.check(ctx.lib.hg_set_ntt_variant(ctx.handle, v))
             _lib.check(ctx.lib.hg_ntt_forward(ctx.handle, buf.data_ptr(), rows, off, st))
             _lib.check(ctx.lib.hg_ntt_inverse(ctx.handle, buf.data_ptr(), rows, off, st))
         torch.cuda.synchronize()
         torch.cuda.cudart().cudaProfilerStart()
-        for v in (1, 0):
+        for v in sorted(set(a.variants)):
             _lib.check(ctx.lib.hg_set_ntt_variant(ctx.handle, v))
             _lib.check(ctx.lib.hg_ntt_forward(ctx.handle, buf.data_ptr(), rows, off, st))
             _lib.check(ctx.lib.hg_ntt_inverse(ctx.handle, buf.data_ptr(), rows, off, st))
@@ -44,7 +45,7 @@ def main():
         torch.cuda.cudart().cudaProfilerStop()
         return
     s = torch.cuda.current_stream()
-    for v in (0, 1, 0, 1):
+    for v in a.variants:
         _lib.check(ctx.lib.hg_set_ntt_variant(ctx.handle, v))
         res = {}
         for name, fn in (("fwd", ctx.lib.hg_ntt_forward), ("inv", ctx.lib.hg_ntt_inverse)):
