@@ -23,6 +23,9 @@ constexpr int kTile = 2048;  // words per shared-memory tile
 #ifndef HG_FUSED_MINB
 #define HG_FUSED_MINB 4   // fused inverse pass, 72 -> 64 registers, 3 -> 4 blocks: -2.7 ms of NTT
 #endif
+#ifndef HG_FUSED16_MINB
+#define HG_FUSED16_MINB 6  // radix-16 fused inverse pass (128-thread blocks): 4 -> 6 blocks per SM: -3 ms of NTT per step
+#endif
 #ifndef HG_LO_MINB
 #define HG_LO_MINB 1      // contiguous pass: 40 registers already give 6 blocks
 #endif
@@ -130,19 +133,19 @@ __global__ void __launch_bounds__(256) ntt_hi_kernel(uint32_t* __restrict__ data
 // (G = 2^k1 + chunk index for the contiguous pass, 1 for the strided pass).  A block carries
 // RB rows of the same prime (batch rows of one [B][P][N] launch): the twiddles of a stage are
 // loaded once and applied to every row, and the rows' butterflies interleave.
-template <bool FWD, int R, int B, int LS0, int RB>
-__device__ __forceinline__ void round8(uint32_t (&x)[RB][8], int G, int base,
+template <bool FWD, int R, int B, int LS0, int RB, int E = 8>
+__device__ __forceinline__ void round8(uint32_t (&x)[RB][E], int G, int base,
                                        const uint2* __restrict__ twp, uint32_t p) {
 #pragma unroll
     for (int kk = 0; kk < R; ++kk) {
         const int k = FWD ? kk : R - 1 - kk;
         const int d = 1 << (R - 1 - k);
-        // the 8 >> (R-k) twiddles of this stage are contiguous and aligned to their count:
-        // 16-byte loads
-        // unsigned 32-bit index: one shift-add into the block's table pointer (no sign extension)
+        // the E >> (R-k) twiddles of this stage are contiguous and aligned to their count:
+        // 16-byte loads.  Unsigned 32-bit index: one shift-add into the block's table pointer
         const uint2* tg = twp + (((uint32_t)G << (LS0 + k)) + ((uint32_t)base >> (B + R - k)));
-        uint2 w[4];
-        const int nt = 8 >> (R - k);
+        constexpr int kMaxT = E / 2;
+        uint2 w[kMaxT];
+        const int nt = E >> (R - k);
         if (nt == 1) {
             w[0] = __ldg(tg);
         } else {
@@ -154,7 +157,7 @@ __device__ __forceinline__ void round8(uint32_t (&x)[RB][8], int G, int base,
             }
         }
 #pragma unroll
-        for (int m = 0; m < 8; ++m) {
+        for (int m = 0; m < E; ++m) {
             if (m & d) continue;
 #pragma unroll
             for (int r = 0; r < RB; ++r) {
@@ -165,120 +168,137 @@ __device__ __forceinline__ void round8(uint32_t (&x)[RB][8], int G, int base,
     }
 }
 
-template <int B>
-__device__ __forceinline__ void load8(uint32_t (&x)[8], const uint32_t* src, int base) {
+template <int B, int E = 8>
+__device__ __forceinline__ void load8(uint32_t (&x)[E], const uint32_t* src, int base) {
     if (B == 0) {   // contiguous: 16-byte accesses
-        const uint4 a = *reinterpret_cast<const uint4*>(src + base);
-        const uint4 b = *reinterpret_cast<const uint4*>(src + base + 4);
-        x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+#pragma unroll
+        for (int v = 0; v < E / 4; ++v) {
+            const uint4 a = *reinterpret_cast<const uint4*>(src + base + 4 * v);
+            x[4 * v] = a.x; x[4 * v + 1] = a.y; x[4 * v + 2] = a.z; x[4 * v + 3] = a.w;
+        }
     } else {
 #pragma unroll
-        for (int m = 0; m < 8; ++m) x[m] = src[base + (m << B)];
+        for (int m = 0; m < E; ++m) x[m] = src[base + (m << B)];
     }
 }
-template <int B>
-__device__ __forceinline__ void store8(const uint32_t (&x)[8], uint32_t* dst, int base) {
+template <int B, int E = 8>
+__device__ __forceinline__ void store8(const uint32_t (&x)[E], uint32_t* dst, int base) {
     if (B == 0) {
-        *reinterpret_cast<uint4*>(dst + base) = make_uint4(x[0], x[1], x[2], x[3]);
-        *reinterpret_cast<uint4*>(dst + base + 4) = make_uint4(x[4], x[5], x[6], x[7]);
+#pragma unroll
+        for (int v = 0; v < E / 4; ++v)
+            *reinterpret_cast<uint4*>(dst + base + 4 * v) = make_uint4(x[4 * v], x[4 * v + 1], x[4 * v + 2], x[4 * v + 3]);
     } else {
 #pragma unroll
-        for (int m = 0; m < 8; ++m) dst[base + (m << B)] = x[m];
+        for (int m = 0; m < E; ++m) dst[base + (m << B)] = x[m];
     }
 }
 
-// Shared-memory rows are padded: word i of a 2048-word row sits at pad(i) = i + 4 (i >> 5) (four
-// spare words after every 32), which keeps every round's access pattern free of bank conflicts
-// and -- unlike an XOR swizzle -- lets a thread's 8 words be one base address plus compile-time
-// offsets: for B >= 5 the 8 words lie in different 32-word blocks (offset m 2^B + m 2^(B-3)),
-// for B <= 2 in the thread's own block (base mod 32 + 7 2^B < 32: offset m 2^B)
-__device__ __forceinline__ int pad(int i) { return i + ((i >> 5) << 2); }
+// Shared-memory rows are padded: word i of a 2048-word row sits at
+//     pad(i) = i + 4 (i >> 5) + 8 (i >> 7)
+// (four spare words after every 32, eight more after every 128), which keeps every round's
+// access pattern -- radix-8 and radix-16, every stride 2^B -- free of bank conflicts and, unlike
+// an XOR swizzle, makes a thread's words one base address plus compile-time offsets: a thread's
+// base has zero bits [B, B + log2 E) and its words add m 2^B, so (base mod 128) + (m 2^B mod 128)
+// never carries past bit 6 and pad(base + m 2^B) = pad(base) + pad(m 2^B).
+__device__ __forceinline__ int pad(int i) { return i + ((i >> 5) << 2) + ((i >> 7) << 3); }
 template <int B>
-__device__ __forceinline__ int pad_off(int pb, int base, int m) {
-    if constexpr (B >= 5) return pb + (m << B) + (m << (B - 3));
-    else if constexpr (B <= 2) return pb + (m << B);
-    else return pad(base + (m << B));
+__device__ __forceinline__ constexpr int pad_c(int m) {
+    return (m << B) + (((m << B) >> 5) << 2) + (((m << B) >> 7) << 3);
 }
-template <int B>
-__device__ __forceinline__ void sload8(uint32_t (&x)[8], const uint32_t* s, int base) {
-    const int pb = pad(base);
-    if (B == 0) {   // 8 words inside one 32-word block: 16-byte accesses
-        const uint4 a = *reinterpret_cast<const uint4*>(s + pb);
-        const uint4 b = *reinterpret_cast<const uint4*>(s + pb + 4);
-        x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+template <int B, int E = 8>
+__device__ __forceinline__ void sload8(uint32_t (&x)[E], const uint32_t* s, int base) {
+    const uint32_t* sb = s + pad(base);
+    if (B == 0) {   // E words inside one 32-word block: 16-byte accesses
+#pragma unroll
+        for (int v = 0; v < E / 4; ++v) {
+            const uint4 a = *reinterpret_cast<const uint4*>(sb + 4 * v);
+            x[4 * v] = a.x; x[4 * v + 1] = a.y; x[4 * v + 2] = a.z; x[4 * v + 3] = a.w;
+        }
     } else {
 #pragma unroll
-        for (int m = 0; m < 8; ++m) x[m] = s[pad_off<B>(pb, base, m)];
+        for (int m = 0; m < E; ++m) x[m] = sb[pad_c<B>(m)];
     }
 }
-template <int B>
-__device__ __forceinline__ void sstore8(const uint32_t (&x)[8], uint32_t* s, int base) {
-    const int pb = pad(base);
+template <int B, int E = 8>
+__device__ __forceinline__ void sstore8(const uint32_t (&x)[E], uint32_t* s, int base) {
+    uint32_t* sb = s + pad(base);
     if (B == 0) {
-        *reinterpret_cast<uint4*>(s + pb) = make_uint4(x[0], x[1], x[2], x[3]);
-        *reinterpret_cast<uint4*>(s + pb + 4) = make_uint4(x[4], x[5], x[6], x[7]);
+#pragma unroll
+        for (int v = 0; v < E / 4; ++v)
+            *reinterpret_cast<uint4*>(sb + 4 * v) = make_uint4(x[4 * v], x[4 * v + 1], x[4 * v + 2], x[4 * v + 3]);
     } else {
 #pragma unroll
-        for (int m = 0; m < 8; ++m) s[pad_off<B>(pb, base, m)] = x[m];
+        for (int m = 0; m < E; ++m) sb[pad_c<B>(m)] = x[m];
     }
 }
 
-constexpr int kSmRow = kTile + kTile / 8;   // padded row (2304 words)
+constexpr int kSmRow = kTile + kTile / 8 + kTile / 16;   // padded row (2432 words)
 
-template <bool FWD, int K2, int ROUND, int RB, bool PRELOADED = false>
-__device__ __forceinline__ void lo_round(uint32_t (&x)[RB][8], uint32_t* __restrict__ rowp,
+// Words per thread of the contiguous passes: radix-16 rounds (4 stages per shared-memory
+// exchange, 2^K2 / 16 threads per chunk) from K2 = 8 up, radix 8 below (HG_NTT_E=8 forces 8)
+#ifndef HG_NTT_E
+#define HG_NTT_E 16
+#endif
+template <int K2>
+struct LoE { static constexpr int value = (HG_NTT_E == 16 && K2 >= 10) ? 16 : 8; };
+template <int K2>
+struct LoThreads { static constexpr int value = (1 << K2) / LoE<K2>::value; };
+
+template <bool FWD, int K2, int ROUND, int RB, bool PRELOADED = false, int E = LoE<K2>::value>
+__device__ __forceinline__ void lo_round(uint32_t (&x)[RB][E], uint32_t* __restrict__ rowp,
                                          size_t rstride, uint32_t* __restrict__ sm, int G, int t,
                                          const uint2* __restrict__ twp, uint32_t p) {
-    constexpr int NR = (K2 + 2) / 3;
-    constexpr int R_IDX = FWD ? ROUND : NR - 1 - ROUND;   // which stage triple
-    constexpr int LS0 = 3 * R_IDX;
-    constexpr int R = (K2 - LS0) < 3 ? (K2 - LS0) : 3;
+    constexpr int LE = E == 16 ? 4 : 3;                    // stages per full round
+    constexpr int NR = (K2 + LE - 1) / LE;
+    constexpr int R_IDX = FWD ? ROUND : NR - 1 - ROUND;   // which stage group
+    constexpr int LS0 = LE * R_IDX;
+    constexpr int R = (K2 - LS0) < LE ? (K2 - LS0) : LE;  // a short round is the last (B = 0)
     constexpr int B = K2 - LS0 - R;
-    const int base = ((t >> B) << (B + 3)) | (t & ((1 << B) - 1));
+    const int base = ((t >> B) << (B + LE)) | (t & ((1 << B) - 1));
 #pragma unroll
     for (int r = 0; r < RB; ++r) {
         if (ROUND == 0) {
-            if (!PRELOADED) load8<B>(x[r], rowp + r * rstride, base);
+            if (!PRELOADED) load8<B, E>(x[r], rowp + r * rstride, base);
         } else {
-            sload8<B>(x[r], sm + r * kSmRow, base);
+            sload8<B, E>(x[r], sm + r * kSmRow, base);
         }
     }
     // one buffer, updated in place: a round reads and writes the same words of each row (its
     // thread -> word map partitions the row), so one barrier per round orders it after the
     // previous round's writes
-    round8<FWD, R, B, LS0, RB>(x, G, base, twp, p);
+    round8<FWD, R, B, LS0, RB, E>(x, G, base, twp, p);
     if (ROUND == NR - 1) {
 #pragma unroll
-        for (int r = 0; r < RB; ++r) store8<B>(x[r], rowp + r * rstride, base);
+        for (int r = 0; r < RB; ++r) store8<B, E>(x[r], rowp + r * rstride, base);
     } else {
 #pragma unroll
-        for (int r = 0; r < RB; ++r) sstore8<B>(x[r], sm + r * kSmRow, base);
+        for (int r = 0; r < RB; ++r) sstore8<B, E>(x[r], sm + r * kSmRow, base);
         __syncthreads();
     }
 }
 
 // Contiguous stages on chunk `chunk` (2^K2 words) of RB rows of one prime; K2/3 rounds, 2^K2 / 8
 // threads.  Leaves sm free (its last shared-memory round is followed by a barrier).
-template <bool FWD, int K2, int RB>
+template <bool FWD, int K2, int RB, int E = LoE<K2>::value>
 __device__ __forceinline__ void lo_chunk(uint32_t* __restrict__ rowp0, size_t rstride, int chunk,
                                          int k1, uint32_t* __restrict__ sm,
                                          const uint2* __restrict__ twp, uint32_t p) {
     uint32_t* rowp = rowp0 + ((size_t)chunk << K2);
     const int G = (1 << k1) + chunk;
     const int t = threadIdx.x;
-    uint32_t x[RB][8];
-    constexpr int NR = (K2 + 2) / 3;
-    lo_round<FWD, K2, 0, RB>(x, rowp, rstride, sm, G, t, twp, p);
-    if (NR > 1) lo_round<FWD, K2, (NR > 1 ? 1 : 0), RB>(x, rowp, rstride, sm, G, t, twp, p);
-    if (NR > 2) lo_round<FWD, K2, (NR > 2 ? 2 : 0), RB>(x, rowp, rstride, sm, G, t, twp, p);
-    if (NR > 3) lo_round<FWD, K2, (NR > 3 ? 3 : 0), RB>(x, rowp, rstride, sm, G, t, twp, p);
+    uint32_t x[RB][E];
+    constexpr int NR = (K2 + (E == 16 ? 3 : 2)) / (E == 16 ? 4 : 3);
+    lo_round<FWD, K2, 0, RB, false, E>(x, rowp, rstride, sm, G, t, twp, p);
+    if (NR > 1) lo_round<FWD, K2, (NR > 1 ? 1 : 0), RB, false, E>(x, rowp, rstride, sm, G, t, twp, p);
+    if (NR > 2) lo_round<FWD, K2, (NR > 2 ? 2 : 0), RB, false, E>(x, rowp, rstride, sm, G, t, twp, p);
+    if (NR > 3) lo_round<FWD, K2, (NR > 3 ? 3 : 0), RB, false, E>(x, rowp, rstride, sm, G, t, twp, p);
 }
 
 // Contiguous stages: chunk of 2^K2 words, K2/3 rounds; block = 2^K2 / 8 threads.
 // grid = (N >> K2 chunks, batch-row groups of RB, primes): prime-major scheduling keeps the
 // prime's twiddles in L2 while its batch rows pass.
 template <bool FWD, int K2, int RB>
-__global__ void __launch_bounds__(256, HG_LO_MINB) ntt_lo8_kernel(uint32_t* __restrict__ data, int log_n,
+__global__ void __launch_bounds__(LoThreads<K2>::value, HG_LO_MINB * (LoE<K2>::value / 8)) ntt_lo8_kernel(uint32_t* __restrict__ data, int log_n,
                                                       int P, int bb0, int prime_offset,
                                                       const PrimeInfo* __restrict__ pinfo,
                                                       const uint2* __restrict__ tw) {
@@ -379,7 +399,7 @@ struct PreRows { static constexpr int value = PRE == 1 ? 2 : (PRE == 2 ? 3 : 1);
 // blockIdx.y selects one of a batch of independent products sharing in1..in3 (PRE 1: several
 // key switches with one key, or one ciphertext times several plaintexts; PRE 5: several
 // polynomials times one plaintext): in0 advances by bstride_in words, out by bstride_out
-template <int K2, int PRE>
+template <int K2, int PRE, int E = LoE<K2>::value>
 __device__ __forceinline__ void lo_fused_chunk(uint32_t* out, const uint32_t* in0, const uint32_t* in1,
                                                const uint32_t* in2, const uint32_t* in3, size_t rstride,
                                                size_t roff0, int chunk, int k1, const PrimeInfo& pi,
@@ -389,16 +409,16 @@ __device__ __forceinline__ void lo_fused_chunk(uint32_t* out, const uint32_t* in
     const size_t roff = roff0 + ((size_t)chunk << K2);
     const int G = (1 << k1) + chunk;
     const int t = threadIdx.x;
-    const int base = t << 3;     // round 0 of the inverse pass has B = 0
-    uint32_t x[RB][8];
+    const int base = t * E;     // round 0 of the inverse pass has B = 0
+    uint32_t x[RB][E];
     {
-        uint32_t u0[8], u1[8], u2[8], u3[8];
-        load8<0>(u0, in0 + roff, base);
-        load8<0>(u1, in1 + roff, base);
-        if (PRE != 3 && PRE != 5) load8<0>(u2, in2 + roff, base);
-        if (PRE == 2) load8<0>(u3, in3 + roff, base);
+        uint32_t u0[E], u1[E], u2[E], u3[E];
+        load8<0, E>(u0, in0 + roff, base);
+        load8<0, E>(u1, in1 + roff, base);
+        if (PRE != 3 && PRE != 5) load8<0, E>(u2, in2 + roff, base);
+        if (PRE == 2) load8<0, E>(u3, in3 + roff, base);
 #pragma unroll
-        for (int m = 0; m < 8; ++m) {
+        for (int m = 0; m < E; ++m) {
             const uint32_t a = min(u0[m], u0[m] - p2);
             if (PRE == 1) {
                 x[0][m] = mont_mul(a, u1[m], p, pi.pinv_neg);
@@ -419,15 +439,15 @@ __device__ __forceinline__ void lo_fused_chunk(uint32_t* out, const uint32_t* in
         }
     }
     uint32_t* rowp = out + roff;
-    constexpr int NR = (K2 + 2) / 3;
-    lo_round<false, K2, 0, RB, true>(x, rowp, rstride, sm, G, t, twp, p);
-    if (NR > 1) lo_round<false, K2, (NR > 1 ? 1 : 0), RB>(x, rowp, rstride, sm, G, t, twp, p);
-    if (NR > 2) lo_round<false, K2, (NR > 2 ? 2 : 0), RB>(x, rowp, rstride, sm, G, t, twp, p);
-    if (NR > 3) lo_round<false, K2, (NR > 3 ? 3 : 0), RB>(x, rowp, rstride, sm, G, t, twp, p);
+    constexpr int NR = (K2 + (E == 16 ? 3 : 2)) / (E == 16 ? 4 : 3);
+    lo_round<false, K2, 0, RB, true, E>(x, rowp, rstride, sm, G, t, twp, p);
+    if (NR > 1) lo_round<false, K2, (NR > 1 ? 1 : 0), RB, false, E>(x, rowp, rstride, sm, G, t, twp, p);
+    if (NR > 2) lo_round<false, K2, (NR > 2 ? 2 : 0), RB, false, E>(x, rowp, rstride, sm, G, t, twp, p);
+    if (NR > 3) lo_round<false, K2, (NR > 3 ? 3 : 0), RB, false, E>(x, rowp, rstride, sm, G, t, twp, p);
 }
 
 template <int K2, int PRE>
-__global__ void __launch_bounds__(256, HG_FUSED_MINB) intt_lo8_fused_kernel(
+__global__ void __launch_bounds__(LoThreads<K2>::value, LoE<K2>::value == 16 ? HG_FUSED16_MINB : HG_FUSED_MINB) intt_lo8_fused_kernel(
     uint32_t* out, const uint32_t* in0, const uint32_t* in1, const uint32_t* in2,
     const uint32_t* in3, int log_n, int P, const PrimeInfo* __restrict__ pinfo,
     const uint2* __restrict__ tw, size_t bstride_in, size_t bstride_out) {
@@ -484,13 +504,13 @@ ntt_c8l2_kernel(uint32_t* __restrict__ data, int P, int bb0, int prime_offset,
         cluster_sync_all();
 #pragma unroll 1
         for (int i = 0; i < CPC; ++i) {
-            lo_chunk<true, K2, RB>(rowp0, rs, k * CPC + i, K1, sm, twp, p);
+            lo_chunk<true, K2, RB, 8>(rowp0, rs, k * CPC + i, K1, sm, twp, p);
             __syncthreads();
         }
     } else {
 #pragma unroll 1
         for (int i = 0; i < CPC; ++i) {
-            lo_chunk<false, K2, RB>(rowp0, rs, k * CPC + i, K1, sm, twp, p);
+            lo_chunk<false, K2, RB, 8>(rowp0, rs, k * CPC + i, K1, sm, twp, p);
             __syncthreads();
         }
         cluster_sync_all();
@@ -517,7 +537,7 @@ intt_fused_c8l2_kernel(uint32_t* out, const uint32_t* in0, const uint32_t* in1, 
     const size_t rs = (size_t)P * N;
 #pragma unroll 1
     for (int i = 0; i < CPC; ++i) {
-        lo_fused_chunk<K2, PRE>(out, in0, in1, in2, in3, rs, (size_t)jp * N, k * CPC + i, K1, pi, sm, twp);
+        lo_fused_chunk<K2, PRE, 8>(out, in0, in1, in2, in3, rs, (size_t)jp * N, k * CPC + i, K1, pi, sm, twp);
         __syncthreads();
     }
     cluster_sync_all();
@@ -574,11 +594,10 @@ template <int PRE>
 int launch_fused_lo8(int k2, dim3 grid, cudaStream_t st, uint32_t* out, const uint32_t* i0,
                      const uint32_t* i1, const uint32_t* i2, const uint32_t* i3, int log_n, int P,
                      const PrimeInfo* pinfo, const uint2* tw, size_t bsi = 0, size_t bso = 0) {
-    const int threads = (1 << k2) / 8;
     switch (k2) {
 #define HG_LOF(K)                                                                               \
     case K:                                                                                     \
-        intt_lo8_fused_kernel<K, PRE><<<grid, threads, 0, st>>>(out, i0, i1, i2, i3, log_n, P,  \
+        intt_lo8_fused_kernel<K, PRE><<<grid, LoThreads<K>::value, 0, st>>>(out, i0, i1, i2, i3, log_n, P, \
                                                                 pinfo, tw, bsi, bso);           \
         return 0;
         HG_LOF(3) HG_LOF(4) HG_LOF(5) HG_LOF(6) HG_LOF(7) HG_LOF(8) HG_LOF(9) HG_LOF(10) HG_LOF(11)
@@ -590,11 +609,10 @@ int launch_fused_lo8(int k2, dim3 grid, cudaStream_t st, uint32_t* out, const ui
 template <bool FWD, int RB>
 int launch_lo8(int k2, dim3 grid, cudaStream_t st, uint32_t* data, int log_n, int P, int bb0,
                int off, const PrimeInfo* pinfo, const uint2* tw) {
-    const int threads = (1 << k2) / 8;
     switch (k2) {
 #define HG_LO(K)                                                                                     \
     case K:                                                                                          \
-        ntt_lo8_kernel<FWD, K, RB><<<grid, threads, 0, st>>>(data, log_n, P, bb0, off, pinfo, tw); \
+        ntt_lo8_kernel<FWD, K, RB><<<grid, LoThreads<K>::value, 0, st>>>(data, log_n, P, bb0, off, pinfo, tw); \
         return 0;
         HG_LO(3) HG_LO(4) HG_LO(5) HG_LO(6) HG_LO(7) HG_LO(8) HG_LO(9) HG_LO(10) HG_LO(11)
 #undef HG_LO
