@@ -27,7 +27,7 @@ constexpr int kTile = 2048;  // words per shared-memory tile
 #define HG_FUSED16_MINB 6  // radix-16 fused inverse pass (128-thread blocks): 4 -> 6 blocks per SM: -3 ms of NTT per step
 #endif
 #ifndef HG_LO_MINB
-#define HG_LO_MINB 1      // contiguous pass: 40 registers already give 6 blocks
+#define HG_LO_MINB 3      // contiguous pass (radix 16, 128-thread blocks): >= 6 blocks per SM, 80 registers
 #endif
 #ifndef HG_HI_MINB
 #define HG_HI_MINB 5      // strided pass (3-row variant 64 -> 48 registers): -15 ms of NTT
