@@ -14,7 +14,7 @@
 // a template on (k2, k1), so all index and address arithmetic is compile-time.  Rows are laid
 // out [B][P][N]; the grid walks rows prime-major so polys sharing a prime reuse its twiddles
 // from L2.
-#include "hg_internal.cuh"
+#include "hg_ntt_common.cuh"
 
 namespace {
 
@@ -33,21 +33,8 @@ constexpr int kTile = 2048;  // words per shared-memory tile
 #define HG_HI_MINB 5      // strided pass (3-row variant 64 -> 48 registers): -15 ms of NTT
 #endif
 
-__device__ __forceinline__ void fwd_bfly(uint32_t& x, uint32_t& y, uint2 w, uint32_t p) {
-    const uint32_t p2 = p << 1;
-    const uint32_t a = min(x, x - p2);   // [0, 4p) -> [0, 2p)
-    const uint32_t t = mul_shoup_lazy(y, w.x, w.y, p);
-    x = a + t;
-    y = a - t + p2;
-}
-__device__ __forceinline__ void inv_bfly(uint32_t& x, uint32_t& y, uint2 w, uint32_t p) {
-    const uint32_t p2 = p << 1;
-    uint32_t s = x + y;
-    s = min(s, s - p2);
-    const uint32_t d = x - y + p2;
-    x = s;
-    y = mul_shoup_lazy(d, w.x, w.y, p);
-}
+using hgntt::fwd_bfly;
+using hgntt::inv_bfly;
 
 // ---- v1 fallback (tiny rings / ragged row counts): radix-2 stages in shared memory -------
 template <bool FWD>
@@ -384,6 +371,45 @@ __global__ void __launch_bounds__(256, HG_HI_MINB) ntt_hi8_kernel(uint32_t* __re
                              tw + (size_t)prime * N, pinfo[prime].p);
 }
 
+// Strided stages [0, 6), register-resident: thread = one column (64 words, rows 2^K2 apart,
+// loaded / stored coalesced across the warp), all 6 stages in registers -- no shared-memory
+// exchange, no barrier, every twiddle warp-uniform (so no batch-row grouping is needed).
+#ifndef HG_HI64
+#define HG_HI64 0   // measured slower than the tiled pass (16 warps per SM at 128 registers): 152.3 vs 147.5 ms of NTT per step
+#endif
+#ifndef HG_HI64_MINB
+#define HG_HI64_MINB 2
+#endif
+template <bool FWD, int K2>
+__global__ void __launch_bounds__(256, HG_HI64_MINB) ntt_hi64_kernel(uint32_t* __restrict__ data, int P,
+                                                                  int prime_offset,
+                                                                  const PrimeInfo* __restrict__ pinfo,
+                                                                  const uint2* __restrict__ tw) {
+    constexpr int N = 1 << (6 + K2);
+    const int jp = blockIdx.z, bb = blockIdx.y;
+    const int prime = prime_offset + jp;
+    const uint32_t p = pinfo[prime].p;
+    const uint2* twp = tw + (size_t)prime * N;
+    uint32_t* col = data + ((size_t)bb * P + jp) * N + blockIdx.x * 256 + threadIdx.x;
+    uint32_t x[64];
+#pragma unroll
+    for (int r = 0; r < 64; ++r) x[r] = col[(size_t)r << K2];
+    hgntt::hi_stages<FWD>(x, twp, p);
+#pragma unroll
+    for (int r = 0; r < 64; ++r) col[(size_t)r << K2] = x[r];
+}
+
+template <bool FWD>
+int launch_hi64(int log_n, int B, int P, cudaStream_t st, uint32_t* data, int off, const PrimeInfo* pinfo,
+                const uint2* tw) {
+    switch (log_n) {
+        case 15: ntt_hi64_kernel<FWD, 9><<<dim3(2, B, P), 256, 0, st>>>(data, P, off, pinfo, tw); return 0;
+        case 16: ntt_hi64_kernel<FWD, 10><<<dim3(4, B, P), 256, 0, st>>>(data, P, off, pinfo, tw); return 0;
+        case 17: ntt_hi64_kernel<FWD, 11><<<dim3(8, B, P), 256, 0, st>>>(data, P, off, pinfo, tw); return 0;
+    }
+    return -1;
+}
+
 // Inverse contiguous pass with the NTT-domain product fused into its first round (which is
 // unit-stride: each thread's 8 words are contiguous).  The products are Montgomery products of
 // lazily reduced inputs, left in [0, 2p) (the inverse butterflies accept < 2p; the CRT reduces).
@@ -641,6 +667,13 @@ template <bool FWD>
 int ntt_pass(hg_ctx* ctx, bool hi, int k1, int k2, uint32_t* data, int B, int P, int off,
              const uint2* tw, cudaStream_t st) {
     const int log_n = ctx->log_n, N = ctx->N;
+    if (HG_HI64 && hi && k1 == 6 && B <= 65535) {
+        if (FWD ? launch_hi64<true>(log_n, B, P, st, data, off, ctx->d_pinfo, tw)
+                : launch_hi64<false>(log_n, B, P, st, data, off, ctx->d_pinfo, tw))
+            return hg_fail(HG_EINVAL, "strided NTT pass: unsupported size");
+        HG_LAUNCH_CHECK(ctx);
+        return HG_OK;
+    }
     const int gx = hi ? N / kTile : N >> k2;
     auto run = [&](int rb, int groups, int bb0) {
         const dim3 g(gx, groups, P);

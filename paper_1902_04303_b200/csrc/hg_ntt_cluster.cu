@@ -32,7 +32,7 @@
 // scoreboard stalls on the lo-phase twiddles 53% of samples.  With no twiddle loads at all
 // (HG_FAKE_TW timing build) it still runs 0.615 us/row.  So the two-pass kernels stay the
 // default (hg_set_ntt_variant / HG_NTT_CLUSTER=1 select this path; tests keep it bit-exact).
-#include "hg_internal.cuh"
+#include "hg_ntt_common.cuh"
 
 #include <chrono>
 
@@ -45,21 +45,10 @@ constexpr int kN = kRowW * kNRows;     // 2^17
 constexpr int kTwcRow = 1984;          // transposed round-B twiddles per row: 32 (2+4+8+16+32)
 constexpr size_t kSmemBytes = (size_t)kNRows * (kRowW / kCS) * 4;   // 64 KB
 
-__device__ __forceinline__ void fwd_bfly(uint32_t& x, uint32_t& y, uint2 w, uint32_t p) {
-    const uint32_t p2 = p << 1;
-    const uint32_t a = min(x, x - p2);   // [0, 4p) -> [0, 2p)
-    const uint32_t t = mul_shoup_lazy(y, w.x, w.y, p);
-    x = a + t;
-    y = a - t + p2;
-}
-__device__ __forceinline__ void inv_bfly(uint32_t& x, uint32_t& y, uint2 w, uint32_t p) {
-    const uint32_t p2 = p << 1;
-    uint32_t s = x + y;
-    s = min(s, s - p2);
-    const uint32_t d = x - y + p2;
-    x = s;
-    y = mul_shoup_lazy(d, w.x, w.y, p);
-}
+using hgntt::fwd_bfly;
+using hgntt::inv_bfly;
+using hgntt::stage64;
+using hgntt::hi_stages;
 
 // position of word q of a row inside its 2048-word shared-memory row: bits 0-4 ^= bits 6-10
 __device__ __forceinline__ int swz(int q) { return q ^ ((q >> 6) & 31); }
@@ -83,47 +72,6 @@ __device__ __forceinline__ void cluster_arrive() {
 }
 __device__ __forceinline__ void cluster_wait() {
     asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-
-// One stage on x[64]: butterflies (2 D g + i, 2 D g + i + D) for the 32 / D groups g, group g
-// taking twiddle tw[g * TS] (TS = the twiddle stride of the caller's table).  Template
-// parameters keep every index compile-time, so x stays in registers.
-template <bool FWD, int D, int TS>
-__device__ __forceinline__ void stage64(uint32_t (&x)[64], const uint2* __restrict__ tw, uint32_t p) {
-#pragma unroll
-    for (int g = 0; g < 32 / D; ++g) {
-#ifdef HG_FAKE_TW   // timing experiment only: twiddles without loads (wrong results)
-        const uint2 w = make_uint2(0x1234567u + g * 977u + (uint32_t)(size_t)tw, 0x2345678u + g);
-#else
-        const uint2 w = __ldg(tw + g * TS);
-#endif
-#pragma unroll
-        for (int i = 0; i < D; ++i) {
-            if (FWD) fwd_bfly(x[2 * D * g + i], x[2 * D * g + i + D], w, p);
-            else inv_bfly(x[2 * D * g + i], x[2 * D * g + i + D], w, p);
-        }
-    }
-}
-
-// 6 column stages on x[r] = word (2048 r + c); stage s uses psi_rev[2^s + (r >> (6 - s))]
-template <bool FWD>
-__device__ __forceinline__ void hi_stages(uint32_t (&x)[64], const uint2* __restrict__ twp,
-                                          uint32_t p) {
-    if (FWD) {
-        stage64<true, 32, 1>(x, twp + 1, p);
-        stage64<true, 16, 1>(x, twp + 2, p);
-        stage64<true, 8, 1>(x, twp + 4, p);
-        stage64<true, 4, 1>(x, twp + 8, p);
-        stage64<true, 2, 1>(x, twp + 16, p);
-        stage64<true, 1, 1>(x, twp + 32, p);
-    } else {
-        stage64<false, 1, 1>(x, twp + 32, p);
-        stage64<false, 2, 1>(x, twp + 16, p);
-        stage64<false, 4, 1>(x, twp + 8, p);
-        stage64<false, 8, 1>(x, twp + 4, p);
-        stage64<false, 16, 1>(x, twp + 2, p);
-        stage64<false, 32, 1>(x, twp + 1, p);
-    }
 }
 
 // round A: lo stages ls = 0..5 of row G - 64 with lane l holding words q = l + 32 m (x[m]);
