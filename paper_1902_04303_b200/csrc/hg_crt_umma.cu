@@ -539,17 +539,17 @@ __global__ void __launch_bounds__(PipeCfg<FUSED>::kWarps * 32, 1) crt_umma_pipe_
     __shared__ uint4 s_hand[2][kRows];             // carry lo/hi, previous word, ambiguity
     __shared__ uint2 s_hand2[2][kRows];            // emitter state: carry, previous word
     __shared__ uint32_t tmem_base;
-    // p, cinv, cinv_sh, floor(2^53/p) (1,0,0,0 padding); PRESCALED: p, ~0, 0, floor(2^53/p)
+    // p, cinv, cinv_sh, floor(2^55/p) (1,0,0,0 padding); PRESCALED: p, ~0, 0, floor(2^55/p)
     __shared__ uint4 s_pc[HG_MAX_PRIMES + 32];
-    __shared__ uint64_t s_acc[2][kRows];
+    __shared__ uint32_t s_acc[2][kRows];
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     for (int j = tid; j < P32p; j += blockDim.x) {
         const bool ok = j < P;
         const uint32_t p = ok ? pinfo[j].p : 1u;
         s_pc[j] = !ok ? make_uint4(1u, 0u, 0u, 0u)
-              : PRESCALED ? make_uint4(p, 0xffffffffu, 0u, (uint32_t)((1ull << 53) / p))
-                          : make_uint4(p, cinv[j], cinv_sh[j], (uint32_t)((1ull << 53) / p));
+              : PRESCALED ? make_uint4(p, 0xffffffffu, 0u, (uint32_t)((1ull << 55) / p))
+                          : make_uint4(p, cinv[j], cinv_sh[j], (uint32_t)((1ull << 55) / p));
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base)), "n"(512));
@@ -703,9 +703,12 @@ __global__ void __launch_bounds__(PipeCfg<FUSED>::kWarps * 32, 1) crt_umma_pipe_
         int ir = 0, ia = 0;
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
           for (int h = 0; h < jpt; ++h) {
-            // v = round(sum y_j / p_j) in fixed point: y_j * floor(2^53 / p_j) summed exactly
-            // (error < P * 2^30 * 2^-53 << 1/8, the CRT margin)
-            uint64_t acc = 0;
+            // v = round(sum y_j / p_j) in 32-bit fixed point with 23 fraction bits: each term
+            // umulhi(y_j, floor(2^55 / p_j)) is y_j / p_j 2^23 less at most 2 units, so the sum
+            // (< 321 2^23 < 2^32) is within 2^-13.6 below the true value, and the true value lies
+            // within 1/8 of an integer (|c| < Q/8): rounding is exact.  One multiply-high and a
+            // 32-bit add per residue instead of a 64-bit multiply-accumulate.
+            uint32_t acc = 0;
             for (int kc = 0; kc < nkc; ++kc, ++ir, ++ia) {
                 const int s = ir % kRR, sa_ = ia % kRA;
                 PWAIT(0, smem_u32(&bar_res_full[s]), (ir / kRR) & 1);
@@ -723,7 +726,7 @@ __global__ void __launch_bounds__(PipeCfg<FUSED>::kWarps * 32, 1) crt_umma_pipe_
                     const uint4 pc = s_pc[j0 + u];
                     y[u] = PRESCALED ? reduce_2p(y[u] & pc.y, pc.x)
                                      : reduce_2p(mul_shoup_lazy(y[u], pc.y, pc.z, pc.x), pc.x);
-                    acc += (uint64_t)y[u] * pc.w;
+                    acc += __umulhi(y[u], pc.w);
                 }
                 if (kc == nkc - 1) {
 #ifdef HG_CRT_PROF
@@ -732,9 +735,9 @@ __global__ void __launch_bounds__(PipeCfg<FUSED>::kWarps * 32, 1) crt_umma_pipe_
                     // slot P of the last chunk carries v (its B row holds -Q): combine the halves
                     s_acc[half][n] = acc;
                     asm volatile("bar.sync 1, %0;\n" ::"n"(8 * 32) : "memory");
-                    const uint64_t tot = s_acc[0][n] + s_acc[1][n];
+                    const uint32_t tot = s_acc[0][n] + s_acc[1][n];
                     asm volatile("bar.sync 1, %0;\n" ::"n"(8 * 32) : "memory");
-                    const uint32_t v = (uint32_t)((tot + (1ull << 52)) >> 53);
+                    const uint32_t v = (tot + (1u << 22)) >> 23;
 #pragma unroll
                     for (int u = 0; u < 16; ++u)
                         if (j0 + u == P) y[u] = v;
