@@ -27,7 +27,11 @@ constexpr int kWMax = 64;         // widest operand handled here (words)
 constexpr int kBChunkBytes = 256 * 4 * kWMax;   // 64 KB: 256 rows x 256 K bytes
 constexpr int kAStage = kRows * 4 * kWMax;      // 32 KB
 constexpr int kEpiGroups = 4;    // epilogue warps per TMEM lane quarter
-constexpr int kEpiWarp0 = 6;
+#ifndef HG_MODUP_LOADERS
+#define HG_MODUP_LOADERS 4   // A-loader warps: 4 (one coefficient per thread) or 8 (two threads per coefficient)
+#endif
+constexpr int kLoaders = HG_MODUP_LOADERS;
+constexpr int kEpiWarp0 = 2 + kLoaders;
 constexpr int kWarps = kEpiWarp0 + 4 * kEpiGroups;
 constexpr int kEpiPrimes = kPrimesChunk / kEpiGroups;   // primes per epilogue warp and chunk
 constexpr size_t kSmem = 2 * (size_t)kBChunkBytes + 2 * (size_t)kAStage;   // 192 KB
@@ -86,6 +90,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) modup_umma_kernel(
     __shared__ __align__(8) uint64_t bar_b_full[2], bar_b_empty[2], bar_a_full[2], bar_a_empty[2];
     __shared__ __align__(8) uint64_t bar_tm_full[2], bar_tm_empty[2], bar_fl_full[2], bar_fl_empty[2];
     __shared__ uint32_t s_fl[2][kRows];            // bit0 sign, bit1 negate, bit2 any-nonzero
+    __shared__ uint32_t s_flp[kLoaders == 8 ? 2 : 1][2][kLoaders == 8 ? kRows : 1];   // per loader part
     // per prime: p, 2^30 mod p (+ Shoup); per operand and prime: the sign correction
     // p - 2^bits mod p and the negation base (p for signed, p + 2^bits mod p for unsigned)
     // padded by a prime chunk so the epilogue indexes base + constant without clamping
@@ -125,11 +130,11 @@ __global__ void __launch_bounds__(kWarps * 32, 1) modup_umma_kernel(
         for (int s = 0; s < 2; ++s) {
             init(&bar_b_full[s], 1);
             init(&bar_b_empty[s], 1);
-            init(&bar_a_full[s], 4);
+            init(&bar_a_full[s], kLoaders);
             init(&bar_a_empty[s], 1);
             init(&bar_tm_full[s], 1);
             init(&bar_tm_empty[s], 4 * kEpiGroups);
-            init(&bar_fl_full[s], 4);
+            init(&bar_fl_full[s], kLoaders);
             init(&bar_fl_empty[s], 4 * kEpiGroups);
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n");
@@ -195,7 +200,11 @@ __global__ void __launch_bounds__(kWarps * 32, 1) modup_umma_kernel(
         }
     } else if (warp < kEpiWarp0) {
         // ---------------- A loaders ----------------
-        const int n = (warp - 2) * 32 + lane;
+        // kLoaders = 8: warps (c, c + 4) share coefficients 32c .. 32c+31, each loading half of
+        // the 32-word batches (more loads in flight per coefficient); flags merge in s_fl2
+        const int lw = warp - 2;
+        const int n = (lw & 3) * 32 + lane;
+        const int part = kLoaders == 8 ? lw >> 2 : 0;
         const int g = n >> 3, rr = n & 7;
         int ia = 0;
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++ia) {
@@ -221,7 +230,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1) modup_umma_kernel(
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
             uint8_t* dst = s_a + sa_ * kAStage + (g * 16) * 128 + rr * 16;
             uint32_t any = 0, sign = 0;
-            for (int w0 = 0; w0 < W8; w0 += 32) {
+            // batches of 32 words: part p of kLoaders/4 parts takes batches p, p + parts, ...
+            constexpr int kParts = kLoaders / 4;
+            for (int w0 = 32 * part; w0 < W8; w0 += 32 * kParts) {
                 uint32_t wv[32];
 #pragma unroll
                 for (int e = 0; e < 32; ++e) {
@@ -243,7 +254,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1) modup_umma_kernel(
                         *reinterpret_cast<uint4*>(dst + ((w0 >> 2) + c) * 128) =
                             make_uint4(wv[4 * c], wv[4 * c + 1], wv[4 * c + 2], wv[4 * c + 3]);
             }
-            s_fl[sa_][n] = (sign ? 1u : 0u) | (neg ? 2u : 0u) | (any ? 4u : 0u);
+            const uint32_t fl = (sign ? 1u : 0u) | (neg ? 2u : 0u) | (any ? 4u : 0u);
+            if (kParts == 1) s_fl[sa_][n] = fl;
+            else s_flp[part][sa_][n] = fl;
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
             __syncwarp();
             if (lane == 0) {
@@ -262,7 +275,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) modup_umma_kernel(
             uint32_t* outp = out + (size_t)op * P * N + cb + n;
             const int sa_ = ia & 1;
             mbar_wait(smem_u32(&bar_fl_full[sa_]), (ia >> 1) & 1);
-            const uint32_t fl = s_fl[sa_][n];
+            const uint32_t fl = kLoaders == 8 ? (s_flp[0][sa_][n] | s_flp[1][sa_][n]) : s_fl[sa_][n];
             __syncwarp();
             if (lane == 0) mbar_arrive(smem_u32(&bar_fl_empty[sa_]));
             const bool sgn = fl & 1u, ng = (fl & 2u) && (fl & 4u);
