@@ -329,8 +329,12 @@ int ensure_twc(hg_ctx* ctx) {
     const size_t per = (size_t)kNRows * kTwcRow;
     const size_t bytes = per * ctx->nprimes * sizeof(uint2);
     uint2 *f = nullptr, *i = nullptr;
-    if (cudaMalloc(&f, bytes) != cudaSuccess) return hg_fail(HG_ENOMEM, "cluster NTT twiddle table");
+    if (cudaMalloc(&f, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return hg_fail(HG_ENOMEM, "cluster NTT twiddle table");
+    }
     if (cudaMalloc(&i, bytes) != cudaSuccess) {
+        cudaGetLastError();
         cudaFree(f);
         return hg_fail(HG_ENOMEM, "cluster NTT twiddle table");
     }
@@ -357,6 +361,14 @@ extern "C" int hg_set_ntt_variant(hg_ctx* ctx, int variant) {
     if (!ctx) return hg_fail(HG_EINVAL, "hg_set_ntt_variant: null context");
     if (variant < 0 || variant > 2) return hg_fail(HG_EINVAL, "hg_set_ntt_variant: variant must be 0, 1 or 2");
     ctx->ntt_cluster = variant;
+    if (variant != 1 && ctx->d_twc_fwd) {
+        // the DSMEM variant's transposed twiddles (~650 MB at log_n 17) go with it; cudaFree
+        // waits for queued work that may still read them
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        cudaFree(ctx->d_twc_fwd);
+        cudaFree(ctx->d_twc_inv);
+        ctx->d_twc_fwd = ctx->d_twc_inv = nullptr;
+    }
     return HG_OK;
 }
 

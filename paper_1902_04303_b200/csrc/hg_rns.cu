@@ -381,7 +381,16 @@ struct Scratch {
     void* p = nullptr;
     cudaStream_t s;
     explicit Scratch(cudaStream_t st) : s(st) {}
-    cudaError_t alloc(size_t bytes) { return cudaMallocAsync(&p, bytes, s); }
+    // a failed allocation also sets the runtime's last-error state; clear it, so the caller's
+    // retry (_lib.call) does not see a stale out-of-memory at its next launch check
+    cudaError_t alloc(size_t bytes) {
+        const cudaError_t e = cudaMallocAsync(&p, bytes, s);
+        if (e != cudaSuccess) {
+            p = nullptr;
+            (void)cudaGetLastError();
+        }
+        return e;
+    }
     ~Scratch() {
         if (p) cudaFreeAsync(p, s);
     }
