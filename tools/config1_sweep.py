@@ -101,8 +101,12 @@ def main():
                 rec["rotate_left_keyswitches"] = bin(params.slot_count - 2).count("1")
                 hi = [ckks.Ciphertext(c0=c.c0, c1=c.c1, level_bits=c.level_bits, scale_bits=90,
                                       slots=c.slots, params=params) for c in cts]   # post-mult scale
-                rec["rescale_per_s"] = b / device_time(lambda: [hg.rescale(c, 45) for c in hi], reps)
-                rec["mult_plain_per_s"] = b / device_time(lambda: [eng.mult_plain(c, mask) for c in cts], reps)
+                # rescale / mult_plain batches through the array-of-handles entry points
+                # (hg_ct_rescale_batch, hg_ct_mult_plain_batch: one launch group per 8 / per batch)
+                rec["rescale_per_s"] = b / device_time(
+                    (lambda: eng.rescale_many(hi, 45)) if b > 1 else (lambda: hg.rescale(hi[0], 45)), reps)
+                rec["mult_plain_per_s"] = b / device_time(
+                    (lambda: eng.mult_plain_many(cts, mask)) if b > 1 else (lambda: eng.mult_plain(cts[0], mask)), reps)
                 # hg_ntt_forward cycles rows over min(count, 320) primes: keep the batched fast
                 # path by using whole multiples of the 320-prime table past it
                 nrows = b * P if b * P <= 320 else 320 * (min(b * P, 4096) // 320)
@@ -123,7 +127,8 @@ def main():
     if args.out:
         with open(args.out, "w") as f:
             json.dump({"config": "BASELINE config 1 (primitive sweep), dnum=1, device-timed, resident inputs; "
-                                 "batches > 1 through HeEngine.mult_many / rotate_many",
+                                 "batches > 1 through HeEngine.mult_many / rotate_many / rescale_many / "
+                                 "mult_plain_many",
                        "device": torch.cuda.get_device_name(), "rows": rows}, f, indent=1)
 
 

@@ -60,6 +60,7 @@ class T:
         if BUSY:
             _lib.get_context(17).set_kernel_timing(True)
         self.acc = dict(ACC)
+        torch.cuda.reset_peak_memory_stats()
         self.ms = torch.cuda.memory_stats()
         self.t = time.perf_counter()
 
@@ -80,7 +81,8 @@ class T:
               f"{d['key_s']:5.2f}s  masks {d['mask_n']:4d} {d['mask_s']:5.2f}s  "
               f"cudaMalloc {ms['num_device_alloc'] - self.ms.get('num_device_alloc', 0):5d} "
               f"retries {ms['num_alloc_retries'] - self.ms.get('num_alloc_retries', 0)} "
-              f"reserved {ms['reserved_bytes.all.current'] / 1e9:5.1f} GB{busy}", flush=True)
+              f"reserved {ms['reserved_bytes.all.current'] / 1e9:5.1f} GB peak alloc "
+              f"{ms['allocated_bytes.all.peak'] / 1e9:5.1f} GB{busy}", flush=True)
 
 
 def main():
