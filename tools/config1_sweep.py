@@ -84,7 +84,7 @@ def main():
                 math.ceil((2 * log_l + log_n + 4) / 29.9)
             for b in batches:
                 cts = [random_ct(params, gen, 45) for _ in range(b)]
-                reps = max(1, args.reps if b <= 16 else 1)
+                reps = max(1, args.reps)
                 rec = {"log_n": log_n, "N": params.n, "log_l": log_l, "batch": b}
                 # warm the key cache at this level
                 eng.mult(cts[0], cts[0])
