@@ -397,6 +397,25 @@ struct Scratch {
     uint32_t* u32() { return static_cast<uint32_t*>(p); }
 };
 
+// out[k][j] = out[k][j] + 2^(32 kSplitW) hi[k][j] mod p_j, lazily in [0, 4p): the residues of an
+// operand wider than the tensor-core ModUp takes, from the residues of its low kSplitW words
+// (unsigned) and of its high words (the operand's own signedness) -- ModUp is linear
+constexpr int kSplitW = 64;
+__global__ void modup_combine_kernel(uint32_t* __restrict__ out, const uint32_t* __restrict__ hi, int N, int P,
+                                     const PrimeInfo* __restrict__ pinfo,
+                                     const uint32_t* __restrict__ modup_tab) {
+    const int j = blockIdx.y, k = blockIdx.z;
+    const uint32_t p = pinfo[j].p;
+    const uint32_t c = modup_tab[(size_t)j * HG_MODUP_WMAX + kSplitW];   // 2^(32 kSplitW) mod p
+    const uint32_t c_sh = (uint32_t)(((uint64_t)c << 32) / p);
+    const size_t row = ((size_t)k * P + j) * N;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+        uint32_t lo = out[row + i];
+        lo = min(lo, lo - 2 * p);                                  // [0, 2p)
+        out[row + i] = lo + mul_shoup_lazy(hi[row + i], c, c_sh, p);   // + [0, 2p)
+    }
+}
+
 int launch_modup(hg_ctx* ctx, const OperandSet& ops, int nops, int P, uint32_t* out,
                  int64_t kinv, cudaStream_t st) {
     int maxw = 0;
@@ -420,9 +439,48 @@ int launch_modup(hg_ctx* ctx, const OperandSet& ops, int nops, int P, uint32_t* 
     for (int k = 0; k < nops; ++k) macs += (double)words_for_bits(ops.bits[k]) * P * N;
     if (!getenv("HG_NO_UMMA") && !getenv("HG_NO_MMA")) {
         HgTimed tm(ctx, st, HG_K_MODUP, macs);
-        int h = hg_modup_umma_launch(ctx, ops.words, ops.bits, ops.is_signed, nops, P, out, kinv, st);
-        if (h < 0) return -h;
-        if (h == 1) return HG_OK;
+        if (maxw > kSplitW && kinv == 0 && N >= 128 && !getenv("HG_NO_MODUP_SPLIT")) {
+            // operands wider than the tensor-core kernel takes (switching keys, l + L bits): low
+            // kSplitW words unsigned into `out`, the high words (signed as the operand) into
+            // scratch, then out += 2^(32 kSplitW) hi mod p.  (Not under an automorphism: the
+            // negation acts on the whole value.)
+            const uint32_t* wl[4];
+            const uint32_t* wh[4];
+            int bl[4], bh[4], sl[4], sh[4];
+            for (int k = 0; k < nops; ++k) {
+                const bool wide = words_for_bits(ops.bits[k]) > kSplitW;
+                wl[k] = ops.words[k];
+                bl[k] = wide ? 32 * kSplitW : ops.bits[k];
+                sl[k] = wide ? 0 : ops.is_signed[k];
+                wh[k] = wide ? ops.words[k] + (size_t)kSplitW * N : ops.words[k];   // narrow: in bounds, cleared below
+                bh[k] = wide ? ops.bits[k] - 32 * kSplitW : 1;   // narrow operands: a 1-bit zero-free dummy
+                sh[k] = wide ? ops.is_signed[k] : 0;
+            }
+            void* hi = nullptr;
+            if (cudaMallocAsync(&hi, (size_t)nops * P * N * 4, st) != cudaSuccess) {
+                cudaGetLastError();
+                return hg_fail(HG_ENOMEM, "ModUp split: scratch allocation failed");
+            }
+            int h = hg_modup_umma_launch(ctx, wl, bl, sl, nops, P, out, 0, st);
+            if (h == 1) h = hg_modup_umma_launch(ctx, wh, bh, sh, nops, P, (uint32_t*)hi, 0, st);
+            if (h == 1) {
+                // narrow operands' high "part" must contribute 0: clear those rows
+                for (int k = 0; k < nops; ++k)
+                    if (words_for_bits(ops.bits[k]) <= kSplitW)
+                        cudaMemsetAsync((uint32_t*)hi + (size_t)k * P * N, 0, (size_t)P * N * 4, st);
+                modup_combine_kernel<<<dim3((N + 255) / 256 < 64 ? (N + 255) / 256 : 64, P, nops), 256, 0, st>>>(
+                    out, (const uint32_t*)hi, N, P, ctx->d_pinfo, ctx->d_modup);
+                cudaFreeAsync(hi, st);
+                HG_LAUNCH_CHECK(ctx);
+                return HG_OK;
+            }
+            cudaFreeAsync(hi, st);
+            if (h < 0) return -h;
+        } else {
+            int h = hg_modup_umma_launch(ctx, ops.words, ops.bits, ops.is_signed, nops, P, out, kinv, st);
+            if (h < 0) return -h;
+            if (h == 1) return HG_OK;
+        }
     }
     if (!getenv("HG_NO_MMA")) {
         HgTimed tm(ctx, st, HG_K_MODUP, macs);
