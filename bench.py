@@ -231,6 +231,15 @@ def run_ours(args, world, rank, local):
     barrier(world)
     torch.cuda.synchronize()
     s.record()
+    # rows stream at the projector's level (the M S_i products read only those words).  Starting
+    # the uploads with the setup (SnpBatchStream.start(), HG_STREAM_EARLY=1) was measured slower:
+    # the slots' 25-38 GB squeeze the setup's ~75 GB working set (setup 3.7 -> 4.5-5.6 s)
+    m_level = params.log_l - 150
+    stream = None
+    early = os.environ.get("HG_STREAM_EARLY") == "1"
+    if hbatch is not None and early:
+        stream = SnpBatchStream([hbatch] * my_batches, params, level=m_level,
+                                slots=int(os.environ.get("HG_STREAM_SLOTS", "2"))).start()
     if world > 1:   # column-split setup + NCCL all-gathers of z' partials and M_dup
         beta, p_prev, inter, m_dup = compute_setup_sharded(engine, inputs, rank, world, gather_m=False)
     else:
@@ -247,10 +256,13 @@ def run_ours(args, world, rank, local):
               f"{torch.cuda.max_memory_allocated() / 1e9:.1f} GB", file=sys.stderr, flush=True)
     job_keep = []
     marks = []
-    # rows stream at the projector's level: the M S_i products read only those words
-    m_level = inter.M.cols[0].level_bits
-    if hbatch is not None:
-        for b in SnpBatchStream([hbatch] * my_batches, params, level=m_level):
+    if inter.M.cols[0].level_bits != m_level:
+        raise RuntimeError(f"projector level {inter.M.cols[0].level_bits} != the streamed level {m_level}")
+    if hbatch is not None and stream is None:
+        stream = SnpBatchStream([hbatch] * my_batches, params, level=m_level,
+                                slots=int(os.environ.get("HG_STREAM_SLOTS", "2")))
+    if stream is not None:
+        for b in stream:
             read_back(compute_batch(engine, inputs, inter, m_dup, b), job_keep)
             if os.environ.get("HG_BENCH_DEBUG"):
                 marks.append(torch.cuda.Event(enable_timing=True))
@@ -266,7 +278,7 @@ def run_ours(args, world, rank, local):
         print(f"[bench] whole-job batch ms: {per}; library OOM retries {_lib.OOM_RETRIES}", file=sys.stderr,
               flush=True)
     t_whole = max_over_ranks(s.elapsed_time(e) / 1e3, world) if hbatch is not None else None
-    del job_keep
+    del job_keep, stream   # the ring's slots (k x 12.6 GB) go back before the resident steps
 
     def step_resident():
         return compute_batch(engine, inputs, inter, m_dup, batch)

@@ -129,8 +129,11 @@ def test_toy_pipeline_streamed_batches_bit_exact(toy):
     # three passes over the batches so both device slots are reused while the next one loads;
     # then the rows streamed only at the projector's level (mod_down on upload)
     m_level = g.meta("out.M0")["level_bits"]
-    for level in (None, m_level):
-        stream = SnpBatchStream(host * 3, params, level=level)
+    # ... and a ring of three slots whose first uploads are issued before the setup runs
+    for level, slots, early in ((None, 2, False), (m_level, 2, False), (m_level, 3, True)):
+        stream = SnpBatchStream(host * 3, params, level=level, slots=slots)
+        if early:
+            stream.start()
         out = compute_gwas_encrypted(hg.HeEngine(params, evk, rot), enc, cache=stream)
         assert len(out.batch_outputs) == 3 * len(host)
         for bo in out.batch_outputs:
