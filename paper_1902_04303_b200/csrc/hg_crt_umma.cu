@@ -352,7 +352,13 @@ template <bool FUSED> struct PipeCfg {
 #define HG_CRT_RR_PLAIN 4
 #endif
     static constexpr int kRR = FUSED ? HG_CRT_RR_FUSED : HG_CRT_RR_PLAIN;
-    static constexpr int kRA = FUSED ? 3 : 4;
+#ifndef HG_CRT_RA_FUSED
+#define HG_CRT_RA_FUSED 3
+#endif
+#ifndef HG_CRT_RA_PLAIN
+#define HG_CRT_RA_PLAIN 4
+#endif
+    static constexpr int kRA = FUSED ? HG_CRT_RA_FUSED : HG_CRT_RA_PLAIN;
     static constexpr int kRB = FUSED ? 2 : 3;
 };
 #ifndef HG_CRT_JOBCOLS
