@@ -92,6 +92,13 @@ int hg_poly_divide_round(hg_ctx* ctx, uint32_t* out, int out_bits, const uint32_
 int hg_poly_automorphism(hg_ctx* ctx, uint32_t* out, const uint32_t* a, int bits,
                          int64_t k, void* stream);
 
+/* out[i] = float(centered(a_i) >> s) as Python's float(int) rounds it (nearest, ties to even),
+ * s = bitlen(max_i |centered(a_i)|) - 500 if that exceeds 960 else 0; aux is a device int[2]
+ * that receives (max bit length, s).  The coefficient -> float64 step of decode
+ * (encoding.py:93-105, 108-115; the caller applies the multiplier 2^min(s,300)).         */
+int hg_poly_to_double(hg_ctx* ctx, double* out, int* aux, const uint32_t* a, int bits,
+                      void* stream);
+
 /* ---- exact negacyclic product ------------------------------------------------------ */
 /* out (out_bits) = (a * b) mod 2^out_bits, exact negacyclic convolution of the two
  * operand values.  Replaces RingElement.mul / mul_mod (ring.py:140-150), i.e.

@@ -55,6 +55,7 @@ SIGNATURES = {
     "hg_poly_lift_centered": (_i, [_vp, _vp, _i, _vp, _i, _vp]),
     "hg_poly_divide_round": (_i, [_vp, _vp, _i, _vp, _i, _i, _vp]),
     "hg_poly_automorphism": (_i, [_vp, _vp, _vp, _i, _i64, _vp]),
+    "hg_poly_to_double": (_i, [_vp, _vp, _vp, _vp, _i, _vp]),
     "hg_poly_mul": (_i, [_vp, _vp, _i, Operand, Operand, _vp]),
     "hg_poly_tensor": (_i, [_vp, _vp, _vp, _vp, _i, Operand, Operand, Operand, Operand, _vp]),
     "hg_key_prepare": (_i, [_vp, _vp, _vp, _i, _i, _i, _vp, ctypes.POINTER(_vp)]),

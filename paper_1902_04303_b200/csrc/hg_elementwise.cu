@@ -375,7 +375,152 @@ __global__ void __launch_bounds__(kThreads) mult_const_rescale_kernel(PolyPtrs p
     }
 }
 
+// ---- decode: centered coefficients -> float64 (encoding.py:93-105) -------------------------
+// The reference converts each centered coefficient c to float with Python's float(int) --
+// round to nearest, ties to even -- after shifting every coefficient right (floor) by
+// s = bitlen(max |c|) - 500 when that bit length exceeds 960.  These kernels reproduce that
+// bit for bit: magnitudes are read word by word from the two's-complement canonical words,
+// s comes from a device-wide max of the bit lengths, and the quotient is rounded from a
+// 64-bit window plus sticky / all-ones flags of the bits below it.
+
+// Word w of |centered(c)| for a coefficient whose canonical words are a[w*N + i].
+struct CenteredMag {
+    const uint32_t* a;
+    int N, i, W, bits, z;  // z: lowest nonzero word (negation carry stops there)
+    bool neg;
+    __device__ uint32_t word(int w) const {
+        if (w < 0 || w >= W) return 0u;
+        uint32_t x = a[(size_t)w * N + i];
+        if (neg) x = w < z ? 0u : (w == z ? 0u - x : ~x);
+        if (w == W - 1) x &= mask_for(bits);
+        return x;
+    }
+};
+
+__device__ __forceinline__ CenteredMag centered_mag(const uint32_t* a, int W, int bits, int N, int i) {
+    CenteredMag m{a, N, i, W, bits, W, false};
+    // centered: c > 2^(bits-1) -> c - 2^bits (ring.py:106-110); c == 2^(bits-1) stays positive
+    const int tb = (bits - 1) & 31;
+    const bool top = (a[(size_t)(W - 1) * N + i] >> tb) & 1u;
+    int z = W;
+    for (int w = 0; w < W; ++w) {
+        uint32_t x = a[(size_t)w * N + i];
+        if (w == W - 1) x &= mask_for(bits);
+        if (x) { z = w; break; }
+    }
+    bool above_half = false;
+    if (top) {  // any bit below bit bits-1 set?
+        const uint32_t topw = a[(size_t)(W - 1) * N + i] & mask_for(bits) & ((1u << tb) - 1u);
+        above_half = topw != 0u || z < W - 1;
+    }
+    m.neg = above_half;
+    m.z = z;
+    return m;
+}
+
+// bit length of the magnitude (0 for zero)
+__device__ __forceinline__ int mag_bitlen(const CenteredMag& m) {
+    for (int w = m.W - 1; w >= 0; --w) {
+        uint32_t x = m.word(w);
+        if (x) return 32 * w + 32 - __clz(x);
+    }
+    return 0;
+}
+
+// 64 bits of the magnitude starting at bit `lo` (bits past the top read as 0)
+__device__ __forceinline__ uint64_t mag_bits64(const CenteredMag& m, int lo) {
+    const int w0 = lo >> 5, sh = lo & 31;
+    uint64_t v = (uint64_t)m.word(w0) | ((uint64_t)m.word(w0 + 1) << 32);
+    if (sh) v = (v >> sh) | ((uint64_t)m.word(w0 + 2) << (64 - sh));
+    return v;
+}
+
+// any / all bits of the magnitude in [lo, hi)
+__device__ __forceinline__ void mag_range_flags(const CenteredMag& m, int lo, int hi, bool& any,
+                                                bool& all) {
+    any = false;
+    all = true;
+    for (int w = lo >> 5; w << 5 < hi; ++w) {
+        const int b0 = max(lo, w << 5) - (w << 5), b1 = min(hi, (w << 5) + 32) - (w << 5);
+        const uint32_t mask = (b1 - b0 == 32) ? 0xffffffffu : (((1u << (b1 - b0)) - 1u) << b0);
+        const uint32_t x = m.word(w) & mask;
+        any |= x != 0u;
+        all &= x == mask;
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) decode_bitlen_kernel(const uint32_t* __restrict__ a, int W,
+                                                                 int bits, int N, int* __restrict__ maxlen) {
+    const int i = blockIdx.x * kThreads + threadIdx.x;
+    int bl = 0;
+    if (i < N) bl = mag_bitlen(centered_mag(a, W, bits, N, i));
+    for (int o = 16; o; o >>= 1) bl = max(bl, __shfl_xor_sync(0xffffffffu, bl, o));
+    if ((threadIdx.x & 31) == 0 && bl) atomicMax(maxlen, bl);
+}
+
+// out[i] = float(centered(c_i) >> s), s = bitlen - 500 if bitlen > 960 else 0 (maxlen[0] holds
+// the bit length on entry; maxlen[1] receives s)
+__global__ void __launch_bounds__(kThreads) decode_double_kernel(const uint32_t* __restrict__ a, int W,
+                                                                 int bits, int N, int* __restrict__ maxlen,
+                                                                 double* __restrict__ out) {
+    const int i = blockIdx.x * kThreads + threadIdx.x;
+    const int top = maxlen[0];
+    const int s = top > 960 ? top - 500 : 0;
+    if (i == 0) maxlen[1] = s;
+    if (i >= N) return;
+    const CenteredMag m = centered_mag(a, W, bits, N, i);
+    const int bl = mag_bitlen(m);
+    // floor(c / 2^s): q = mag >> s for c >= 0, -(mag >> s) - (low s bits nonzero) for c < 0
+    bool low_any = false, low_all = true;
+    if (s > 0) mag_range_flags(m, 0, min(s, bl), low_any, low_all);
+    const bool add1 = m.neg && low_any;
+    const int hq = bl - s;  // bit length of q
+    double r;
+    if (hq <= 64) {
+        const uint64_t q = hq > 0 ? mag_bits64(m, s) & (hq == 64 ? ~0ull : ((1ull << hq) - 1ull)) : 0ull;
+        if (add1 && q == ~0ull)
+            r = 18446744073709551616.0;  // 2^64
+        else
+            r = __ull2double_rn(q + (add1 ? 1ull : 0ull));
+    } else {
+        const int lo = s + hq - 64;  // window = bits [lo, lo + 64) of mag, top bit set
+        uint64_t win = mag_bits64(m, lo);
+        bool any, all;
+        mag_range_flags(m, s, lo, any, all);
+        bool sticky = any;
+        int e = lo - s;
+        if (add1) {
+            if (all) {
+                sticky = false;
+                if (++win == 0ull) {  // 2^64 * 2^e exactly
+                    win = 1ull << 63;
+                    e += 1;
+                }
+            } else {
+                sticky = true;
+            }
+        }
+        uint64_t mant = win >> 11;
+        const uint32_t rem = (uint32_t)(win & 0x7ffu);
+        if (rem > 0x400u || (rem == 0x400u && (sticky || (mant & 1ull)))) mant += 1ull;
+        r = ldexp((double)mant, e + 11);
+    }
+    out[i] = m.neg ? -r : r;
+}
+
 }  // namespace
+
+int hg_ew_to_double(hg_ctx* ctx, double* out, int* aux, const uint32_t* a, int bits, cudaStream_t st) {
+    const int W = words_for_bits(bits);
+    HgTimed tm(ctx, st, HG_K_ELEMENTWISE, (double)ctx->N);
+    if (cudaMemsetAsync(aux, 0, 2 * sizeof(int), st) != cudaSuccess)
+        return hg_fail(HG_ECUDA, "hg_poly_to_double: memset failed");
+    decode_bitlen_kernel<<<grid_for(ctx->N), kThreads, 0, st>>>(a, W, bits, ctx->N, aux);
+    HG_LAUNCH_CHECK(ctx);
+    decode_double_kernel<<<grid_for(ctx->N), kThreads, 0, st>>>(a, W, bits, ctx->N, aux, out);
+    HG_LAUNCH_CHECK(ctx);
+    return HG_OK;
+}
 
 // ---- internal entry points (used by the fused drivers in hg_rns.cu) --------------------------
 int hg_ew_add(hg_ctx* ctx, uint32_t* out, const uint32_t* a, const uint32_t* b, int bits,
@@ -525,6 +670,12 @@ extern "C" int hg_poly_divide_round(hg_ctx* ctx, uint32_t* out, int out_bits, co
                   "hg_poly_divide_round: bad arguments");
     HG_CHECK_ARGS(out != a, "hg_poly_divide_round: out must not alias the input");
     return hg_ew_divide_round(ctx, out, out_bits, a, in_bits, shift, (cudaStream_t)stream);
+}
+
+extern "C" int hg_poly_to_double(hg_ctx* ctx, double* out, int* aux, const uint32_t* a, int bits,
+                                 void* stream) {
+    HG_CHECK_ARGS(ctx && out && aux && a && bits >= 1, "hg_poly_to_double: bad arguments");
+    return hg_ew_to_double(ctx, out, aux, a, bits, (cudaStream_t)stream);
 }
 
 extern "C" int hg_poly_automorphism(hg_ctx* ctx, uint32_t* out, const uint32_t* a, int bits,

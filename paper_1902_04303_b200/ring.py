@@ -342,6 +342,19 @@ class RingElement:
                                                 ctx.stream()))
         return out
 
+    def to_float64(self) -> tuple[np.ndarray, float]:
+        """float64 of the centered coefficients plus the power-of-two multiplier, exactly as
+        encoding.py:93-105 computes them (Python float(int) rounding, the >960-bit shift),
+        converted on the GPU; only the N doubles cross to the host."""
+        torch = _torch()
+        ctx = _ctx(self.n)
+        out = torch.empty(self.n, dtype=torch.float64, device=self.words.device)
+        aux = torch.empty(2, dtype=torch.int32, device=self.words.device)
+        _lib.check(ctx.lib.hg_poly_to_double(ctx.handle, out.data_ptr(), aux.data_ptr(),
+                                             self.words.data_ptr(), self.mod_bits, ctx.stream()))
+        shift = int(aux[1].item())
+        return out.cpu().numpy(), 2.0 ** min(shift, 300)
+
     # -- dunder ------------------------------------------------------------------------------
     def __eq__(self, other):
         if not isinstance(other, RingElement):
