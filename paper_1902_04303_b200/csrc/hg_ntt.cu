@@ -52,7 +52,9 @@ __global__ void __launch_bounds__(256) ntt_lo_kernel(uint32_t* __restrict__ data
     const uint2* twp = tw + (size_t)prime * N;
     uint32_t* rowp = data + (size_t)row * N;
     const int base = blockIdx.x * chunk;
-    for (int i = threadIdx.x; i < chunk; i += blockDim.x) sm[i] = rowp[base + i];
+    const bool perm = k2 >= 9;   // NTT-domain side in the transposed order (ntt_pos)
+    for (int i = threadIdx.x; i < chunk; i += blockDim.x)
+        sm[i] = rowp[!FWD && perm ? hgntt::ntt_pos(base + i) : base + i];
     __syncthreads();
     const int half = chunk >> 1;
     for (int si = s_begin; si < s_end; ++si) {
@@ -70,7 +72,8 @@ __global__ void __launch_bounds__(256) ntt_lo_kernel(uint32_t* __restrict__ data
         }
         __syncthreads();
     }
-    for (int i = threadIdx.x; i < chunk; i += blockDim.x) rowp[base + i] = sm[i];
+    for (int i = threadIdx.x; i < chunk; i += blockDim.x)
+        rowp[FWD && perm ? hgntt::ntt_pos(base + i) : base + i] = sm[i];
 }
 
 template <bool FWD>
@@ -155,12 +158,13 @@ __device__ __forceinline__ void round8(uint32_t (&x)[RB][E], int G, int base,
     }
 }
 
-template <int B, int E = 8>
+// PERM: the words are NTT-domain data in the transposed storage order (ntt_pos; B == 0 only)
+template <int B, int E = 8, bool PERM = false>
 __device__ __forceinline__ void load8(uint32_t (&x)[E], const uint32_t* src, int base) {
     if (B == 0) {   // contiguous: 16-byte accesses
 #pragma unroll
         for (int v = 0; v < E / 4; ++v) {
-            const uint4 a = *reinterpret_cast<const uint4*>(src + base + 4 * v);
+            const uint4 a = *reinterpret_cast<const uint4*>(src + (PERM ? hgntt::ntt_pos(base + 4 * v) : base + 4 * v));
             x[4 * v] = a.x; x[4 * v + 1] = a.y; x[4 * v + 2] = a.z; x[4 * v + 3] = a.w;
         }
     } else {
@@ -168,12 +172,12 @@ __device__ __forceinline__ void load8(uint32_t (&x)[E], const uint32_t* src, int
         for (int m = 0; m < E; ++m) x[m] = src[base + (m << B)];
     }
 }
-template <int B, int E = 8>
+template <int B, int E = 8, bool PERM = false>
 __device__ __forceinline__ void store8(const uint32_t (&x)[E], uint32_t* dst, int base) {
     if (B == 0) {
 #pragma unroll
         for (int v = 0; v < E / 4; ++v)
-            *reinterpret_cast<uint4*>(dst + base + 4 * v) = make_uint4(x[4 * v], x[4 * v + 1], x[4 * v + 2], x[4 * v + 3]);
+            *reinterpret_cast<uint4*>(dst + (PERM ? hgntt::ntt_pos(base + 4 * v) : base + 4 * v)) = make_uint4(x[4 * v], x[4 * v + 1], x[4 * v + 2], x[4 * v + 3]);
     } else {
 #pragma unroll
         for (int m = 0; m < E; ++m) dst[base + (m << B)] = x[m];
@@ -245,7 +249,7 @@ __device__ __forceinline__ void lo_round(uint32_t (&x)[RB][E], uint32_t* __restr
 #pragma unroll
     for (int r = 0; r < RB; ++r) {
         if (ROUND == 0) {
-            if (!PRELOADED) load8<B, E>(x[r], rowp + r * rstride, base);
+            if (!PRELOADED) load8<B, E, (K2 >= 9)>(x[r], rowp + r * rstride, base);
         } else {
             sload8<B, E>(x[r], sm + r * kSmRow, base);
         }
@@ -256,7 +260,7 @@ __device__ __forceinline__ void lo_round(uint32_t (&x)[RB][E], uint32_t* __restr
     round8<FWD, R, B, LS0, RB, E>(x, G, base, twp, p);
     if (ROUND == NR - 1) {
 #pragma unroll
-        for (int r = 0; r < RB; ++r) store8<B, E>(x[r], rowp + r * rstride, base);
+        for (int r = 0; r < RB; ++r) store8<B, E, (K2 >= 9)>(x[r], rowp + r * rstride, base);
     } else {
 #pragma unroll
         for (int r = 0; r < RB; ++r) sstore8<B, E>(x[r], sm + r * kSmRow, base);
@@ -439,10 +443,11 @@ __device__ __forceinline__ void lo_fused_chunk(uint32_t* out, const uint32_t* in
     uint32_t x[RB][E];
     {
         uint32_t u0[E], u1[E], u2[E], u3[E];
-        load8<0, E>(u0, in0 + roff, base);
-        load8<0, E>(u1, in1 + roff, base);
-        if (PRE != 3 && PRE != 5) load8<0, E>(u2, in2 + roff, base);
-        if (PRE == 2) load8<0, E>(u3, in3 + roff, base);
+        constexpr bool PERM = K2 >= 9;
+        load8<0, E, PERM>(u0, in0 + roff, base);
+        load8<0, E, PERM>(u1, in1 + roff, base);
+        if (PRE != 3 && PRE != 5) load8<0, E, PERM>(u2, in2 + roff, base);
+        if (PRE == 2) load8<0, E, PERM>(u3, in3 + roff, base);
 #pragma unroll
         for (int m = 0; m < E; ++m) {
             const uint32_t a = min(u0[m], u0[m] - p2);

@@ -170,7 +170,7 @@ ntt_fwd_c8_kernel(uint32_t* __restrict__ data, int P, int prime_offset,
     __syncwarp();
     uint32_t* orow = rowp + (size_t)r * kRowW;
 #pragma unroll
-    for (int m = 0; m < 64; ++m) orow[l + 32 * m] = srow[swz(l + 32 * m)];
+    for (int m = 0; m < 64; ++m) orow[hgntt::ntt_pos(l + 32 * m)] = srow[swz(l + 32 * m)];
 }
 
 // Inverse.  PRE 0: plain, rows [B][P][N] in place (grid (8, B, P), prime prime_offset + jp).
@@ -214,7 +214,9 @@ ntt_inv_c8_kernel(uint32_t* out, const uint32_t* in0, const uint32_t* in1, const
     const int G = kNRows + r;
     const uint2* twc_row = twc + (size_t)prime * (kNRows * kTwcRow) + (size_t)r * kTwcRow + l;
     uint32_t* srow = sm + w * kRowW;
-    const size_t roff = (size_t)r * kRowW + l;
+    // NTT-domain words in the transposed storage order (ntt_pos): word l + 32 m of row r
+    const size_t roff = (size_t)r * kRowW;
+    auto qi = [&](int m) { return roff + (size_t)hgntt::ntt_pos(l + 32 * m); };
     uint32_t x[64];
 
 #pragma unroll 1
@@ -224,11 +226,11 @@ ntt_inv_c8_kernel(uint32_t* out, const uint32_t* in0, const uint32_t* in1, const
         if (o == 0) {
             if (PRE == 0) {
 #pragma unroll
-                for (int m = 0; m < 64; ++m) x[m] = orow[roff + 32 * m];
+                for (int m = 0; m < 64; ++m) x[m] = orow[qi(m)];
             } else {
 #pragma unroll
                 for (int m = 0; m < 64; ++m) {
-                    const size_t q = roff + 32 * m;
+                    const size_t q = qi(m);
                     const uint32_t u0 = in0[q];
                     const uint32_t a = min(u0, u0 - p2);
                     if (PRE == 1) {
@@ -254,7 +256,7 @@ ntt_inv_c8_kernel(uint32_t* out, const uint32_t* in0, const uint32_t* in1, const
         } else {
             // raw product rows stashed by this same thread in pass 0
 #pragma unroll
-            for (int m = 0; m < 64; ++m) x[m] = orow[roff + 32 * m];
+            for (int m = 0; m < 64; ++m) x[m] = orow[qi(m)];
             __syncthreads();   // the previous output's column reads of sm are done
         }
         // ---- rows: round B (distances 1..16) then round A (32..1024) ------------------------

@@ -25,6 +25,19 @@ __device__ __forceinline__ void inv_bfly(uint32_t& x, uint32_t& y, uint2 w, uint
     y = mul_shoup_lazy(d, w.x, w.y, p);
 }
 
+// NTT-domain storage order.  The forward transform's bit-reversed output (and the inverse's
+// input) is stored with every 512-word block transposed as a 32 x 4 matrix of 16-byte vectors:
+// word q = 512 b + 16 a + 4 v + j (a < 32, v < 4, j < 4) sits at 512 b + 128 v + 4 a + j.  A
+// contiguous-pass thread holds E consecutive words in its unit-stride round, so in natural
+// order a warp's 16-byte accesses stride 4E bytes (16 cache lines and twice the ideal sectors
+// per STG.128 at E = 16); in this order every 16-byte access of a warp lands in 128-byte runs.
+// Every NTT-domain consumer is elementwise (products, sums, prepared operands), so the order is
+// invisible outside the transforms; rows of 2^k >= 512 words use it (chunks of the contiguous
+// pass are >= 512 words exactly then), shorter rows keep natural order.
+__host__ __device__ __forceinline__ int ntt_pos(int q) {
+    return (q & ~511) | (((q >> 2) & 3) << 7) | (((q >> 4) & 31) << 2) | (q & 3);
+}
+
 // One stage on x[64]: butterflies (2 D g + i, 2 D g + i + D) for the 32 / D groups g, group g
 // taking twiddle tw[g * TS] (TS = the twiddle stride of the caller's table).  Template
 // parameters keep every index compile-time, so x stays in registers.
