@@ -520,10 +520,12 @@ __device__ void pipe_rescan_exact(const uint32_t* __restrict__ r, int P, int N, 
 // PRESCALED: the residues were produced from operands pre-multiplied by the per-prime CRT
 // constant (hg_key / hg_ctprep prepared for this window), so y_j = x_j mod p_j is one
 // conditional subtraction instead of a Shoup product
-template <bool FUSED, bool PRESCALED>
+// LOGN: log2 N as a compile-time constant (the epilogue's word-row strides become address
+// immediates), 0 = N at run time
+template <bool FUSED, bool PRESCALED, int LOGN>
 __global__ void __launch_bounds__(PipeCfg<FUSED>::kWarps * 32, 1) crt_umma_pipe_kernel(
     const __grid_constant__ CUtensorMap res_map, const __grid_constant__ CUtensorMap add_map,
-    const uint32_t* __restrict__ res, int P, int P32p, int N, int nouts,
+    const uint32_t* __restrict__ res, int P, int P32p, int N_rt, int nouts,
     const PrimeInfo* __restrict__ pinfo, const uint8_t* __restrict__ Bpipe,
     const uint32_t* __restrict__ Mtab, int W, const uint32_t* __restrict__ negQ,
     const uint32_t* __restrict__ cinv, const uint32_t* __restrict__ cinv_sh,
@@ -531,6 +533,7 @@ __global__ void __launch_bounds__(PipeCfg<FUSED>::kWarps * 32, 1) crt_umma_pipe_
     constexpr int kRR = PipeCfg<FUSED>::kRR;
     constexpr int kRA = PipeCfg<FUSED>::kRA;
     constexpr int kRB = PipeCfg<FUSED>::kRB;
+    const int N = LOGN ? (1 << LOGN) : N_rt;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* s_res = smem;
     uint8_t* s_a = smem + kRR * kResStage;
@@ -729,9 +732,11 @@ __global__ void __launch_bounds__(PipeCfg<FUSED>::kWarps * 32, 1) crt_umma_pipe_
 #pragma unroll
                 for (int u = 0; u < 16; ++u) {
                     // padding primes: x is stale but cinv = 0 (PRESCALED: mask 0) gives y = 0
+                    // (PRESCALED: a padding slot keeps a stale value -- its B rows are zero and its
+                    // floor(2^55/p) is 0, so neither the GEMM nor v sees it)
                     const uint4 pc = s_pc[j0 + u];
-                    y[u] = PRESCALED ? reduce_2p(y[u] & pc.y, pc.x)
-                                     : reduce_2p(mul_shoup_lazy(y[u], pc.y, pc.z, pc.x), pc.x);
+                    const uint32_t yy = PRESCALED ? y[u] : mul_shoup_lazy(y[u], pc.y, pc.z, pc.x);
+                    y[u] = min(yy, yy - pc.x);   // [0, 2p) -> [0, p)
                     acc += __umulhi(y[u], pc.w);
                 }
                 if (kc == nkc - 1) {
@@ -911,25 +916,20 @@ __global__ void __launch_bounds__(PipeCfg<FUSED>::kWarps * 32, 1) crt_umma_pipe_
                             const uint64_t sum = (uint64_t)o + ap[hh * kRows] + c2;
                             const uint32_t w = (uint32_t)sum;
                             c2 = (uint32_t)(sum >> 32);
-                            *op = rb ? __funnelshift_r(prev2, w, rb) : w;
+                            op[(size_t)hh * N] = rb ? __funnelshift_r(prev2, w, rb) : w;
                             prev2 = w;
-                            op += N;
                         }
                     } else {
                         uint32_t* op = outi + (size_t)(t0 - sw - ush) * N;
                         if (sbit) {
 #pragma unroll
                             for (int hh = 0; hh < 8; ++hh) {
-                                *op = __funnelshift_r(prev, wv[hh], sbit);
+                                op[(size_t)hh * N] = __funnelshift_r(prev, wv[hh], sbit);
                                 prev = wv[hh];
-                                op += N;
                             }
                         } else {
 #pragma unroll
-                            for (int hh = 0; hh < 8; ++hh) {
-                                *op = wv[hh];
-                                op += N;
-                            }
+                            for (int hh = 0; hh < 8; ++hh) op[(size_t)hh * N] = wv[hh];
                             prev = wv[7];
                         }
                     }
@@ -1031,16 +1031,27 @@ int hg_crt_umma_pipe_launch(hg_ctx* ctx, const CrtTable* tab, const uint32_t* re
                             cudaStream_t st, const CrtFinish* finish, bool prescaled) {
     static std::atomic<uint64_t> attr_set{0};
     const int nsm = ctx->nsm;
+    using Kern = void (*)(const CUtensorMap, const CUtensorMap, const uint32_t*, int, int, int, int, const PrimeInfo*,
+                          const uint8_t*, const uint32_t*, int, const uint32_t*, const uint32_t*, const uint32_t*,
+                          const double*, int, int, int, UOuts, CrtFinish);
+    // [log_n class: run-time N, 2^16, 2^17][fused finish][prescaled]
+    static const Kern kerns[3][2][2] = {
+        {{crt_umma_pipe_kernel<false, false, 0>, crt_umma_pipe_kernel<false, true, 0>},
+         {crt_umma_pipe_kernel<true, false, 0>, crt_umma_pipe_kernel<true, true, 0>}},
+        {{crt_umma_pipe_kernel<false, false, 16>, crt_umma_pipe_kernel<false, true, 16>},
+         {crt_umma_pipe_kernel<true, false, 16>, crt_umma_pipe_kernel<true, true, 16>}},
+        {{crt_umma_pipe_kernel<false, false, 17>, crt_umma_pipe_kernel<false, true, 17>},
+         {crt_umma_pipe_kernel<true, false, 17>, crt_umma_pipe_kernel<true, true, 17>}}};
     if (hg_first_on_device(attr_set, ctx->device)) {
-        HG_CUDA_TRY(cudaFuncSetAttribute(crt_umma_pipe_kernel<false, false>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pipe_smem<false>()));
-        HG_CUDA_TRY(cudaFuncSetAttribute(crt_umma_pipe_kernel<false, true>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pipe_smem<false>()));
-        HG_CUDA_TRY(cudaFuncSetAttribute(crt_umma_pipe_kernel<true, false>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pipe_smem<true>()));
-        HG_CUDA_TRY(cudaFuncSetAttribute(crt_umma_pipe_kernel<true, true>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pipe_smem<true>()));
+        for (int a = 0; a < 3; ++a)
+            for (int c = 0; c < 2; ++c) {
+                HG_CUDA_TRY(cudaFuncSetAttribute(kerns[a][0][c], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)pipe_smem<false>()));
+                HG_CUDA_TRY(cudaFuncSetAttribute(kerns[a][1][c], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)pipe_smem<true>()));
+            }
     }
+    const int lc = ctx->log_n == 17 ? 2 : (ctx->log_n == 16 ? 1 : 0);
     UOuts o{};
     for (int k = 0; k < nouts; ++k) o.out[k] = outs_in[k];
     const int ntiles = nouts * (ctx->N / kRows);
@@ -1058,12 +1069,12 @@ int hg_crt_umma_pipe_launch(hg_ctx* ctx, const CrtTable* tab, const uint32_t* re
         if (int rc = hg_tmap_2d_u32(&add_map, fin.add[0], (uint64_t)ctx->N, (uint64_t)nouts * out_w, kRows,
                                     kJobCols))
             return rc;
-        auto kern = prescaled ? crt_umma_pipe_kernel<true, true> : crt_umma_pipe_kernel<true, false>;
+        const Kern kern = kerns[lc][1][prescaled ? 1 : 0];
         kern<<<grid, PipeCfg<true>::kWarps * 32, pipe_smem<true>(), st>>>(
             res_map, add_map, res, P, tab->P32p, ctx->N, nouts, ctx->d_pinfo, tab->d_Bpipe, tab->d_M, tab->W,
             tab->d_negQ, tab->d_cinv, tab->d_cinv_sh, tab->d_invp, shift, out_bits, tb0, o, fin);
     } else {
-        auto kern = prescaled ? crt_umma_pipe_kernel<false, true> : crt_umma_pipe_kernel<false, false>;
+        const Kern kern = kerns[lc][0][prescaled ? 1 : 0];
         kern<<<grid, PipeCfg<false>::kWarps * 32, pipe_smem<false>(), st>>>(
             res_map, res_map, res, P, tab->P32p, ctx->N, nouts, ctx->d_pinfo, tab->d_Bpipe, tab->d_M, tab->W,
             tab->d_negQ, tab->d_cinv, tab->d_cinv_sh, tab->d_invp, shift, out_bits, tb0, o, fin);

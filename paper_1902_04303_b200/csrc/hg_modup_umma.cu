@@ -17,6 +17,8 @@
 //   warps 6-21  epilogue: four warps per TMEM lane quarter split a chunk's 64 primes
 // TMEM is double-buffered per prime chunk, so the epilogue of chunk c overlaps the MMAs of c+1
 // and the A / B rings keep the loads of the next tile in flight.
+#include <type_traits>
+
 #include "hg_internal.cuh"
 
 namespace {
@@ -78,11 +80,14 @@ __device__ __forceinline__ T pick(const T (&a)[4], int k) {
 
 // SIGNED: some operand is two's complement (else the sign correction is compiled out);
 // AUTOMORPH: the gather runs through x -> x^k (else the negation correction is compiled out)
-template <bool SIGNED, bool AUTOMORPH>
+// LOGN: log2 N as a compile-time constant (row strides of the loaders' word gathers and of the
+// epilogue's residue stores become address immediates), 0 = N at run time
+template <bool SIGNED, bool AUTOMORPH, int LOGN>
 __global__ void __launch_bounds__(kWarps * 32, 1) modup_umma_kernel(
-    MOps ops, int nops, int N, const PrimeInfo* __restrict__ pinfo,
+    MOps ops, int nops, int N_rt, const PrimeInfo* __restrict__ pinfo,
     const uint32_t* __restrict__ modup_tab, const uint8_t* __restrict__ Bimg, int P,
     uint32_t* __restrict__ out, int64_t automorph_kinv) {
+    const int N = LOGN ? (1 << LOGN) : N_rt;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* s_b = smem;                           // 2 x 64 KB
     uint8_t* s_a = smem + 2 * kBChunkBytes;        // 2 x 32 KB
@@ -100,7 +105,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) modup_umma_kernel(
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     for (int j = tid; j < P + kPrimesChunk; j += blockDim.x) {
         if (j >= P) {
-            s_pc[j] = make_uint4(1u, 0u, 0u, 0u);
+            s_pc[j] = make_uint4(1u, 2u, 0u, 0xffffffffu);
             for (int k = 0; k < 4; ++k) s_corr[k][j] = make_uint2(0u, 0u);
             continue;
         }
@@ -108,8 +113,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) modup_umma_kernel(
 #ifdef HG_MODUP_FOLD30
         s_pc[j] = make_uint4(pi.p, pi.c30, pi.c30_sh, 0u);
 #else
-        // 2^16 mod p = 2^16 (p > 2^16): its Shoup companion floor(2^48 / p)
-        s_pc[j] = make_uint4(pi.p, 1u << 16, (uint32_t)((1ull << 48) / pi.p), 0u);
+        // (p, 2p, floor(2^48 / p) = the Shoup companion of 2^16 mod p = 2^16, -p)
+        s_pc[j] = make_uint4(pi.p, 2u * pi.p, (uint32_t)((1ull << 48) / pi.p), 0u - pi.p);
 #endif
         for (int k = 0; k < nops; ++k) {
             const int bits = pick(ops.bits, k);
@@ -234,6 +239,19 @@ __global__ void __launch_bounds__(kWarps * 32, 1) modup_umma_kernel(
             constexpr int kParts = kLoaders / 4;
             for (int w0 = 32 * part; w0 < W8; w0 += 32 * kParts) {
                 uint32_t wv[32];
+                if (w0 + 32 < W) {
+                    // interior batch (all 32 words below the top word): no predicates, no masks
+                    const uint32_t* pw = in + (size_t)w0 * N + src;
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) wv[e] = __ldg(pw + (size_t)e * N);
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) any |= wv[e];
+#pragma unroll
+                    for (int c = 0; c < 8; ++c)
+                        *reinterpret_cast<uint4*>(dst + ((w0 >> 2) + c) * 128) =
+                            make_uint4(wv[4 * c], wv[4 * c + 1], wv[4 * c + 2], wv[4 * c + 3]);
+                    continue;
+                }
 #pragma unroll
                 for (int e = 0; e < 32; ++e) {
                     const int w = w0 + e;
@@ -278,7 +296,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) modup_umma_kernel(
             const uint32_t fl = kLoaders == 8 ? (s_flp[0][sa_][n] | s_flp[1][sa_][n]) : s_fl[sa_][n];
             __syncwarp();
             if (lane == 0) mbar_arrive(smem_u32(&bar_fl_empty[sa_]));
-            const bool sgn = fl & 1u, ng = (fl & 2u) && (fl & 4u);
+            const uint32_t sgn01 = fl & 1u;
+            const bool ng = (fl & 2u) && (fl & 4u);
             for (int ch = 0; ch < nch; ++ch, ++ic) {
                 const int ts = ic & 1;
                 mbar_wait(smem_u32(&bar_tm_full[ts]), (ic >> 1) & 1);
@@ -305,35 +324,47 @@ __global__ void __launch_bounds__(kWarps * 32, 1) modup_umma_kernel(
                                  : "r"(lane_addr + (uint32_t)(jj * 4)));
                     asm volatile("tcgen05.wait::ld.sync.aligned;\n");
                     const int nv = P - (jbase + jj);   // primes of this group that exist (warp-uniform)
+                    uint32_t* og = orow + (size_t)jj * N;
+                    // FULL: all 8 primes exist (every group but a basis' last): unpredicated stores
+                    auto group = [&](auto full) {
+                        constexpr bool FULL = decltype(full)::value;
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) {
-                        // branch-free: the 8 primes are independent chains the scheduler interleaves
-                        const uint4 pc = pcb[jj + e];
-                        const uint32_t p = pc.x;
+                        for (int e = 0; e < 8; ++e) {
+                            // branch-free: the 8 primes are independent chains the scheduler interleaves
+                            const uint4 pc = pcb[jj + e];
 #ifdef HG_MODUP_FOLD30
-                        // digits < 2^24 (K <= 256 bytes): v < 2^49, one 2^30 fold reaches [0, 4p)
-                        const uint32_t t = d[4 * e + 3] * 256u + d[4 * e + 2];   // < 2^31 (byte 3 < 64)
-                        const uint64_t v = madw(t, 1u << 16, madw(d[4 * e + 1], 256u, (uint64_t)d[4 * e]));
-                        uint32_t r = mul_shoup_lazy((uint32_t)(v >> 30), pc.y, pc.z, p) +
-                                     ((uint32_t)v & 0x3fffffffu);
+                            // digits < 2^24 (K <= 256 bytes): v < 2^49, one 2^30 fold reaches [0, 4p)
+                            const uint32_t p = pc.x;
+                            const uint32_t t = d[4 * e + 3] * 256u + d[4 * e + 2];   // < 2^31 (byte 3 < 64)
+                            const uint64_t v = madw(t, 1u << 16, madw(d[4 * e + 1], 256u, (uint64_t)d[4 * e]));
+                            uint32_t r = mul_shoup_lazy((uint32_t)(v >> 30), pc.y, pc.z, p) +
+                                         ((uint32_t)v & 0x3fffffffu);
 #else
-                        // v = D0 + D1 2^8 + D2 2^16 + D3 2^24 (digits <= 256 * 255^2 < 2^24, D3 < 2^22)
-                        //   = T' 2^16 + (U mod 2^16),  U = D1 2^8 + D0 < 2^32,  T' = D3 2^8 + D2 + (U >> 16) < 2^31
-                        // so one Shoup product by 2^16 (a shift and one multiply-high) and a 16-bit add
-                        // land in [0, 2p + 2^16) within [0, 3p), all in 32-bit arithmetic
-                        const uint32_t u = d[4 * e + 1] * 256u + d[4 * e];
-                        const uint32_t tt = d[4 * e + 3] * 256u + d[4 * e + 2] + (u >> 16);
-                        const uint32_t q = __umulhi(tt, pc.z);
-                        uint32_t r = (tt << 16) - q * p + (u & 0xffffu);
+                            // v = D0 + D1 2^8 + D2 2^16 + D3 2^24 (digits <= 256 * 255^2 < 2^24, D3 < 2^22)
+                            //   = T' 2^16 + (U mod 2^16),  U = D1 2^8 + D0 < 2^32,  T' = D3 2^8 + D2 + (U >> 16) < 2^31
+                            // so one Shoup product by 2^16 (one multiply-high; T' 2^16 + (U mod 2^16) mod 2^32 is a
+                            // byte permute) lands in [0, 2p + 2^16) within [0, 3p), all in 32-bit arithmetic:
+                            // r = (T' 2^16 | U mod 2^16) - q p, as one multiply-add by -p
+                            const uint32_t u = (d[4 * e + 1] << 8) + d[4 * e];
+                            const uint32_t tt = (d[4 * e + 3] << 8) + d[4 * e + 2] + (u >> 16);
+                            const uint32_t q = __umulhi(tt, pc.z);
+                            uint32_t r = q * pc.w + __byte_perm(u, tt, 0x5410);
 #endif
-                        if (SIGNED || AUTOMORPH) {
-                            const uint2 cr = crb[jj + e];
-                            r = min(r, r - 2 * p);              // [0, 2p)
-                            if (SIGNED) r += sgn ? cr.x : 0u;   // two's-complement sign: -2^bits, [0, 3p)
-                            if (AUTOMORPH) r = ng ? cr.y - r : r;   // automorphism sign, (0, 4p)
+                            if (SIGNED || AUTOMORPH) {
+                                const uint2 cr = crb[jj + e];
+#ifdef HG_MODUP_FOLD30
+                                r = min(r, r - 2u * pc.x);          // [0, 2p)
+#else
+                                r = min(r, r - pc.y);               // [0, 2p)
+#endif
+                                if (SIGNED) r += sgn01 * cr.x;      // two's-complement sign: -2^bits, [0, 3p)
+                                if (AUTOMORPH) r = ng ? cr.y - r : r;   // automorphism sign, (0, 4p)
+                            }
+                            if (FULL || e < nv) og[(size_t)e * N] = r;
                         }
-                        if (e < nv) orow[(size_t)(jj + e) * N] = r;
-                    }
+                    };
+                    if (nv >= 8) group(std::true_type{});
+                    else group(std::false_type{});
                 }
                 asm volatile("tcgen05.fence::before_thread_sync;\n");
                 __syncwarp();
@@ -392,12 +423,21 @@ int hg_modup_umma_launch(hg_ctx* ctx, const uint32_t* const* words, const int* b
     if (rc) return -rc;
     static std::atomic<uint64_t> attr_set{0};
     const int nsm = ctx->nsm;
+    using Kern = void (*)(MOps, int, int, const PrimeInfo*, const uint32_t*, const uint8_t*, int, uint32_t*, int64_t);
+    // [log_n class: run-time N, 2^16, 2^17][signed][automorphism]
+    static const Kern kerns[3][2][2] = {
+        {{modup_umma_kernel<false, false, 0>, modup_umma_kernel<false, true, 0>},
+         {modup_umma_kernel<true, false, 0>, modup_umma_kernel<true, true, 0>}},
+        {{modup_umma_kernel<false, false, 16>, modup_umma_kernel<false, true, 16>},
+         {modup_umma_kernel<true, false, 16>, modup_umma_kernel<true, true, 16>}},
+        {{modup_umma_kernel<false, false, 17>, modup_umma_kernel<false, true, 17>},
+         {modup_umma_kernel<true, false, 17>, modup_umma_kernel<true, true, 17>}}};
     if (hg_first_on_device(attr_set, ctx->device)) {
-        if (cudaFuncSetAttribute(modup_umma_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem) != cudaSuccess ||
-            cudaFuncSetAttribute(modup_umma_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem) != cudaSuccess ||
-            cudaFuncSetAttribute(modup_umma_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem) != cudaSuccess ||
-            cudaFuncSetAttribute(modup_umma_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem) != cudaSuccess)
-            return -hg_fail(HG_ECUDA, "modup_umma smem attribute");
+        for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 2; ++b)
+                for (int c = 0; c < 2; ++c)
+                    if (cudaFuncSetAttribute(kerns[a][b][c], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem) != cudaSuccess)
+                        return -hg_fail(HG_ECUDA, "modup_umma smem attribute");
     }
     MOps o{};
     for (int k = 0; k < nops; ++k) {
@@ -409,10 +449,9 @@ int hg_modup_umma_launch(hg_ctx* ctx, const uint32_t* const* words, const int* b
     const int grid = ntiles < nsm ? ntiles : nsm;
     bool any_signed = false;
     for (int k = 0; k < nops; ++k) any_signed |= is_signed[k] != 0;
-    auto kern = any_signed ? (kinv ? modup_umma_kernel<true, true> : modup_umma_kernel<true, false>)
-                           : (kinv ? modup_umma_kernel<false, true> : modup_umma_kernel<false, false>);
-    kern<<<grid, kWarps * 32, kSmem, st>>>(o, nops, ctx->N, ctx->d_pinfo, ctx->d_modup,
-                                                        ctx->d_modup_umma, P, out, kinv);
+    const int lc = ctx->log_n == 17 ? 2 : (ctx->log_n == 16 ? 1 : 0);
+    kerns[lc][any_signed ? 1 : 0][kinv ? 1 : 0]<<<grid, kWarps * 32, kSmem, st>>>(
+        o, nops, ctx->N, ctx->d_pinfo, ctx->d_modup, ctx->d_modup_umma, P, out, kinv);
     ctx->launches.fetch_add(1, std::memory_order_relaxed);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return -hg_fail(HG_ECUDA, std::string("modup_umma launch: ") + cudaGetErrorString(e));
