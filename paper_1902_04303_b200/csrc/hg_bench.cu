@@ -1,9 +1,10 @@
 // hg_bench.cu -- integer-pipe roofline probe: the exact lazy Harvey butterfly (Shoup
-// modmul + add/sub) the NTT kernels execute, register resident, 8 independent chains per
-// thread, enough CTAs to fill all SMs.  The measured butterflies/s is the integer-pipe
+// modmul + add/sub) the NTT kernels execute -- hgntt::fwd_bfly itself, so the probe carries the
+// kernels' instruction mix (IMAD.HI + 2 IMAD on the fma pipe, VIADDMNMX + 2 IADD3 on the alu
+// pipe) --, register resident, 8 independent chains per thread, enough CTAs to fill all SMs.  The measured butterflies/s is the integer-pipe
 // "peak" that NTT kernel throughput is reported against (MEASURED_PEAKS.json has no
 // integer figure).
-#include "hg_internal.cuh"
+#include "hg_ntt_common.cuh"
 
 namespace {
 
@@ -15,15 +16,10 @@ __global__ void __launch_bounds__(256) modmul_probe_kernel(int iters, uint32_t p
         x[k] = (threadIdx.x * 2654435761u + k * 40503u) % p;
         y[k] = (blockIdx.x * 97u + k * 7919u + threadIdx.x) % p;
     }
-    const uint32_t p2 = p << 1;
+    const uint2 tw = make_uint2(w, wsh);
     for (int it = 0; it < iters; ++it) {
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            uint32_t a = x[k] >= p2 ? x[k] - p2 : x[k];
-            uint32_t t = mul_shoup_lazy(y[k], w, wsh, p);
-            x[k] = a + t;
-            y[k] = a - t + p2;
-        }
+        for (int k = 0; k < 8; ++k) hgntt::fwd_bfly(x[k], y[k], tw, p);
     }
     uint32_t acc = 0;
 #pragma unroll

@@ -668,20 +668,24 @@ int launch_hi8(int k1, dim3 grid, cudaStream_t st, uint32_t* data, int log_n, in
 }
 
 // one pass over all rows: groups of 2 batch rows per block (3 for an odd count), 1 if B == 1
+// [j0, j0 + pz) of the P primes (pz < 0: all): the row stride stays P
 template <bool FWD>
 int ntt_pass(hg_ctx* ctx, bool hi, int k1, int k2, uint32_t* data, int B, int P, int off,
-             const uint2* tw, cudaStream_t st) {
+             const uint2* tw, cudaStream_t st, int j0 = 0, int pz = -1) {
     const int log_n = ctx->log_n, N = ctx->N;
+    if (pz < 0) pz = P;
+    data += (size_t)j0 * N;
+    off += j0;
     if (HG_HI64 && hi && k1 == 6 && B <= 65535) {
-        if (FWD ? launch_hi64<true>(log_n, B, P, st, data, off, ctx->d_pinfo, tw)
-                : launch_hi64<false>(log_n, B, P, st, data, off, ctx->d_pinfo, tw))
+        if (pz != P || (FWD ? launch_hi64<true>(log_n, B, P, st, data, off, ctx->d_pinfo, tw)
+                            : launch_hi64<false>(log_n, B, P, st, data, off, ctx->d_pinfo, tw)))
             return hg_fail(HG_EINVAL, "strided NTT pass: unsupported size");
         HG_LAUNCH_CHECK(ctx);
         return HG_OK;
     }
     const int gx = hi ? N / kTile : N >> k2;
     auto run = [&](int rb, int groups, int bb0) {
-        const dim3 g(gx, groups, P);
+        const dim3 g(gx, groups, pz);
         if (rb == 1) {
             if (hi) launch_hi8<FWD, 1>(k1, g, st, data, log_n, P, bb0, off, ctx->d_pinfo, tw);
             else launch_lo8<FWD, 1>(k2, g, st, data, log_n, P, bb0, off, ctx->d_pinfo, tw);
@@ -704,6 +708,20 @@ int ntt_pass(hg_ctx* ctx, bool hi, int k1, int k2, uint32_t* data, int B, int P,
     return HG_OK;
 }
 
+// Primes per group of launches when a transform's two passes run prime range by prime range, so
+// that a range's rows (`rows_per_prime` rows of N words per prime) stay in L2 between the passes
+// (HG_NTT_L2_MB: the budget in MB, 0 = one launch per pass over all primes).
+int prime_chunk(const hg_ctx* ctx, int rows_per_prime, int P) {
+    static const int mb = [] { const char* e = getenv("HG_NTT_L2_MB"); return e ? atoi(e) : 0; }();
+    if (mb <= 0) return P;
+    const size_t per_prime = (size_t)rows_per_prime * ctx->N * sizeof(uint32_t);
+    int pc = (int)(((size_t)mb << 20) / per_prime);
+    if (pc < 1) pc = 1;
+    if (pc >= P) return P;
+    const int chunks = (P + pc - 1) / pc;   // even ranges
+    return (P + chunks - 1) / chunks;
+}
+
 }  // namespace
 
 // rows = number of length-N rows laid out [B][P][N]; row r uses prime prime_offset + r % P.
@@ -724,12 +742,16 @@ int hg_ntt_launch(hg_ctx* ctx, uint32_t* data, int rows, int P, int prime_offset
         if (ctx->ntt_cluster == 2 && log_n == 17)   // 256 threads per 2048-word chunk and per tile
             return forward ? ntt_c8l2<true>(ctx, data, B, P, prime_offset, tw, stream)
                            : ntt_c8l2<false>(ctx, data, B, P, prime_offset, tw, stream);
-        if (forward) {
-            if (k1 && (rc = ntt_pass<true>(ctx, true, k1, k2, data, B, P, prime_offset, tw, stream))) return rc;
-            if ((rc = ntt_pass<true>(ctx, false, k1, k2, data, B, P, prime_offset, tw, stream))) return rc;
-        } else {
-            if ((rc = ntt_pass<false>(ctx, false, k1, k2, data, B, P, prime_offset, tw, stream))) return rc;
-            if (k1 && (rc = ntt_pass<false>(ctx, true, k1, k2, data, B, P, prime_offset, tw, stream))) return rc;
+        const int pc = k1 ? prime_chunk(ctx, B, P) : P;
+        for (int j0 = 0; j0 < P; j0 += pc) {
+            const int pz = P - j0 < pc ? P - j0 : pc;
+            if (forward) {
+                if (k1 && (rc = ntt_pass<true>(ctx, true, k1, k2, data, B, P, prime_offset, tw, stream, j0, pz))) return rc;
+                if ((rc = ntt_pass<true>(ctx, false, k1, k2, data, B, P, prime_offset, tw, stream, j0, pz))) return rc;
+            } else {
+                if ((rc = ntt_pass<false>(ctx, false, k1, k2, data, B, P, prime_offset, tw, stream, j0, pz))) return rc;
+                if (k1 && (rc = ntt_pass<false>(ctx, true, k1, k2, data, B, P, prime_offset, tw, stream, j0, pz))) return rc;
+            }
         }
         return HG_OK;
     }
@@ -786,13 +808,22 @@ int hg_intt_fused(hg_ctx* ctx, int pre, uint32_t* out, const uint32_t* i0, const
         HG_LAUNCH_CHECK(ctx);
         return HG_OK;
     }
-    const dim3 g(N >> k2, batch, P);
-    if (pre == 1) launch_fused_lo8<1>(k2, g, st, out, i0, i1, i2, i3, log_n, P, ctx->d_pinfo, ctx->d_tw_inv, bsi, bso);
-    else if (pre == 2) launch_fused_lo8<2>(k2, g, st, out, i0, i1, i2, i3, log_n, P, ctx->d_pinfo, ctx->d_tw_inv);
-    else if (pre == 5) launch_fused_lo8<5>(k2, g, st, out, i0, i1, i2, i3, log_n, P, ctx->d_pinfo, ctx->d_tw_inv, bsi, bso);
-    else launch_fused_lo8<3>(k2, g, st, out, i0, i1, i2, i3, log_n, P, ctx->d_pinfo, ctx->d_tw_inv);
-    HG_LAUNCH_CHECK(ctx);
-    if (k1) return ntt_pass<false>(ctx, true, k1, k2, out, batch * rb, P, 0, ctx->d_tw_inv, st);
+    const int pc = k1 ? prime_chunk(ctx, batch * rb, P) : P;
+    for (int j0 = 0; j0 < P; j0 += pc) {
+        const int pz = P - j0 < pc ? P - j0 : pc;
+        const dim3 g(N >> k2, batch, pz);
+        const size_t o = (size_t)j0 * N;
+        const PrimeInfo* pin = ctx->d_pinfo + j0;
+        const uint2* twj = ctx->d_tw_inv + o;
+        const uint32_t* j2 = i2 ? i2 + o : i2;
+        const uint32_t* j3 = i3 ? i3 + o : i3;
+        if (pre == 1) launch_fused_lo8<1>(k2, g, st, out + o, i0 + o, i1 + o, j2, j3, log_n, P, pin, twj, bsi, bso);
+        else if (pre == 2) launch_fused_lo8<2>(k2, g, st, out + o, i0 + o, i1 + o, j2, j3, log_n, P, pin, twj);
+        else if (pre == 5) launch_fused_lo8<5>(k2, g, st, out + o, i0 + o, i1 + o, j2, j3, log_n, P, pin, twj, bsi, bso);
+        else launch_fused_lo8<3>(k2, g, st, out + o, i0 + o, i1 + o, j2, j3, log_n, P, pin, twj);
+        HG_LAUNCH_CHECK(ctx);
+        if (k1 && (rc = ntt_pass<false>(ctx, true, k1, k2, out, batch * rb, P, 0, ctx->d_tw_inv, st, j0, pz))) return rc;
+    }
     return HG_OK;
 }
 

@@ -19,10 +19,7 @@ def cpulist(s):
 
 
 def gpu_numa_node():
-    try:
-        bdf = torch.cuda.get_device_properties(0).pci_bus_id  # torch >= 2.3
-    except Exception:
-        bdf = None
+    bdf = None   # torch's pci_bus_id is the bus number only: ask nvidia-smi for the full address
     if bdf is None:
         import subprocess
         bdf = subprocess.run(["nvidia-smi", "--query-gpu=pci.bus_id", "--format=csv,noheader", "-i", "0"],
