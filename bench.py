@@ -658,8 +658,9 @@ def main():
         "unit": "G" + ("butterflies" if dom == "ntt" else "MAC") + "/s",
         "frac": round(achieved / r["peaks"][peak_key], 4) if r["peaks"][peak_key] else None,
         "traffic": ncu_traffic(dom),
-        "peak_source": "measured in-run: register-resident probe of the kernel's own instruction mix "
-                       "(MEASURED_PEAKS.json has no integer-pipe figure)",
+        "peak_source": "measured in-run: register-resident probe running the NTT kernels' own butterfly "
+                       "(hgntt::fwd_bfly: IMAD.HI + 2 IMAD on the fma pipe, VIADDMNMX + 2 IADD3 on the alu pipe), "
+                       "a burst at the unthrottled clock (MEASURED_PEAKS.json has no integer-pipe figure)",
         "share_of_step": round(ks[dom]["ms"] / step_ms_total, 3) if step_ms_total else None,
         "kernel_classes": {k: {"ms_per_step": round(v["ms"] / steps, 2), "launches": v["launches"],
                                "G_work_per_s": round(v["work"] / (v["ms"] / 1e3) / 1e9, 1) if v["ms"] else 0}
@@ -676,6 +677,13 @@ def main():
             roofline["kernel_classes"][k]["int8_tops"] = round(tops, 1)
             roofline["kernel_classes"][k]["frac_of_i8_peak"] = round(tops / i8_tops, 4)
     roofline["i8_peak_tops"] = round(i8_tops, 1)
+    # the timed steps run power-capped below the clock the burst probe sees: the same pipe's
+    # peak at the step's own median SM clock, next to the burst figure
+    clk = r.get("clocks") or {}
+    if dom == "ntt" and clk.get("sm_mhz") and clk.get("sm_max_mhz") and roofline["frac"]:
+        scale = min(1.0, clk["sm_mhz"] / clk["sm_max_mhz"])
+        roofline["peak_at_step_clock"] = round(roofline["peak"] * scale, 1)
+        roofline["frac_at_step_clock"] = round(roofline["frac"] / scale, 4)
     cpu = None
     if not args.no_cpu_baseline and world == 1:   # the contract: rank 0 at N=1 only
         cb = cpu_baseline_sample(params.log_n, params.log_l)
