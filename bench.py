@@ -184,6 +184,7 @@ def run_ours(args, world, rank, local):
         compute_batch,
         compute_setup,
         encrypt_gwas_inputs,
+        plan_setup,
     )
 
     from paper_1902_04303_b200.parallel import compute_setup_sharded, shard_batches
@@ -209,6 +210,8 @@ def run_ours(args, world, rank, local):
     batch = build_snp_batch(ds.S, 0, inputs.config, params, pk, gen)
     hbatch = HostSnpBatch.from_device(batch) if not args.no_e2e else None
     torch.cuda.synchronize()
+    if hbatch is not None:
+        batch = None   # the whole job streams from the host copy; resident again for the timed steps
 
     def read_back(out, keep):
         """the step's 3 result ciphertexts -> pinned host memory, stream-ordered (no host stall)"""
@@ -231,15 +234,17 @@ def run_ours(args, world, rank, local):
     barrier(world)
     torch.cuda.synchronize()
     s.record()
-    # rows stream at the projector's level (the M S_i products read only those words).  Starting
-    # the uploads with the setup (SnpBatchStream.start(), HG_STREAM_EARLY=1) was measured slower:
-    # the slots' 25-38 GB squeeze the setup's ~75 GB working set (setup 3.7 -> 4.5-5.6 s)
+    # rows stream at the projector's level (the M S_i products read only those words); the ring's
+    # first uploads start with the setup (HG_STREAM_EARLY=0: after it)
     m_level = params.log_l - 150
     stream = None
-    early = os.environ.get("HG_STREAM_EARLY") == "1"
+    early = os.environ.get("HG_STREAM_EARLY", "1") == "1" and world == 1
+    n_slots = int(os.environ.get("HG_STREAM_SLOTS", "4" if early else "2"))
     if hbatch is not None and early:
-        stream = SnpBatchStream([hbatch] * my_batches, params, level=m_level,
-                                slots=int(os.environ.get("HG_STREAM_SLOTS", "2"))).start()
+        # the first uploads run while the setup's kernels leave the PCIe link idle: the pools
+        # are grown first (plan_setup) so the ring's slots are carved out of the reservation
+        plan_setup(engine, config)
+        stream = SnpBatchStream([hbatch] * my_batches, params, level=m_level, slots=n_slots).start()
     if world > 1:   # column-split setup + NCCL all-gathers of z' partials and M_dup
         beta, p_prev, inter, m_dup = compute_setup_sharded(engine, inputs, rank, world, gather_m=False)
     else:
@@ -259,8 +264,7 @@ def run_ours(args, world, rank, local):
     if inter.M.cols[0].level_bits != m_level:
         raise RuntimeError(f"projector level {inter.M.cols[0].level_bits} != the streamed level {m_level}")
     if hbatch is not None and stream is None:
-        stream = SnpBatchStream([hbatch] * my_batches, params, level=m_level,
-                                slots=int(os.environ.get("HG_STREAM_SLOTS", "2")))
+        stream = SnpBatchStream([hbatch] * my_batches, params, level=m_level, slots=n_slots)
     if stream is not None:
         for b in stream:
             read_back(compute_batch(engine, inputs, inter, m_dup, b), job_keep)
@@ -279,6 +283,9 @@ def run_ours(args, world, rank, local):
               flush=True)
     t_whole = max_over_ranks(s.elapsed_time(e) / 1e3, world) if hbatch is not None else None
     del job_keep, stream   # the ring's slots (k x 12.6 GB) go back before the resident steps
+    if batch is None:
+        batch = hbatch.to_device(params)
+        torch.cuda.synchronize()
 
     def step_resident():
         return compute_batch(engine, inputs, inter, m_dup, batch)

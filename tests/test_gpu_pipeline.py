@@ -159,3 +159,27 @@ def test_batch_keys_prepared_by_the_setup(toy):
         bo = compute_batch(engine, enc, inter, m_dup, batch)
         assert_ct_equal(bo.num_ct, g, f"out.b{bo.index}.num")
     assert KEY_CACHE.misses == misses
+
+
+def test_projector_duplicated_in_column_groups(toy, monkeypatch):
+    """compute_setup runs the M_dup ladders and prepares column group by column group
+    (gwas.DUP_GROUP); groups of 3 over the toy's 8 columns (3 + 3 + 2) give the reference's op
+    counts, rotation order and batch outputs, and HostSnpBatch.to_device round-trips a batch."""
+    import paper_1902_04303_b200 as hg
+    from paper_1902_04303_b200 import gwas
+    from paper_1902_04303_b200.gwas import HostSnpBatch, compute_gwas_encrypted
+
+    g, params, (sk, pk, evk, rot), ds, config, seed = toy
+    enc = _golden_inputs(g, params, config)
+    enc.batches = [HostSnpBatch.from_device(b).to_device(params) for b in enc.batches]
+    monkeypatch.setattr(gwas, "DUP_GROUP", 3)
+    with hg.track_ops() as ops:
+        out = compute_gwas_encrypted(hg.HeEngine(params, evk, rot), enc)
+    names = [str(s) for s in g.arr("op_count_names")]
+    assert ops.snapshot() == dict(zip(names, [int(x) for x in g.arr("op_counts")]))
+    assert ops.rotation_amounts == [int(x) for x in g.arr("rotation_amounts")]
+    for bo in out.batch_outputs:
+        assert_ct_equal(bo.num_ct, g, f"out.b{bo.index}.num")
+        assert_ct_equal(bo.den_even_ct, g, f"out.b{bo.index}.den_even")
+        if config.complex_packing:
+            assert_ct_equal(bo.den_odd_ct, g, f"out.b{bo.index}.den_odd")
