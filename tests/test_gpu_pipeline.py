@@ -130,9 +130,11 @@ def test_toy_pipeline_streamed_batches_bit_exact(toy):
     # then the rows streamed only at the projector's level (mod_down on upload)
     m_level = g.meta("out.M0")["level_bits"]
     # ... and a ring of three slots whose first uploads are issued before the setup runs
-    for level, slots, early in ((None, 2, False), (m_level, 2, False), (m_level, 3, True)):
-        stream = SnpBatchStream(host * 3, params, level=level, slots=slots)
-        if early:
+    # (early="manual"), or by compute_gwas_encrypted before the setup's M_dup stage (early=True)
+    for level, slots, early in ((None, 2, False), (m_level, 2, False), (m_level, 3, "manual"),
+                                (m_level, 4, True)):
+        stream = SnpBatchStream(host * 3, params, level=level, slots=slots, early=early is True)
+        if early == "manual":
             stream.start()
         out = compute_gwas_encrypted(hg.HeEngine(params, evk, rot), enc, cache=stream)
         assert len(out.batch_outputs) == 3 * len(host)
