@@ -189,6 +189,14 @@ def run_ours(args, world, rank, local):
 
     from paper_1902_04303_b200.parallel import compute_setup_sharded, shard_batches
 
+    # a process that has just exited (e.g. the test run before this bench) can still be releasing
+    # its device memory: wait, bounded, until the GPU is (nearly) empty before sizing the pools
+    t_wait = time.time()
+    while time.time() - t_wait < 60:
+        free, total = torch.cuda.mem_get_info()
+        if free > 0.95 * total:
+            break
+        time.sleep(0.5)
     params = hg.CkksParams(log_n=args.log_n, log_l=args.log_l, log_p=45, log_p_small=30)
     t_wall0 = time.time()
     # every rank holds the same keys and setup inputs: the column-split setup combines their
@@ -213,6 +221,16 @@ def run_ours(args, world, rank, local):
     if hbatch is not None:
         batch = None   # the whole job streams from the host copy; resident again for the timed steps
 
+    def mem_note(tag):
+        if os.environ.get("HG_BENCH_DEBUG"):
+            free, total = torch.cuda.mem_get_info()
+            print(f"[bench] {tag}: free {free / 1e9:.1f} of {total / 1e9:.1f} GB, torch reserved "
+                  f"{torch.cuda.memory_reserved() / 1e9:.1f} / allocated {torch.cuda.memory_allocated() / 1e9:.1f} GB, "
+                  f"library pool {ctx.pool_bytes() / 1e9:.1f} / in use {ctx.pool_bytes(True) / 1e9:.1f} GB",
+                  file=sys.stderr, flush=True)
+
+    mem_note("before the whole job")
+
     def read_back(out, keep):
         """the step's 3 result ciphertexts -> pinned host memory, stream-ordered (no host stall)"""
         host = []
@@ -234,17 +252,18 @@ def run_ours(args, world, rank, local):
     barrier(world)
     torch.cuda.synchronize()
     s.record()
-    # rows stream at the projector's level (the M S_i products read only those words); the ring's
-    # first uploads start with the setup (HG_STREAM_EARLY=0: after it)
+    # rows stream at the projector's level (the M S_i products read only those words).  The ring
+    # starts after the setup; HG_STREAM_EARLY=1 starts it before the setup's last stage
+    # (compute_setup before_dup) or with the setup (HG_STREAM_WHEN=start) -- both measured: the
+    # early batches run compute-bound (-0.45 s) but the setup slows by as much (same-box A/B,
+    # profiles/r2_stream_early_v3_ab.txt)
     m_level = params.log_l - 150
     stream = None
-    early = os.environ.get("HG_STREAM_EARLY", "1") == "1" and world == 1
+    early = os.environ.get("HG_STREAM_EARLY", "0") == "1" and world == 1
     n_slots = int(os.environ.get("HG_STREAM_SLOTS", "4" if early else "2"))
     when = os.environ.get("HG_STREAM_WHEN", "dup")   # "dup": before the M_dup ladders; "start": with the setup
     if hbatch is not None and early:
-        # the first uploads run while the setup's kernels leave the PCIe link idle -- from its
-        # last stage on (the M_dup ladders upload nothing themselves; started earlier, the bulk
-        # copies delay the setup's own plaintext uploads: measured 3.2 -> 3.9-4.0 s)
+        # the first uploads run while the setup's kernels leave the PCIe link idle
         stream = SnpBatchStream([hbatch] * my_batches, params, level=m_level, slots=n_slots, early=True)
         if when == "start":
             plan_setup(engine, config)   # the ring's slots come out of the planned reservation
@@ -295,6 +314,7 @@ def run_ours(args, world, rank, local):
     def step_resident():
         return compute_batch(engine, inputs, inter, m_dup, batch)
 
+    mem_note("before the resident steps")
     for _ in range(args.warmup):
         step_resident()
     torch.cuda.synchronize()
@@ -340,6 +360,7 @@ def run_ours(args, world, rank, local):
     # The batch's 245 ciphertexts sit in pinned host memory; SnpBatchStream copies batch i+1 on a
     # side stream while batch i computes; every step's 3 result ciphertexts are read back.
     e2e = None
+    mem_note("before e2e")
     if not args.no_e2e:
         def run_e2e(nsteps):
             # every step's 3 result ciphertexts are copied to pinned host memory asynchronously
