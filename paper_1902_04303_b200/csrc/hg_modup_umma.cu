@@ -62,6 +62,20 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
 }
+// HG_MODUP_PROF (diagnostic builds only): per-CTA, per-warp cycles spent in each barrier wait
+// (and in the loaders' gather / the epilogue's column loop), read back with hg_modup_prof_read:
+// [cta][warp][0..3 waits / work by role, 5 = elapsed]
+#ifdef HG_MODUP_PROF
+__device__ unsigned long long g_modup_prof[160][24][8];
+#define MWAIT(cat, bar, par)                                  \
+    do {                                                      \
+        const long long _t = clock64();                       \
+        mbar_wait(bar, par);                                  \
+        prof[cat] += (unsigned long long)(clock64() - _t);    \
+    } while (0)
+#else
+#define MWAIT(cat, bar, par) mbar_wait(bar, par)
+#endif
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar) : "memory");
 }
@@ -103,6 +117,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1) modup_umma_kernel(
     __shared__ uint2 s_corr[4][HG_MAX_PRIMES + kPrimesChunk];
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+#ifdef HG_MODUP_PROF
+    unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const long long t_start = clock64();
+#endif
     for (int j = tid; j < P + kPrimesChunk; j += blockDim.x) {
         if (j >= P) {
             s_pc[j] = make_uint4(1u, 2u, 0u, 0xffffffffu);
@@ -162,7 +180,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) modup_umma_kernel(
                 const uint32_t bytes = (uint32_t)(W8 / 4) * 4096u;   // K chunks 0 .. W8/4-1
                 for (int ch = 0; ch < nch; ++ch, ++ib) {
                     const int s = ib & 1;
-                    mbar_wait(smem_u32(&bar_b_empty[s]), ((ib >> 1) & 1) ^ 1);
+                    MWAIT(0, smem_u32(&bar_b_empty[s]), ((ib >> 1) & 1) ^ 1);
                     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
                     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(&bar_b_full[s])), "r"(bytes) : "memory");
                     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
@@ -182,11 +200,11 @@ __global__ void __launch_bounds__(kWarps * 32, 1) modup_umma_kernel(
                 const int op = tile / tpo;
                 const int W8 = (((pick(ops.bits, op) + 31) >> 5) + 7) & ~7;
                 const int sa_ = ia & 1;
-                mbar_wait(smem_u32(&bar_a_full[sa_]), (ia >> 1) & 1);
+                MWAIT(0, smem_u32(&bar_a_full[sa_]), (ia >> 1) & 1);
                 for (int ch = 0; ch < nch; ++ch, ++ib, ++ic) {
                     const int sb_ = ib & 1, ts = ic & 1;
-                    mbar_wait(smem_u32(&bar_b_full[sb_]), (ib >> 1) & 1);
-                    mbar_wait(smem_u32(&bar_tm_empty[ts]), ((ic >> 1) & 1) ^ 1);
+                    MWAIT(1, smem_u32(&bar_b_full[sb_]), (ib >> 1) & 1);
+                    MWAIT(2, smem_u32(&bar_tm_empty[ts]), ((ic >> 1) & 1) ^ 1);
                     asm volatile("tcgen05.fence::after_thread_sync;\n");
                     for (int k = 0; k < W8 / 8; ++k) {
                         // A: core (row group g, K chunk c) at (16g + c) * 128; B: at (32c + g) * 128
@@ -229,8 +247,11 @@ __global__ void __launch_bounds__(kWarps * 32, 1) modup_umma_kernel(
                 src = (int)j;
             }
             const int sa_ = ia & 1;
-            mbar_wait(smem_u32(&bar_a_empty[sa_]), ((ia >> 1) & 1) ^ 1);
-            mbar_wait(smem_u32(&bar_fl_empty[sa_]), ((ia >> 1) & 1) ^ 1);
+            MWAIT(0, smem_u32(&bar_a_empty[sa_]), ((ia >> 1) & 1) ^ 1);
+            MWAIT(1, smem_u32(&bar_fl_empty[sa_]), ((ia >> 1) & 1) ^ 1);
+#ifdef HG_MODUP_PROF
+            const long long t_ld = clock64();
+#endif
             // WAR across proxies: the tensor core's reads of this stage precede our stores
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
             uint8_t* dst = s_a + sa_ * kAStage + (g * 16) * 128 + rr * 16;
@@ -281,6 +302,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1) modup_umma_kernel(
                 mbar_arrive(smem_u32(&bar_a_full[sa_]));
                 mbar_arrive(smem_u32(&bar_fl_full[sa_]));
             }
+#ifdef HG_MODUP_PROF
+            prof[2] += (unsigned long long)(clock64() - t_ld);
+#endif
         }
     } else {
         // ---------------- epilogue ----------------
@@ -292,7 +316,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) modup_umma_kernel(
             const uint2* corr = s_corr[op];
             uint32_t* outp = out + (size_t)op * P * N + cb + n;
             const int sa_ = ia & 1;
-            mbar_wait(smem_u32(&bar_fl_full[sa_]), (ia >> 1) & 1);
+            MWAIT(0, smem_u32(&bar_fl_full[sa_]), (ia >> 1) & 1);
             const uint32_t fl = kLoaders == 8 ? (s_flp[0][sa_][n] | s_flp[1][sa_][n]) : s_fl[sa_][n];
             __syncwarp();
             if (lane == 0) mbar_arrive(smem_u32(&bar_fl_empty[sa_]));
@@ -300,7 +324,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1) modup_umma_kernel(
             const bool ng = (fl & 2u) && (fl & 4u);
             for (int ch = 0; ch < nch; ++ch, ++ic) {
                 const int ts = ic & 1;
-                mbar_wait(smem_u32(&bar_tm_full[ts]), (ic >> 1) & 1);
+                MWAIT(1, smem_u32(&bar_tm_full[ts]), (ic >> 1) & 1);
+#ifdef HG_MODUP_PROF
+                const long long t_col = clock64();
+#endif
                 asm volatile("tcgen05.fence::after_thread_sync;\n");
                 const int jbase = ch * kPrimesChunk + h * kEpiPrimes;
                 const uint32_t lane_addr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ts * 256) +
@@ -369,15 +396,31 @@ __global__ void __launch_bounds__(kWarps * 32, 1) modup_umma_kernel(
                 asm volatile("tcgen05.fence::before_thread_sync;\n");
                 __syncwarp();
                 if (lane == 0) mbar_arrive(smem_u32(&bar_tm_empty[ts]));
+#ifdef HG_MODUP_PROF
+                prof[2] += (unsigned long long)(clock64() - t_col);
+#endif
             }
         }
     }
+#ifdef HG_MODUP_PROF
+    if (lane == 0 && blockIdx.x < 160 && warp < 24) {
+        prof[5] = (unsigned long long)(clock64() - t_start);
+        for (int k = 0; k < 8; ++k) g_modup_prof[blockIdx.x][warp][k] = prof[k];
+    }
+#endif
     asm volatile("tcgen05.fence::before_thread_sync;\n");
     __syncthreads();
     if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(512));
 }
 
 }  // namespace
+
+#ifdef HG_MODUP_PROF
+// copies the wait-cycle table of the last tcgen05 ModUp launch: [160][24][8] u64
+extern "C" int hg_modup_prof_read(unsigned long long* out) {
+    return cudaMemcpyFromSymbol(out, g_modup_prof, sizeof(g_modup_prof)) == cudaSuccess ? 0 : 1;
+}
+#endif
 
 // B images, K-chunk-major so that a W-word operand copies only its first W8/4 K chunks:
 // chunk ch = primes 64ch..64ch+63 -> 256 rows (j, r) x K = 256 bytes (64 words x 4 bytes);
