@@ -30,7 +30,7 @@ constexpr int kBChunkBytes = 256 * 4 * kWMax;   // 64 KB: 256 rows x 256 K bytes
 constexpr int kAStage = kRows * 4 * kWMax;      // 32 KB
 constexpr int kEpiGroups = 4;    // epilogue warps per TMEM lane quarter
 #ifndef HG_MODUP_LOADERS
-#define HG_MODUP_LOADERS 4   // A-loader warps: 4 (one coefficient per thread) or 8 (two threads per coefficient)
+#define HG_MODUP_LOADERS 8   // A-loader warps: 4 (one coefficient per thread) or 8 (two threads per coefficient, each gathering every other 32-word batch: both batches of a level-1550 operand in flight at once; 72 registers, no spills; ModUp 23.96 -> 22.0 ms per batch step, profiles/r2_modup_loader_ab.txt)
 #endif
 constexpr int kLoaders = HG_MODUP_LOADERS;
 constexpr int kEpiWarp0 = 2 + kLoaders;
@@ -66,7 +66,7 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 // (and in the loaders' gather / the epilogue's column loop), read back with hg_modup_prof_read:
 // [cta][warp][0..3 waits / work by role, 5 = elapsed]
 #ifdef HG_MODUP_PROF
-__device__ unsigned long long g_modup_prof[160][24][8];
+__device__ unsigned long long g_modup_prof[160][32][8];
 #define MWAIT(cat, bar, par)                                  \
     do {                                                      \
         const long long _t = clock64();                       \
@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) modup_umma_kernel(
         }
     }
 #ifdef HG_MODUP_PROF
-    if (lane == 0 && blockIdx.x < 160 && warp < 24) {
+    if (lane == 0 && blockIdx.x < 160 && warp < 32) {
         prof[5] = (unsigned long long)(clock64() - t_start);
         for (int k = 0; k < 8; ++k) g_modup_prof[blockIdx.x][warp][k] = prof[k];
     }
@@ -416,7 +416,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) modup_umma_kernel(
 }  // namespace
 
 #ifdef HG_MODUP_PROF
-// copies the wait-cycle table of the last tcgen05 ModUp launch: [160][24][8] u64
+// copies the wait-cycle table of the last tcgen05 ModUp launch: [160][32][8] u64
 extern "C" int hg_modup_prof_read(unsigned long long* out) {
     return cudaMemcpyFromSymbol(out, g_modup_prof, sizeof(g_modup_prof)) == cudaSuccess ? 0 : 1;
 }

@@ -21,15 +21,16 @@ import torch  # noqa: E402
 import paper_1902_04303_b200 as hg  # noqa: E402
 from paper_1902_04303_b200 import _lib  # noqa: E402
 
+LOADERS = int(os.environ.get("HG_MODUP_LOADERS", "8"))   # as the library was built
 ROLES = [("B TMA", [0], ["b_empty"]), ("MMA", [1], ["a_full", "b_full", "tm_empty"]),
-         ("loaders", [2, 3, 4, 5], ["a_empty", "fl_empty", "gather+store"]),
-         ("epilogue", list(range(6, 22)), ["fl_full", "tm_full", "col_loop"])]
+         ("loaders", list(range(2, 2 + LOADERS)), ["a_empty", "fl_empty", "gather+store"]),
+         ("epilogue", list(range(2 + LOADERS, 18 + LOADERS)), ["fl_full", "tm_full", "col_loop"])]
 
 
 def read(lib):
-    buf = (ctypes.c_ulonglong * (160 * 24 * 8))()
+    buf = (ctypes.c_ulonglong * (160 * 32 * 8))()
     assert lib.hg_modup_prof_read(buf) == 0
-    return np.frombuffer(buf, dtype=np.uint64).reshape(160, 24, 8).astype(np.float64)
+    return np.frombuffer(buf, dtype=np.uint64).reshape(160, 32, 8).astype(np.float64)
 
 
 def report(name, t, nsm):
