@@ -189,6 +189,10 @@ def run_ours(args, world, rank, local):
 
     from paper_1902_04303_b200.parallel import compute_setup_sharded, shard_batches
 
+    if os.environ.get("HG_BENCH_NOGC") == "1":   # diagnostic: are host stalls the cyclic collector?
+        import gc
+
+        gc.disable()
     # a process that has just exited (e.g. the test run before this bench) can still be releasing
     # its device memory: wait, bounded, until the GPU is (nearly) empty before sizing the pools
     t_wait = time.time()
@@ -268,11 +272,17 @@ def run_ours(args, world, rank, local):
         if when == "start":
             plan_setup(engine, config)   # the ring's slots come out of the planned reservation
             stream.start()
+    if hbatch is not None and stream is None:
+        # as compute_gwas_encrypted(cache=stream) does: the ring's slots and events are allocated
+        # behind the setup's last, device-bound stage; the uploads start after the setup
+        stream = SnpBatchStream([hbatch] * my_batches, params, level=m_level, slots=n_slots)
     if world > 1:   # column-split setup + NCCL all-gathers of z' partials and M_dup
         beta, p_prev, inter, m_dup = compute_setup_sharded(engine, inputs, rank, world, gather_m=False)
     else:
-        beta, p_prev, inter, m_dup = compute_setup(
-            engine, inputs, before_dup=stream.start if stream is not None and when == "dup" else None)
+        hook = None
+        if stream is not None:
+            hook = (stream.start if when == "dup" else None) if early else stream.allocate
+        beta, p_prev, inter, m_dup = compute_setup(engine, inputs, before_dup=hook)
     e_setup.record()
     if os.environ.get("HG_BENCH_DEBUG"):
         from paper_1902_04303_b200.ckks import KEY_CACHE
@@ -287,8 +297,6 @@ def run_ours(args, world, rank, local):
     marks = []
     if inter.M.cols[0].level_bits != m_level:
         raise RuntimeError(f"projector level {inter.M.cols[0].level_bits} != the streamed level {m_level}")
-    if hbatch is not None and stream is None:
-        stream = SnpBatchStream([hbatch] * my_batches, params, level=m_level, slots=n_slots)
     if stream is not None:
         for b in stream:
             read_back(compute_batch(engine, inputs, inter, m_dup, b), job_keep)
