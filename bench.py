@@ -486,10 +486,10 @@ def measure_primitives(torch, hg, _lib, log_n: int = 16, level: int = 1550, reps
 
 def ncu_traffic(dom: str):
     """DRAM bytes per unit of the dominant kernel from the committed `ncu --set full` capture
-    (profiles/r1_ncu_traffic.json): per row-pass of the contiguous NTT pass (the largest NTT
+    (profiles/r2_ncu_traffic.json): per row-pass of the contiguous NTT pass (the largest NTT
     launch), against its algorithmic read+write of 2^17 words."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r1_ncu_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r2_ncu_traffic.json")) as f:
             cap = json.load(f)
     except OSError:
         return None
@@ -497,12 +497,12 @@ def ncu_traffic(dom: str):
         return None
     for ln in cap["launches"]:
         if ln["kernel"].startswith("void ntt_lo8_kernel<1, 11, 2>"):
-            rows = int(ln["grid_size"]) // 32   # 64 chunks x 2-row blocks per prime: 32 blocks/row
+            rows = int(ln["grid_size"]) // 32   # 64 chunks per row, 2 rows per block: 32 blocks/row
             scale = {"Mbyte": 1e6, "Gbyte": 1e9, "Kbyte": 1e3}.get(ln["unit"], 1.0)
             per_row = (ln["dram_read"] + ln["dram_write"]) * scale / rows
             return {"bytes_per_row_pass": round(per_row), "algorithmic_bytes_per_row_pass": 2 * (1 << 17) * 4,
                     "ratio": round(per_row / (2 * (1 << 17) * 4), 3),
-                    "source": "profiles/r1_ncu_traffic.json (ncu --set full, ntt_lo8_kernel<1,11,2>, "
+                    "source": "profiles/r2_ncu_traffic.json (ncu --set full, ntt_lo8_kernel<1,11,2>, "
                               f"{rows} rows); the excess over 1.0 is the twiddle table"}
     return None
 
