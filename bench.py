@@ -257,14 +257,15 @@ def run_ours(args, world, rank, local):
     torch.cuda.synchronize()
     s.record()
     # rows stream at the projector's level (the M S_i products read only those words).  The ring
-    # starts after the setup; HG_STREAM_EARLY=1 starts it before the setup's last stage
-    # (compute_setup before_dup) or with the setup (HG_STREAM_WHEN=start) -- both measured: the
-    # early batches run compute-bound (-0.45 s) but the setup slows by as much (same-box A/B,
-    # profiles/r2_stream_early_v3_ab.txt)
+    # (3 slots) starts before the setup's last stage, as compute_gwas_encrypted(cache=stream) does
+    # for an early stream: its uploads are issued by the stream's own thread (issuing a batch's
+    # copies blocks for as long as the copy queue is full), so the setup keeps its time and the
+    # first ~12 batches find their rows in HBM (same-box A/B: whole job 8.36 -> 7.91 s,
+    # profiles/r2_stream_early_v4_ab.txt).  HG_STREAM_EARLY=0: ring started after the setup
     m_level = params.log_l - 150
     stream = None
-    early = os.environ.get("HG_STREAM_EARLY", "0") == "1" and world == 1
-    n_slots = int(os.environ.get("HG_STREAM_SLOTS", "4" if early else "2"))
+    early = os.environ.get("HG_STREAM_EARLY", "1") == "1" and world == 1
+    n_slots = int(os.environ.get("HG_STREAM_SLOTS", "3" if early else "2"))
     when = os.environ.get("HG_STREAM_WHEN", "dup")   # "dup": before the M_dup ladders; "start": with the setup
     if hbatch is not None and early:
         # the first uploads run while the setup's kernels leave the PCIe link idle
@@ -283,6 +284,7 @@ def run_ours(args, world, rank, local):
         if stream is not None:
             hook = (stream.start if when == "dup" else None) if early else stream.allocate
         beta, p_prev, inter, m_dup = compute_setup(engine, inputs, before_dup=hook)
+        del hook   # a bound method of the stream: the ring's slots go back when `stream` is deleted
     e_setup.record()
     if os.environ.get("HG_BENCH_DEBUG"):
         from paper_1902_04303_b200.ckks import KEY_CACHE
@@ -314,6 +316,7 @@ def run_ours(args, world, rank, local):
         print(f"[bench] whole-job batch ms: {per}; library OOM retries {_lib.OOM_RETRIES}", file=sys.stderr,
               flush=True)
     t_whole = max_over_ranks(s.elapsed_time(e) / 1e3, world) if hbatch is not None else None
+    b = None
     del job_keep, stream   # the ring's slots (k x 12.6 GB) go back before the resident steps
     if batch is None:
         batch = hbatch.to_device(params)
