@@ -313,3 +313,30 @@ def test_native_samplers_replay_cpython_random():
         assert got == want, seed
         assert a.getstate() == b.getstate()
         assert a.getrandbits(64) == b.getrandbits(64) and a.gauss(0, 1) == b.gauss(0, 1)
+
+
+def test_row_events_hand_out_only_issued_rows():
+    """gwas._RowEvents (the ready list of a streamed batch): indexing blocks until the uploader
+    thread has marked the row, and an uploader failure surfaces in the consumer."""
+    import threading
+    import time
+
+    from paper_1902_04303_b200.gwas import _RowEvents
+
+    ev = _RowEvents(["e0", "e1", "e2"])
+    assert len(ev) == 3
+    got = []
+    t = threading.Thread(target=lambda: got.append(ev[1]))
+    t.start()
+    time.sleep(0.05)
+    assert not got            # row 1 not issued yet
+    ev.mark(0)
+    time.sleep(0.05)
+    assert not got
+    ev.mark(1)
+    t.join(timeout=5)
+    assert got == ["e1"] and ev[0] == "e0"
+    bad = _RowEvents(["e0"])
+    bad.fail(RuntimeError("upload failed"))
+    with pytest.raises(RuntimeError, match="upload failed"):
+        bad[0]
