@@ -728,6 +728,10 @@ def main():
         scale = min(1.0, clk["sm_mhz"] / clk["sm_max_mhz"])
         roofline["peak_at_step_clock"] = round(roofline["peak"] * scale, 1)
         roofline["frac_at_step_clock"] = round(roofline["frac"] / scale, 4)
+        roofline["note"] = ("the probe runs the kernels' own butterfly since round 2 (3.75-3.93 T/s); round 1's "
+                            "probe carried one more ALU instruction per butterfly (3.0-3.1 T/s), against which "
+                            "the same kernels read 0.68; ncu of the contiguous passes: fma-heavy pipe 70-72% of "
+                            "elapsed cycles, first stall math_pipe_throttle (profiles/r2_v4_ncu_mult4_full.txt)")
     cpu = None
     if not args.no_cpu_baseline and world == 1:   # the contract: rank 0 at N=1 only
         cb = cpu_baseline_sample(params.log_n, params.log_l)
